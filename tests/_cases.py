@@ -1,0 +1,100 @@
+"""Shared test inputs: golden loading and tree builders (host mirror)."""
+
+import json
+import os
+
+import numpy as np
+
+from paper_2107_10987_b200 import hydro, mesh, problems
+
+GOLD = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
+EOS = hydro.EosConfig(gamma=1.4)
+
+
+def golden(name):
+    return np.load(os.path.join(GOLD, name + ".npz"))
+
+
+def random_smooth(tree, seed=0, amp=0.2, eos=EOS):
+    """Same field as the reference's tests/test_hydro_step.py:37-49."""
+    for leaf in tree.leaves():
+        sg = leaf.subgrid
+        x = sg.cell_centers(0)[:, None, None]
+        y = sg.cell_centers(1)[None, :, None]
+        z = sg.cell_centers(2)[None, None, :]
+        rho = 1.0 + amp * np.sin(np.pi * x) * np.cos(np.pi * y)
+        p = 1.0 + amp * np.cos(np.pi * z)
+        vx = amp * np.sin(np.pi * y)
+        sg.interior[:] = hydro.conserved_from_primitive(
+            rho, (vx, 0.05 * np.ones_like(rho), -0.02 * np.ones_like(rho)), p, eos)
+
+
+def state_of(tree):
+    return np.stack([lf.subgrid.interior for lf in tree.sorted_leaves()])
+
+
+def set_state(tree, arr):
+    for lf, a in zip(tree.sorted_leaves(), arr):
+        lf.subgrid.interior[:] = a
+
+
+def case_tree(name):
+    """Rebuild the tree of a golden step case, with the golden initial state."""
+    if name == "sedov_c1":
+        t = mesh.build_uniform_tree(2, 8, boundary="reflecting")
+        problems.init_sedov(problems.SedovConfig(), t, EOS)
+    elif name == "smooth_periodic":
+        t = mesh.build_uniform_tree(1, 8, boundary="periodic")
+    elif name == "smooth_reflecting":
+        t = mesh.build_uniform_tree(1, 8, boundary="reflecting")
+    elif name == "smooth_old":
+        t = mesh.build_uniform_tree(1, 8, boundary="periodic")
+    elif name == "amr_reflux":
+        t = mesh.build_uniform_tree(1, 8, boundary="periodic")
+        t.split(t.leaf_at(1, (0, 0, 0)))
+        t.reindex()
+    elif name == "sources":
+        t = mesh.build_uniform_tree(1, 8, boundary="outflow")
+    else:
+        raise KeyError(name)
+    g = golden(name)
+    if "paths" in g:
+        assert [json.loads(p) for p in g["paths"]] == [list(lf.path) for lf in t.sorted_leaves()]
+    set_state(t, g["init"])
+    return t, g
+
+
+class FixedGravity:
+    def __init__(self, fields):
+        self.fields = fields
+
+    def solve(self, tree, need_derivative=False):
+        return self.fields
+
+
+def sources_gravity(tree, g):
+    fields = {}
+    for i, lf in enumerate(tree.sorted_leaves()):
+        a = g[f"g_{i}"]
+        fields[lf.path] = dict(gx=a[0], gy=a[1], gz=a[2], dphi_dt=a[3], phi=np.zeros_like(a[0]))
+    return FixedGravity(fields)
+
+
+def bitwise_mismatch(a, b):
+    """Number of entries that differ (NaN==NaN counts as equal; +-0 equal)."""
+    a = np.asarray(a)
+    b = np.asarray(b)
+    same = (a == b) | (np.isnan(a) & np.isnan(b))
+    return int(np.size(same) - np.count_nonzero(same))
+
+
+def rel_close(x, ref, rtol=1e-12):
+    """Per-cell |x-ref| <= rtol*max(|ref|, field scale) (SURVEY.md §7 comparator)."""
+    x = np.asarray(x)
+    ref = np.asarray(ref)
+    bad = 0
+    for f in range(ref.shape[1]):
+        xs, rs = x[:, f], ref[:, f]
+        scale = max(float(np.max(np.abs(rs))), 1e-300)
+        bad += int(np.count_nonzero(np.abs(xs - rs) > rtol * np.maximum(np.abs(rs), scale)))
+    return bad
