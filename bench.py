@@ -1,0 +1,326 @@
+"""Benchmark of the B200 FP64 hydro step (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
+
+One "step" is what the reference driver does per timestep
+(``om/driver.py:165-168``): ``cfl_dt(0.4)`` then one SSP-RK3 ``rk3_step`` --
+here the CFL reduction kernels plus three launches of the fused stage kernel,
+dt kept on the device.  Workload (N=1): config c2 of BASELINE.json, Sedov-Taylor
+blast wave on a uniform 128^3 grid = 4096 sub-grids of 8^3 (level-4 octree,
+reflecting walls), synthetic initial data from ``init_sedov`` (no RNG).
+``value`` = cells x steps / device time (state resident in HBM); ``e2e`` = the
+same metric through the public drop-in API (``B200HydroStepper.cfl_dt`` +
+``rk3_step`` with host_sync) including the H2D upload and D2H download of the
+whole state every step.
+
+``--impl reference`` times the CPU oracle (C restatement of the reference's
+compiled kernels + its numpy orchestration, all host threads) on a bounded
+sample of the same workload, rank 0 only.
+"""
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "hydro cell-updates/sec (FP64) per GPU & at 1/2/4/8 B200; % of roofline"
+UNIT = "cell-updates/s"
+# algorithmic FP64 flops per cell per RK stage (non-redundant count)
+FLOPS_PER_CELL_STAGE = 4115.0
+FLOPS_PER_CELL_UPDATE = 12362.0
+# algorithmic HBM bytes per cell per stage: read cur + write next (48+48) + u0 on 2 of 3 stages
+BYTES_PER_CELL_STAGE = 48.0 + 48.0 + 48.0 * 2.0 / 3.0
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=60)
+    p.add_argument("--warmup", type=int, default=5)
+    p.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    p.add_argument("--level", type=int, default=None, help="octree level of the uniform tree (default: c2 = 4)")
+    p.add_argument("--max-run", type=int, default=4)
+    p.add_argument("--e2e-steps", type=int, default=8)
+    p.add_argument("--cpu-leaves", type=int, default=512)
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    return p.parse_args()
+
+
+def sedov_tree(level):
+    from paper_2107_10987_b200 import EosConfig, SedovConfig, build_uniform_tree, init_sedov
+
+    t = build_uniform_tree(level, 8, boundary="reflecting")
+    init_sedov(SedovConfig(), t, EosConfig(gamma=1.4))
+    return t
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return json.load(f)
+    except Exception:  # noqa: BLE001
+        return {}
+
+
+# ---------------------------------------------------------------------------
+# clocks during the timed region (B200_PROFILING.md recipe)
+# ---------------------------------------------------------------------------
+class ClockSampler:
+    def __init__(self, index):
+        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", f"--id={index}", f"--query-gpu={q}", "--format=csv,noheader,nounits",
+                                       "-lms", "100"], stdout=self.f, stderr=subprocess.DEVNULL)
+        except Exception:  # noqa: BLE001
+            self.p = None
+
+    def stop(self):
+        if self.p is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.p.terminate()
+        self.p.wait()
+        self.f.seek(0)
+        rows = [r.split(",") for r in self.f.read().strip().splitlines() if r.strip()]
+        os.unlink(self.f.name)
+        sm = [float(r[1]) for r in rows if len(r) >= 9 and r[1].strip().replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in rows if len(r) >= 9 and r[2].strip().replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = set()
+        for r in rows:
+            if len(r) < 9:
+                continue
+            for k, nm in enumerate(names):
+                if r[5 + k].strip().lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ---------------------------------------------------------------------------
+# CPU side: the oracle (test infrastructure) timed on the host cores
+# ---------------------------------------------------------------------------
+def cpu_run(level, nleaves, steps, warmup):
+    """Time OracleStepper on a contiguous (Morton) sample of leaves; returns
+    (cell-updates/s, threads, sample description)."""
+    import oracle
+    from oracle.step import OracleStepper
+
+    tree = sedov_tree(level)
+    leaves = tree.sorted_leaves()[:nleaves]
+    nthr = os.cpu_count() or 1
+    st = OracleStepper(tree, 1.4, nthreads=nthr)
+    oracle.lib()
+    times = []
+    for k in range(warmup + steps):
+        t0 = time.perf_counter()
+        dt = st.cfl_dt(0.4)  # full-tree CFL, as the reference's step does
+        st.rk3_step(dt, leaves=leaves)
+        t1 = time.perf_counter()
+        if k >= warmup:
+            times.append(t1 - t0)
+    tot = sum(times)
+    value = len(leaves) * 512 * len(times) / tot
+    sample = (f"{len(times)} x (cfl_dt over all {len(tree.leaves())} leaves + one RK3 step of the first "
+              f"{len(leaves)} Morton-ordered leaves = {len(leaves) * 512} cells), C oracle (omb_oracle.c) "
+              f"with {nthr} pthreads + numpy ghost exchange")
+    return value, nthr, sample, tot / len(times)
+
+
+def reference_arm(args, rank, world):
+    if rank != 0:
+        return
+    level = args.level if args.level is not None else 4
+    # size the per-step sample so the whole run stays within ~3 minutes
+    probe_v, nthr, _, _ = cpu_run(level, 8, 1, 0)
+    budget = 150.0 / max(1, args.steps + args.warmup)
+    nleaves = int(max(8, min(args.cpu_leaves, budget * probe_v / 512)))
+    v, nthr, sample, per = cpu_run(level, nleaves, args.steps, args.warmup)
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": per * 1e3, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic (init_sedov, no RNG)",
+            "config": {"workload": f"sedov_uniform_L{level}_n8 ({8 ** level} sub-grids of 8^3, "
+                                   f"{8 ** level * 512} cells), reflecting, cfl 0.4; CPU sample per step"},
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": nthr, "kind": "port", "sample": sample},
+            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------
+# GPU arm
+# ---------------------------------------------------------------------------
+def fp64_peak(lib, torch):
+    import ctypes
+
+    s = torch.cuda.current_stream()
+    h = ctypes.c_void_p(s.cuda_stream)
+    scratch = torch.zeros(1, dtype=torch.float64, device="cuda")
+    blocks = 148 * 8
+    iters = 4096
+    for _ in range(2):
+        lib.omb_fp64_peak(scratch.data_ptr(), blocks, iters, h)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    reps = 5
+    for _ in range(reps):
+        lib.omb_fp64_peak(scratch.data_ptr(), blocks, iters, h)
+    e1.record()
+    torch.cuda.synchronize()
+    sec = e0.elapsed_time(e1) / 1e3
+    flops = reps * blocks * 256 * 8 * iters * 2.0
+    return flops / sec / 1e12
+
+
+def gpu_arm(args, rank, world):
+    import torch
+
+    from paper_2107_10987_b200 import EosConfig, HydroMode, _lib
+    from paper_2107_10987_b200.stepper import B200HydroStepper
+
+    torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", 0)))
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+
+    level = args.level if args.level is not None else 4
+    tree = sedov_tree(level)
+    eos = EosConfig(gamma=1.4)
+    st = B200HydroStepper(tree, eos, HydroMode("new"), host_sync=False, max_run=args.max_run)
+    lib = _lib.load()
+    cells = st.batch.L * 512
+    peak64 = fp64_peak(lib, torch)
+
+    # warm-up
+    for _ in range(args.warmup):
+        st._cfl_launch(0.4)
+        st.launch_step(None)
+    torch.cuda.synchronize()
+
+    K = args.steps
+    acc_h = torch.empty((K, 6), dtype=torch.int64).pin_memory()
+    dt_h = torch.empty((K, 1), dtype=torch.float64).pin_memory()
+    ev = [[(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(3)]
+          for _ in range(K)]
+    if dist is not None:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clk = ClockSampler(torch.cuda.current_device())
+    time.sleep(0.3)
+    t_start = torch.cuda.Event(enable_timing=True)
+    t_end = torch.cuda.Event(enable_timing=True)
+    t_start.record()
+    for k in range(K):
+        st._cfl_launch(0.4)
+        st.launch_step(None, events=ev[k])
+        acc_h[k].copy_(st._acc, non_blocking=True)
+        dt_h[k].copy_(st._dt, non_blocking=True)
+    t_end.record()
+    torch.cuda.synchronize()
+    clocks = clk.stop()
+    if dist is not None:
+        dist.barrier()
+    ms = t_start.elapsed_time(t_end)
+    stage_ms = [a.elapsed_time(b) for row in ev for (a, b) in row]
+    if dist is not None:
+        t = torch.tensor([ms], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+
+    # the reference's mid-step CFL guard (step.py:132-139) on every timed step
+    amax = acc_h[:, :3].numpy().view(np.float64)
+    ratio = dt_h.numpy() * amax / st.dx_min
+    aborted = bool(np.any(ratio > 1.0))
+
+    # end-to-end through the public drop-in API (host state of record, H2D + D2H every step)
+    e2e = None
+    if args.e2e_steps > 0:
+        t2 = sedov_tree(level)
+        st2 = B200HydroStepper(t2, eos, HydroMode("new"), host_sync=True, max_run=args.max_run)
+        for _ in range(2):
+            st2.rk3_step(st2.cfl_dt(0.4))
+        torch.cuda.synchronize()
+        w0 = time.perf_counter()
+        for _ in range(args.e2e_steps):
+            dt = st2.cfl_dt(0.4)
+            st2.rk3_step(dt)
+        torch.cuda.synchronize()
+        w1 = time.perf_counter()
+        nbytes = 6 * st2.batch.L * 512 * 8
+        e2e = {"value": cells * args.e2e_steps / (w1 - w0) * world, "unit": UNIT,
+               "h2d_bytes_per_step": nbytes, "d2h_bytes_per_step": nbytes + 2 * 8 + 4 + 6 * 8,
+               "steps": args.e2e_steps, "api": "B200HydroStepper.cfl_dt + rk3_step (host_sync=True)"}
+
+    if rank != 0:
+        return
+    value = cells * K * world / (ms / 1e3)
+    mean_stage = sum(stage_ms) / len(stage_ms)
+    achieved_tf = FLOPS_PER_CELL_STAGE * cells / (mean_stage / 1e3) / 1e12
+    pk = peaks()
+    hbm_peak = pk.get("hbm_gbs", 6650.0)
+    achieved_gbs = BYTES_PER_CELL_STAGE * cells / (mean_stage / 1e3) / 1e9
+    traffic = None
+    tf = os.path.join(ROOT, "profiles", "stage_traffic.json")
+    if os.path.exists(tf):
+        with open(tf) as f:
+            traffic = json.load(f).get("bytes_per_launch")
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K, "warmup": args.warmup,
+        "ms_per_step": ms / K, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f64", "data": "synthetic (init_sedov Sedov-Taylor, no RNG)",
+        "config": {"workload": f"sedov_uniform_L{level}_n8: {st.batch.L} sub-grids of 8^3 = {cells} cells "
+                               f"({int(round(cells ** (1 / 3)))}^3), reflecting, cfl 0.4, scheme new",
+                   "step": "cfl_dt + 3 fused RK stages, dt on device",
+                   "l2": "working set (3 x 6 x cells x 8 B = %.0f MB) > 126 MB L2; no flush" % (3 * 48 * cells / 1e6),
+                   "runs": st.batch.nruns, "max_run": args.max_run, "parallelism": f"leaf-partitioned x{world}"},
+        "roofline": {"bound": "fp64", "achieved": achieved_tf, "peak": peak64, "unit": "TFLOP/s",
+                     "frac": achieved_tf / peak64, "traffic": traffic,
+                     "kernel": "k_stage (fused RK stage)", "stage_ms": mean_stage,
+                     "flops_per_launch": FLOPS_PER_CELL_STAGE * cells,
+                     "peak_source": "in-run DFMA probe (omb_fp64_peak); MEASURED_PEAKS.json has no FP64 entry",
+                     "hbm": {"achieved_gbs": achieved_gbs, "peak_gbs": hbm_peak, "frac": achieved_gbs / hbm_peak,
+                             "algorithmic_bytes_per_launch": BYTES_PER_CELL_STAGE * cells}},
+        "clocks": clocks,
+        "e2e": e2e,
+        "gpu_launches": K * 5,
+        "cfl_abort_in_timed_steps": aborted,
+    }
+    if not args.no_cpu_baseline:
+        v, nthr, sample, _ = cpu_run(level, min(args.cpu_leaves, st.batch.L), 1, 0)
+        line["cpu_baseline"] = {"value": v, "unit": UNIT, "cores": nthr, "kind": "port", "sample": sample}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+
+        if args.impl == "b200":
+            torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", 0)))
+        dist.init_process_group("nccl" if args.impl == "b200" else "gloo")
+    if args.impl == "reference":
+        reference_arm(args, rank, world)
+    else:
+        gpu_arm(args, rank, world)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,90 @@
+/*
+ * omb200.h -- C ABI of the B200 hydro-step library (libomb200.so).
+ *
+ * Plain C: device pointers, sizes and a CUDA stream handle passed as void*.
+ * No torch or Python types.  Every call is stream-ordered and asynchronous;
+ * nothing here synchronises the host.  Return value 0 = success, negative =
+ * error (message via omb_last_error()).
+ *
+ * Each entry point replaces one interface of the reference (octomini):
+ *   omb_primitives   <- kernels.primitives         pkg/src/octomini/kernels.py:36, _kernels/reference.py:30-45
+ *   omb_reconstruct  <- kernels.reconstruct        kernels.py:37, _kernels/_core.pyx:41-156
+ *   omb_fluxes       <- kernels.fluxes             kernels.py:38, _kernels/_core.pyx:223-347
+ *   omb_stage        <- HydroStepper._stage        hydro/step.py:106-144 (ghost fill -> reconstruct ->
+ *                       fluxes -> update, fused; the CFL-abort test of :132-139 is done by the
+ *                       caller on the amax this call accumulates)
+ *   omb_cfl          <- HydroStepper.cfl_dt        hydro/step.py:81-92
+ *   omb_gather       <- mesh.ghosts.fill_leaf_ghosts (same-level + physical BCs), ghosts.py:115-150
+ */
+#ifndef OMB200_H
+#define OMB200_H
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define OMB_ABI_VERSION 1
+
+/* per-leaf topology / geometry record (device array, one per leaf) */
+typedef struct {
+    int nbr[27];   /* batch index of the same-level neighbour at offset (i,j,k), index (i+1)*9+(j+1)*3+(k+1); -1 none */
+    int offmask;   /* bit 2a: the -a face is a physical wall; bit 2a+1: the +a face */
+    double ox, oy, oz;  /* first interior cell centre (SubGrid.origin) */
+    double dx, inv_dx;  /* cell width and the host-computed 1.0/dx */
+} OmbLeafInfo;
+
+/* one RK3 stage over all runs of the batch (state layout [6][fstride], leaf-major 8^3 blocks, z fastest) */
+typedef struct {
+    const double *ucur;   /* stage input, also the halo source */
+    const double *u0;     /* RK3 step-start snapshot */
+    double *unext;        /* stage output (must not alias ucur) */
+    const double *grav;   /* [4][fstride] gx,gy,gz,dphi_dt or NULL */
+    long long fstride;    /* doubles between fields (>= nleaves*512) */
+    const OmbLeafInfo *info;
+    const int *run_off;   /* [nruns+1] offsets into run_leaf */
+    const int *run_leaf;  /* leaf indices of each run, consecutive along +x at one level */
+    int nruns;
+    const double *dt;     /* device scalar */
+    double a, b;          /* stage weights (SSP_RK3_STAGES) */
+    double gamma, gm1, eta, inv_gamma, omega;   /* gm1 = gamma-1.0, inv_gamma = 1.0/gamma (host-rounded) */
+    double floor_rho, floor_tau, floor_vmax;
+    int bc;               /* 0 outflow, 1 reflecting, 2 periodic */
+    int new_mode, override_center, contact;
+    unsigned long long *amax_bits;  /* device: running max of the signal speed (bits of a non-negative double) */
+    unsigned long long *fallback;   /* device: running positivity-fallback count */
+} OmbStageDesc;
+
+typedef struct {
+    const double *u;      /* state [6][fstride] */
+    long long fstride;
+    int nleaves;
+    const double *dx;     /* [nleaves] */
+    double gamma, gm1, eta, cfl;
+    double *ratio;        /* scratch [nleaves] */
+    int *bad;             /* scratch [nleaves] */
+    double *out;          /* [2]: worst = min dx/speed, dt = cfl*worst */
+    int *bad_leaf;        /* [1]: first leaf (batch order) with a non-finite speed, -1 none */
+    double *dt_dev;       /* optional: receives dt */
+} OmbCflDesc;
+
+int omb_abi_version(void);
+const char *omb_last_error(void);
+int omb_stage_smem_bytes(void);
+
+int omb_primitives(const double *u, int m, double gamma, double eta, double *prim, void *stream);
+int omb_reconstruct(const double *prim, int m, int new_mode, int contact_on, double gamma,
+                    double *lo, double *hi, unsigned long long *fallback, void *stream);
+int omb_fluxes(const double *lo, const double *hi, int n, double gamma, int new_mode, int override_center,
+               double *fx, double *fy, double *fz, unsigned long long *amax_bits, void *stream);
+int omb_stage(const OmbStageDesc *desc, void *stream);
+int omb_cfl(const OmbCflDesc *desc, void *stream);
+/* FP64 DFMA throughput probe (roofline denominator): blocks*256*8*iters DFMAs */
+int omb_fp64_peak(double *scratch, int blocks, int iters, void *stream);
+/* padded (6,14,14,14) conserved block of one leaf as the ghost fill would produce it */
+int omb_gather(const double *u, long long fstride, const OmbLeafInfo *info, int leaf, int bc,
+               double *out, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,51 @@
+"""Loader of the in-tree CUDA library libomb200.so (include/omb200.h).
+
+There is no fallback: if the library (or a CUDA device) is missing, every
+entry point raises NativeError.  The product never imports the oracle.
+"""
+
+import ctypes
+import os
+
+from ._abi import OmbCflDesc, OmbStageDesc
+from .errors import NativeError
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+SO_PATH = os.path.join(_HERE, "libomb200.so")
+ABI_VERSION = 1
+_lib = None
+
+EXPORTS = ("omb_abi_version", "omb_last_error", "omb_stage_smem_bytes", "omb_primitives", "omb_reconstruct",
+           "omb_fluxes", "omb_stage", "omb_cfl", "omb_gather", "omb_fp64_peak")
+
+
+def load():
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(SO_PATH):
+        raise NativeError(f"{SO_PATH} is not built (run paper_2107_10987_b200/build.py or __graft_entry__.build())")
+    L = ctypes.CDLL(SO_PATH)
+    vp, i, d, ll = ctypes.c_void_p, ctypes.c_int, ctypes.c_double, ctypes.c_longlong
+    L.omb_abi_version.restype = i
+    L.omb_last_error.restype = ctypes.c_char_p
+    L.omb_stage_smem_bytes.restype = i
+    L.omb_primitives.argtypes = [vp, i, d, d, vp, vp]
+    L.omb_reconstruct.argtypes = [vp, i, i, i, d, vp, vp, vp, vp]
+    L.omb_fluxes.argtypes = [vp, vp, i, d, i, i, vp, vp, vp, vp, vp]
+    L.omb_stage.argtypes = [ctypes.POINTER(OmbStageDesc), vp]
+    L.omb_cfl.argtypes = [ctypes.POINTER(OmbCflDesc), vp]
+    L.omb_gather.argtypes = [vp, ll, vp, i, i, vp, vp]
+    L.omb_fp64_peak.argtypes = [vp, i, i, vp]
+    for fn in EXPORTS[3:]:
+        getattr(L, fn).restype = i
+    if L.omb_abi_version() != ABI_VERSION:
+        raise NativeError(f"libomb200.so ABI {L.omb_abi_version()} != {ABI_VERSION}")
+    _lib = L
+    return L
+
+
+def check(rc, what):
+    if rc != 0:
+        msg = load().omb_last_error().decode(errors="replace")
+        raise NativeError(f"{what} failed ({rc}): {msg}")

@@ -1,0 +1,127 @@
+"""Tree -> device batch: leaf order, SoA state layout, neighbour tables, runs.
+
+The B200 layout: the state of record on the device is
+``U[6][fstride]`` with leaf ``i`` (in ``tree.sorted_leaves()`` order, the
+reference's canonical order, tree.py:148-150) owning the 512 doubles at
+``i*512`` of every field, x-major / z-fastest like ``SubGrid.interior``.
+Ghost cells are never materialised: the stage kernel gathers halos straight
+from neighbour interiors through ``info[i].nbr`` (same-level neighbour per
+26-offset, from ``Octree.neighbor_ipos``/``find_leaf_region``,
+tree.py:161-195) and ``offmask`` (physical walls).
+
+Leaves are grouped into RUNS: chains of same-level leaves adjacent along +x
+that one CTA streams through as a single x-pencil, so the halo planes
+between them are computed once.  Runs are capped at ``max_run`` leaves to
+keep >= a few waves of CTAs on 148 SMs.
+"""
+
+import numpy as np
+
+from ._abi import BC_CODES, LEAF_INFO_DTYPE
+from .geometry import NFIELDS
+
+OFFS = [(i, j, k) for i in (-1, 0, 1) for j in (-1, 0, 1) for k in (-1, 0, 1)]
+
+
+class UnsupportedTree(NotImplementedError):
+    pass
+
+
+class LeafBatch:
+    def __init__(self, tree, max_run=4, leaves=None):
+        self.tree = tree
+        self.n = tree.n
+        if self.n != 8:
+            raise UnsupportedTree("the fused stage kernel is built for 8^3 sub-grids")
+        if tree.boundary not in BC_CODES:
+            raise ValueError(f"unknown boundary {tree.boundary!r}")
+        self.bc = BC_CODES[tree.boundary]
+        self.leaves = leaves if leaves is not None else tree.sorted_leaves()
+        self.L = len(self.leaves)
+        self.index = {lf.path: i for i, lf in enumerate(self.leaves)}
+        self.info = np.zeros(self.L, dtype=LEAF_INFO_DTYPE)
+        self.dx = np.empty(self.L)
+        for i, lf in enumerate(self.leaves):
+            sg = lf.subgrid
+            rec = self.info[i]
+            span = 2 ** lf.level
+            off = 0
+            for a in range(3):
+                if tree.boundary != "periodic":
+                    if lf.ipos[a] - 1 < 0:
+                        off |= 1 << (2 * a)
+                    if lf.ipos[a] + 1 >= span:
+                        off |= 1 << (2 * a + 1)
+            rec["offmask"] = off
+            nbr = np.full(27, -1, dtype=np.int32)
+            for q, o in enumerate(OFFS):
+                if o == (0, 0, 0):
+                    nbr[q] = i
+                    continue
+                pos = tree.neighbor_ipos(lf, o)
+                if pos is None:
+                    continue
+                cover = tree.find_leaf_region(lf.level, pos)
+                if cover[0][1] != "same":
+                    raise UnsupportedTree("coarse/fine neighbours (AMR) are not handled by the fused kernel yet")
+                j = self.index.get(cover[0][0].path)
+                if j is None:
+                    raise UnsupportedTree("neighbour outside the batch")
+                nbr[q] = j
+            rec["nbr"] = nbr
+            rec["ox"], rec["oy"], rec["oz"] = (float(x) for x in sg.origin)
+            rec["dx"] = sg.dx
+            rec["inv_dx"] = 1.0 / sg.dx
+            self.dx[i] = sg.dx
+        self.fstride = self.L * 512
+        self._build_runs(max_run)
+
+    def _build_runs(self, max_run):
+        xp = OFFS.index((1, 0, 0))
+        xm = OFFS.index((-1, 0, 0))
+        runs = []
+        for i, lf in enumerate(self.leaves):
+            prev = self.info[i]["nbr"][xm]
+            # a run starts where there is no same-level -x neighbour inside the domain
+            if prev >= 0 and lf.ipos[0] > 0:
+                continue
+            chain = [i]
+            while True:
+                cur = chain[-1]
+                nxt = self.info[cur]["nbr"][xp]
+                if nxt < 0 or self.leaves[cur].ipos[0] + 1 >= 2 ** self.leaves[cur].level:
+                    break
+                chain.append(int(nxt))
+            # balanced split into pieces of <= max_run
+            k = -(-len(chain) // max_run)
+            base, extra = divmod(len(chain), k)
+            s = 0
+            for p in range(k):
+                w = base + (1 if p < extra else 0)
+                runs.append(chain[s:s + w])
+                s += w
+        assert sum(len(r) for r in runs) == self.L
+        self.runs = runs
+        self.run_off = np.zeros(len(runs) + 1, dtype=np.int32)
+        self.run_off[1:] = np.cumsum([len(r) for r in runs])
+        self.run_leaf = np.array([i for r in runs for i in r], dtype=np.int32)
+        self.nruns = len(runs)
+
+    # -- host <-> packed state --------------------------------------------------
+    def pack(self, out=None):
+        U = out if out is not None else np.empty((NFIELDS, self.L, 8, 8, 8))
+        for i, lf in enumerate(self.leaves):
+            U[:, i] = lf.subgrid.interior
+        return U
+
+    def unpack(self, U):
+        for i, lf in enumerate(self.leaves):
+            lf.subgrid.interior[:] = U[:, i]
+
+    def pack_gravity(self, fields):
+        G = np.empty((4, self.L, 8, 8, 8))
+        for i, lf in enumerate(self.leaves):
+            f = fields[lf.path]
+            for k, name in enumerate(("gx", "gy", "gz", "dphi_dt")):
+                G[k, i] = np.broadcast_to(f[name], (8, 8, 8))
+        return G

@@ -1,0 +1,499 @@
+// omb_kernels.cu -- sm_100a kernels of the B200 hydro step and the C ABI
+// (include/omb200.h).  Build: see paper_2107_10987_b200/build.py
+// (nvcc -gencode arch=compute_100a,code=sm_100a -fmad=false ...).
+#include <cuda_runtime.h>
+#include <stdio.h>
+#include <string.h>
+
+#include <mutex>
+#include <string>
+
+#include "../../include/omb200.h"
+#include "omb_math.cuh"
+#include "omb_stage.cuh"
+
+using namespace omb;
+
+static_assert(sizeof(OmbLeafInfo) == sizeof(LeafInfo), "OmbLeafInfo layout");
+
+static thread_local std::string g_err;
+static int set_err(const char* what, cudaError_t e) {
+  g_err = std::string(what) + ": " + cudaGetErrorString(e);
+  return -1;
+}
+static int set_err(const std::string& what) {
+  g_err = what;
+  return -2;
+}
+#define CK(call, what)                       \
+  do {                                       \
+    cudaError_t _e = (call);                 \
+    if (_e != cudaSuccess) return set_err(what, _e); \
+  } while (0)
+
+// ---------------------------------------------------------------------------
+// face quadrature tables (geometry.py:51-123) for the per-sub-grid flux shim
+// ---------------------------------------------------------------------------
+struct FaceTable {
+  int kind[9], nrow[9], line[25], dp[25][3], flip[25];
+};
+__constant__ FaceTable c_ft[3];
+
+static void build_face_tables(FaceTable* ft) {
+  static const int D[13][3] = {{1, 0, 0}, {0, 1, 0}, {0, 0, 1}, {1, 1, 0}, {1, -1, 0}, {1, 0, 1}, {1, 0, -1},
+                               {0, 1, 1}, {0, 1, -1}, {1, 1, 1}, {1, 1, -1}, {1, -1, 1}, {1, -1, -1}};
+  const double off[3] = {0.0, -0.5, 0.5};
+  for (int a = 0; a < 3; a++) {
+    int b = a == 0 ? 1 : 0, c = a == 2 ? 1 : 2;
+    int npt = 0, nr = 0;
+    for (int kind = 0; kind < 3; kind++)  // stable sort by kind of the (tb, tc) enumeration
+      for (int ib = 0; ib < 3; ib++)
+        for (int ic = 0; ic < 3; ic++) {
+          double tb = off[ib], tc = off[ic];
+          int k = (tb != 0.0) + (tc != 0.0);
+          if (k != kind) continue;
+          ft[a].kind[npt] = kind;
+          int cnt = 0;
+          for (int l = 0; l < 13; l++) {
+            if (D[l][a] == 0 || (D[l][b] != 0) != (tb != 0.0) || (D[l][c] != 0) != (tc != 0.0)) continue;
+            double pt[3];
+            pt[a] = 0.5;
+            pt[b] = tb;
+            pt[c] = tc;
+            ft[a].line[nr] = l;
+            for (int q = 0; q < 3; q++) {
+              double p = pt[q] - 0.5 * D[l][q];
+              ft[a].dp[nr][q] = (int)(p < 0 ? p - 0.5 : p + 0.5);
+            }
+            ft[a].flip[nr] = D[l][a] < 0;
+            nr++;
+            cnt++;
+          }
+          ft[a].nrow[npt++] = cnt;
+        }
+  }
+}
+
+static std::once_flag g_init_flag;
+static int g_init_rc = 0;
+static int lib_init() {
+  std::call_once(g_init_flag, [] {
+    FaceTable ft[3];
+    build_face_tables(ft);
+    if (cudaMemcpyToSymbol(c_ft, ft, sizeof(ft)) != cudaSuccess) g_init_rc = -1;
+  });
+  if (g_init_rc) return set_err("face table upload failed");
+  return 0;
+}
+
+// ---------------------------------------------------------------------------
+// per-sub-grid shims (the reference's `kernels` module surface)
+// ---------------------------------------------------------------------------
+__global__ void k_primitives(const double* __restrict__ u, int m, double gamma, double gm1, double eta,
+                             double* __restrict__ prim) {
+  long long nc = (long long)m * m * m;
+  for (long long c = blockIdx.x * (long long)blockDim.x + threadIdx.x; c < nc; c += (long long)gridDim.x * blockDim.x) {
+    double uu[NF], w[NF];
+    for (int v = 0; v < NF; v++) uu[v] = u[v * nc + c];
+    prim_cell(uu, gamma, gm1, eta, w);
+    for (int v = 0; v < NF; v++) prim[v * nc + c] = w[v];
+  }
+}
+
+// one thread per (line, cell in [2,m-2)^3): lo/hi of 6 fields of one cell
+__global__ void k_reconstruct(const double* __restrict__ prim, int m, int nlines, int contact, double gamma,
+                              double* __restrict__ lo, double* __restrict__ hi, unsigned long long* fallback) {
+  int core = m - 4;
+  long long ncore = (long long)core * core * core;
+  long long nc = (long long)m * m * m;
+  long long total = ncore * nlines;
+  unsigned long long fb = 0;
+  for (long long it = blockIdx.x * (long long)blockDim.x + threadIdx.x; it < total;
+       it += (long long)gridDim.x * blockDim.x) {
+    int l = (int)(it / ncore);
+    long long r = it % ncore;
+    int i = 2 + (int)(r / (core * core)), j = 2 + (int)((r / core) % core), k = 2 + (int)(r % core);
+    int dx = ldx(l), dy = ldy(l), dz = ldz(l);
+    long long o[5];
+    for (int q = 0; q < 5; q++) o[q] = ((long long)(i + (q - 2) * dx) * m + (j + (q - 2) * dy)) * m + (k + (q - 2) * dz);
+    double L[NF], H[NF], rr[5], pm1 = 0, pp1 = 0;
+    for (int v = 0; v < NF; v++) {
+      double s[5];
+      for (int q = 0; q < 5; q++) s[q] = prim[v * nc + o[q]];
+      double lv = iface(s[0], s[1], s[2], s[3]);
+      double hv = iface(s[1], s[2], s[3], s[4]);
+      mono(s[2], lv, hv);
+      L[v] = lv;
+      H[v] = hv;
+      if (v == 0)
+        for (int q = 0; q < 5; q++) rr[q] = s[q];
+      if (v == 4) { pm1 = s[1]; pp1 = s[3]; }
+    }
+    if (contact) contact_steepen(rr, pm1, pp1, gamma, L[0], H[0]);
+    if (L[0] <= 0.0 || L[4] <= 0.0) {
+      fb++;
+      for (int v = 0; v < NF; v++) L[v] = prim[v * nc + o[2]];
+    }
+    if (H[0] <= 0.0 || H[4] <= 0.0) {
+      fb++;
+      for (int v = 0; v < NF; v++) H[v] = prim[v * nc + o[2]];
+    }
+    long long base = (long long)l * NF * nc + o[2];
+    for (int v = 0; v < NF; v++) {
+      lo[base + v * nc] = L[v];
+      hi[base + v * nc] = H[v];
+    }
+  }
+  if (fb) atomicAdd(fallback, fb);
+}
+
+// one thread per face: the reference's 9-point / 25-row loop verbatim
+__global__ void k_fluxes(const double* __restrict__ lo, const double* __restrict__ hi, int n, double gamma,
+                         double gm1, int new_mode, int override_center, double* fx, double* fy, double* fz,
+                         unsigned long long* amax_bits) {
+  int m = n + 6;
+  long long nc = (long long)m * m * m;
+  int nface = (n + 1) * n * n;
+  double amax = 0.0;
+  for (int it = blockIdx.x * blockDim.x + threadIdx.x; it < 3 * nface; it += gridDim.x * blockDim.x) {
+    int axis = it / nface, f = it % nface;
+    int n0 = axis == 0 ? n + 1 : n, n1 = axis == 1 ? n + 1 : n, n2 = axis == 2 ? n + 1 : n;
+    int i0 = f / (n1 * n2), i1 = (f / n2) % n1, i2 = f % n2;
+    int low[3] = {axis == 0 ? 2 + i0 : 3 + i0, axis == 1 ? 2 + i1 : 3 + i1, axis == 2 ? 2 + i2 : 3 + i2};
+    const FaceTable& T = c_ft[axis];
+    double center[NF] = {0, 0, 0, 0, 0, 0}, pd[4][NF], edev[NF] = {0, 0, 0, 0, 0, 0}, vdev[NF] = {0, 0, 0, 0, 0, 0};
+    int rr0 = 0, ei = 0, vi = 0;
+    for (int pt = 0; pt < 9; pt++) {
+      int kind = T.kind[pt], nrow = T.nrow[pt];
+      if (kind != 0 && (!new_mode || override_center)) { rr0 += nrow; continue; }
+      double acc[NF] = {0, 0, 0, 0, 0, 0}, pair[NF];
+      for (int r = 0; r < nrow; r++) {
+        int l = T.line[rr0 + r];
+        int p[3] = {low[0] + T.dp[rr0 + r][0], low[1] + T.dp[rr0 + r][1], low[2] + T.dp[rr0 + r][2]};
+        long long P = ((long long)p[0] * m + p[1]) * m + p[2];
+        long long Q = ((long long)(p[0] + ldx(l)) * m + (p[1] + ldy(l))) * m + (p[2] + ldz(l));
+        double wP[NF], wQ[NF];
+        for (int v = 0; v < NF; v++) {
+          wP[v] = hi[((long long)l * NF + v) * nc + P];
+          wQ[v] = lo[((long long)l * NF + v) * nc + Q];
+        }
+        KtState sP, sQ;
+        kt_state(wP, gamma, gm1, sP);
+        kt_state(wQ, gamma, gm1, sQ);
+        double fv[NF];
+        double sp = T.flip[rr0 + r] ? kt_axis(sQ, sP, axis, fv) : kt_axis(sP, sQ, axis, fv);
+        if (sp > amax) amax = sp;
+        if (nrow == 4) {
+          if (r == 0 || r == 2) {
+            for (int v = 0; v < NF; v++) pair[v] = fv[v];
+          } else {
+            for (int v = 0; v < NF; v++) acc[v] += pair[v] + fv[v];
+          }
+        } else {
+          for (int v = 0; v < NF; v++) acc[v] += fv[v];
+        }
+      }
+      rr0 += nrow;
+      if (kind == 0) {
+        for (int v = 0; v < NF; v++) center[v] = acc[v];
+      } else if (kind == 1) {
+        for (int v = 0; v < NF; v++) pd[ei][v] = pdev_edge(acc[v], center[v]);
+        if (++ei == 4)
+          for (int v = 0; v < NF; v++) edev[v] = (pd[0][v] + pd[1][v]) + (pd[2][v] + pd[3][v]);
+      } else {
+        for (int v = 0; v < NF; v++) pd[vi][v] = pdev_vert(acc[v], center[v]);
+        if (++vi == 4)
+          for (int v = 0; v < NF; v++) vdev[v] = (pd[0][v] + pd[1][v]) + (pd[2][v] + pd[3][v]);
+      }
+    }
+    double* F = axis == 0 ? fx : (axis == 1 ? fy : fz);
+    long long fs = (long long)n0 * n1 * n2;
+    for (int v = 0; v < NF; v++)
+      F[v * fs + f] = (new_mode && !override_center) ? face_final(center[v], edev[v], vdev[v]) : center[v];
+  }
+  if (amax > 0.0) atomicMax(amax_bits, (unsigned long long)__double_as_longlong(amax));
+}
+
+// ---------------------------------------------------------------------------
+// fused stage: one CTA per run
+// ---------------------------------------------------------------------------
+constexpr int STAGE_THREADS = 512;
+
+__device__ __forceinline__ void block_reduce(double amax, long long fb, unsigned long long* amax_bits,
+                                             unsigned long long* fallback) {
+  __shared__ double s_max[STAGE_THREADS / 32];
+  __shared__ long long s_fb[STAGE_THREADS / 32];
+  for (int o = 16; o > 0; o >>= 1) {
+    double t = __shfl_xor_sync(0xffffffffu, amax, o);
+    amax = t > amax ? t : amax;
+    fb += __shfl_xor_sync(0xffffffffu, fb, o);
+  }
+  int w = threadIdx.x >> 5;
+  if ((threadIdx.x & 31) == 0) {
+    s_max[w] = amax;
+    s_fb[w] = fb;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double m = 0.0;
+    long long f = 0;
+    for (int i = 0; i < (int)(blockDim.x >> 5); i++) {
+      m = s_max[i] > m ? s_max[i] : m;
+      f += s_fb[i];
+    }
+    if (m > 0.0) atomicMax(amax_bits, (unsigned long long)__double_as_longlong(m));
+    if (f) atomicAdd(fallback, (unsigned long long)f);
+  }
+}
+
+__global__ void __launch_bounds__(STAGE_THREADS, 1) k_stage(StageArgs A) {
+  extern __shared__ double S[];
+  const int tid = threadIdx.x, nthr = blockDim.x;
+  Stage st;
+  st.S = S;
+  st.A = &A;
+  st.run = blockIdx.x;
+  int off = A.run_off[blockIdx.x];
+  st.R = A.run_off[blockIdx.x + 1] - off;
+  st.leaves = A.run_leaf + off;
+  st.amax = 0.0;
+  st.fb = 0;
+  Hold h;
+  const int R = st.R;
+  for (int X = 0; X < 4; X++) st.load_plane(X, tid, nthr);
+  __syncthreads();
+  for (int X = 2; X < 8 * R + 4; X++) {
+    st.X = X;
+    if (X + 2 < 8 * R + 6) st.load_plane(X + 2, tid, nthr);
+    __syncthreads();
+    st.boundary_lines(0, tid, nthr, h);
+    __syncthreads();
+    st.store_hi(h);
+    if (X >= 3) st.combine_A(tid, nthr);
+    __syncthreads();
+    if (A.new_mode) {
+      st.boundary_lines(1, tid, nthr, h);
+      __syncthreads();
+      st.store_hi(h);
+      if (X >= 3 && A.quad) st.combine_B(tid, nthr);
+      __syncthreads();
+    }
+    st.inplane_lines(tid, nthr);
+    __syncthreads();
+    if (st.interior(X)) st.inplane_fluxes(tid, nthr);
+    __syncthreads();
+    if (X >= 3) st.faces_yz(tid, nthr);
+    __syncthreads();
+    if (st.interior(X - 1)) st.update_plane(tid, nthr);
+    __syncthreads();
+  }
+  block_reduce(st.amax, st.fb, A.amax_bits, A.fallback);
+}
+
+// ---------------------------------------------------------------------------
+// CFL: per-leaf speed, then a single-CTA min reduction
+// ---------------------------------------------------------------------------
+__global__ void k_cfl_leaf(const double* __restrict__ U, long long fstride, const double* __restrict__ dxs,
+                           double gamma, double gm1, double eta, double* ratio, int* bad) {
+  int leaf = blockIdx.x;
+  double best = 0.0;
+  bool nan = false, first = true;
+  for (int c = threadIdx.x; c < 512; c += blockDim.x) {
+    double u[NF];
+    for (int v = 0; v < NF; v++) u[v] = U[v * fstride + (long long)leaf * 512 + c];
+    double s = speed_cell(u, gamma, gm1, eta);
+    if (s != s) nan = true;
+    else if (first || s > best) best = s;
+    first = false;
+  }
+  __shared__ double sb[32];
+  __shared__ int sn[32];
+  for (int o = 16; o > 0; o >>= 1) {
+    double t = __shfl_xor_sync(0xffffffffu, best, o);
+    best = t > best ? t : best;
+    nan |= __shfl_xor_sync(0xffffffffu, (int)nan, o) != 0;
+  }
+  if ((threadIdx.x & 31) == 0) {
+    sb[threadIdx.x >> 5] = best;
+    sn[threadIdx.x >> 5] = nan;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double m = sb[0];
+    int anynan = 0;
+    for (int i = 0; i < (int)(blockDim.x >> 5); i++) {
+      m = sb[i] > m ? sb[i] : m;
+      anynan |= sn[i];
+    }
+    // np.max propagates NaN; np.isfinite(speed) rejects NaN and inf
+    bool finite = !anynan && m == m && m < INFINITY && m > -INFINITY;
+    bad[leaf] = finite ? 0 : 1;
+    ratio[leaf] = finite ? dxs[leaf] / m : INFINITY;
+  }
+}
+
+__global__ void k_cfl_reduce(int L, const double* ratio, const int* bad, double cfl, double* out, int* bad_leaf,
+                             double* dt_dev) {
+  __shared__ double sw[32];
+  __shared__ int sb[32];
+  double w = INFINITY;
+  int b = 0x7fffffff;
+  for (int i = threadIdx.x; i < L; i += blockDim.x) {
+    w = ratio[i] < w ? ratio[i] : w;
+    if (bad[i] && i < b) b = i;
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    double t = __shfl_xor_sync(0xffffffffu, w, o);
+    w = t < w ? t : w;
+    int tb = __shfl_xor_sync(0xffffffffu, b, o);
+    b = tb < b ? tb : b;
+  }
+  if ((threadIdx.x & 31) == 0) {
+    sw[threadIdx.x >> 5] = w;
+    sb[threadIdx.x >> 5] = b;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int i = 1; i < (int)(blockDim.x >> 5); i++) {
+      w = sw[i] < w ? sw[i] : w;
+      b = sb[i] < b ? sb[i] : b;
+    }
+    w = sw[0] < w ? sw[0] : w;
+    b = sb[0] < b ? sb[0] : b;
+    out[0] = w;
+    out[1] = cfl * w;
+    *bad_leaf = b == 0x7fffffff ? -1 : b;
+    if (dt_dev) *dt_dev = cfl * w;
+  }
+}
+
+__global__ void k_gather(const double* U, long long fstride, const LeafInfo* info, int leaf, int bc, double* out) {
+  for (int c = threadIdx.x + blockIdx.x * blockDim.x; c < M * M * M; c += blockDim.x * gridDim.x) {
+    double u[NF];
+    gather_cell(U, fstride, info[leaf], bc, c / (M * M), (c / M) % M, c % M, u);
+    for (int v = 0; v < NF; v++) out[v * M * M * M + c] = u[v];
+  }
+}
+
+// FP64 pipe peak probe (roofline denominator; MEASURED_PEAKS.json has no FP64 entry):
+// 8 independent DFMA chains per thread, 2 flops per DFMA.
+__global__ void k_dfma_peak(double* out, int iters) {
+  double a[8];
+  for (int k = 0; k < 8; k++) a[k] = 1.0 + 1e-9 * (threadIdx.x + k);
+  const double m = 0.999999999, c = 1e-12;
+  for (int i = 0; i < iters; i++) {
+#pragma unroll
+    for (int k = 0; k < 8; k++) a[k] = __fma_rn(a[k], m, c);
+  }
+  double s = 0.0;
+  for (int k = 0; k < 8; k++) s += a[k];
+  if (s == 12345.678) out[0] = s;  // keep the chains alive
+}
+
+// ---------------------------------------------------------------------------
+// C ABI
+// ---------------------------------------------------------------------------
+extern "C" {
+
+int omb_abi_version(void) { return OMB_ABI_VERSION; }
+const char* omb_last_error(void) { return g_err.c_str(); }
+int omb_stage_smem_bytes(void) { return Smem::BYTES; }
+
+int omb_primitives(const double* u, int m, double gamma, double eta, double* prim, void* stream) {
+  if (int rc = lib_init()) return rc;
+  long long nc = (long long)m * m * m;
+  int blocks = (int)((nc + 255) / 256);
+  k_primitives<<<blocks, 256, 0, (cudaStream_t)stream>>>(u, m, gamma, gamma - 1.0, eta, prim);
+  CK(cudaGetLastError(), "omb_primitives launch");
+  return 0;
+}
+
+int omb_reconstruct(const double* prim, int m, int new_mode, int contact_on, double gamma, double* lo, double* hi,
+                    unsigned long long* fallback, void* stream) {
+  if (int rc = lib_init()) return rc;
+  int nlines = new_mode ? 13 : 3;
+  long long total = (long long)(m - 4) * (m - 4) * (m - 4) * nlines;
+  int blocks = (int)((total + 255) / 256);
+  k_reconstruct<<<blocks, 256, 0, (cudaStream_t)stream>>>(prim, m, nlines, contact_on, gamma, lo, hi, fallback);
+  CK(cudaGetLastError(), "omb_reconstruct launch");
+  return 0;
+}
+
+int omb_fluxes(const double* lo, const double* hi, int n, double gamma, int new_mode, int override_center, double* fx,
+               double* fy, double* fz, unsigned long long* amax_bits, void* stream) {
+  if (int rc = lib_init()) return rc;
+  int total = 3 * (n + 1) * n * n;
+  k_fluxes<<<(total + 127) / 128, 128, 0, (cudaStream_t)stream>>>(lo, hi, n, gamma, gamma - 1.0, new_mode,
+                                                                    override_center, fx, fy, fz, amax_bits);
+  CK(cudaGetLastError(), "omb_fluxes launch");
+  return 0;
+}
+
+int omb_stage(const OmbStageDesc* d, void* stream) {
+  if (int rc = lib_init()) return rc;
+  if (d->ucur == d->unext) return set_err("omb_stage: unext must not alias ucur");
+  static bool attr_set = false;
+  if (!attr_set) {
+    CK(cudaFuncSetAttribute(k_stage, cudaFuncAttributeMaxDynamicSharedMemorySize, Smem::BYTES), "smem attribute");
+    attr_set = true;
+  }
+  StageArgs A;
+  A.ucur = d->ucur;
+  A.u0 = d->u0;
+  A.unext = d->unext;
+  A.grav = d->grav;
+  A.fstride = d->fstride;
+  A.info = (const LeafInfo*)d->info;
+  A.run_off = d->run_off;
+  A.run_leaf = d->run_leaf;
+  A.dt = d->dt;
+  A.a = d->a;
+  A.b = d->b;
+  A.gamma = d->gamma;
+  A.gm1 = d->gm1;
+  A.eta = d->eta;
+  A.inv_gamma = d->inv_gamma;
+  A.omega = d->omega;
+  A.floor_rho = d->floor_rho;
+  A.floor_tau = d->floor_tau;
+  A.floor_vmax = d->floor_vmax;
+  A.bc = d->bc;
+  A.new_mode = d->new_mode;
+  A.quad = d->new_mode && !d->override_center;
+  A.contact = d->contact;
+  A.amax_bits = d->amax_bits;
+  A.fallback = d->fallback;
+  if (d->nruns <= 0) return 0;
+  k_stage<<<d->nruns, STAGE_THREADS, Smem::BYTES, (cudaStream_t)stream>>>(A);
+  CK(cudaGetLastError(), "omb_stage launch");
+  return 0;
+}
+
+int omb_cfl(const OmbCflDesc* d, void* stream) {
+  if (int rc = lib_init()) return rc;
+  if (d->nleaves <= 0) return set_err("omb_cfl: empty batch");
+  k_cfl_leaf<<<d->nleaves, 128, 0, (cudaStream_t)stream>>>(d->u, d->fstride, d->dx, d->gamma, d->gm1, d->eta,
+                                                           d->ratio, d->bad);
+  CK(cudaGetLastError(), "omb_cfl leaf launch");
+  k_cfl_reduce<<<1, 1024, 0, (cudaStream_t)stream>>>(d->nleaves, d->ratio, d->bad, d->cfl, d->out, d->bad_leaf,
+                                                     d->dt_dev);
+  CK(cudaGetLastError(), "omb_cfl reduce launch");
+  return 0;
+}
+
+/* FP64 peak probe: launches blocks x 256 threads x 8 chains x iters DFMAs */
+int omb_fp64_peak(double* scratch, int blocks, int iters, void* stream) {
+  k_dfma_peak<<<blocks, 256, 0, (cudaStream_t)stream>>>(scratch, iters);
+  CK(cudaGetLastError(), "omb_fp64_peak launch");
+  return 0;
+}
+
+int omb_gather(const double* u, long long fstride, const OmbLeafInfo* info, int leaf, int bc, double* out,
+               void* stream) {
+  if (int rc = lib_init()) return rc;
+  k_gather<<<11, 256, 0, (cudaStream_t)stream>>>(u, fstride, (const LeafInfo*)info, leaf, bc, out);
+  CK(cudaGetLastError(), "omb_gather launch");
+  return 0;
+}
+
+}  // extern "C"

@@ -1,0 +1,473 @@
+// omb_stage.cuh -- the fused RK stage for one RUN of n=8 leaves (a run is
+// R >= 1 same-level leaves adjacent along +x, processed as one x-stream).
+//
+// One CTA per run.  The CTA streams the padded x-planes of the run through
+// shared memory and, per plane X, does what the reference does per leaf in
+// hydro/step.py:106-144:
+//
+//   P0  gather plane X+2 (interior + 3-wide halo from neighbour leaves,
+//       physical BCs applied exactly as mesh/ghosts.py:115-150) and convert
+//       to primitives (reference.py:30-45) into a 5-plane ring
+//   P1A/B  for the 9 lines with d.x = 1: PPM monotonised lo/hi on plane X
+//       (_core.pyx:61-155) and the central-upwind flux (_core.pyx:180-220)
+//       of every interface between planes X-1 and X, for every face axis
+//       that uses it -- computed ONCE (the reference evaluates each 1-4x)
+//   P2A/B  combine the point fluxes into x-face fluxes with the Simpson rule
+//       in the reference's deviation form and summation order
+//       (_core.pyx:310-346) and into boundary point values for y/z faces
+//   P3/P4  in-plane lines (1, 2, 7, 8): lo/hi and their fluxes
+//   P5  finish the y/z faces of plane X-1, start those of plane X
+//   P6  conservative update of plane X-1 + sources + dual-energy + floors
+//       (step.py:243-288)
+//
+// lo/hi and point fluxes never leave shared memory.  Every phase is a loop
+// over independent items separated by barriers; values a thread carries
+// across a barrier live in `Hold`.  The same code is compiled for the host
+// by the CPU emulation harness (tests/native), which runs each phase for
+// every thread index in turn.
+#pragma once
+#include "omb_math.cuh"
+
+namespace omb {
+
+constexpr int N = 8, M = 14, PL = M * M;  // padded plane = 196 cells
+constexpr int NP = 100;                   // lo/hi positions per plane: [2,12)^2
+constexpr int NFACEX = 64;                // x-faces per boundary: [3,11)^2
+constexpr int NYF = 72;                   // y-face slots: y in [2,10], z in [3,10]
+constexpr int NZF = 72;                   // z-face slots: y in [3,10], z in [2,10]
+constexpr int NCOR = 81;                  // corners (a,b) in [2,10]^2
+
+// lines with d.x = 1, in line order; group A = 0..4, group B = 5..8
+OMB_HD int dl_line(int dl) { return dl < 5 ? (dl == 0 ? 0 : dl + 2) : dl + 4; }
+// in-plane lines 1, 2, 7, 8
+OMB_HD int ip_line(int ip) { return ip < 2 ? ip + 1 : ip + 5; }
+
+// inclusive P ranges (y, z) of the interfaces each line contributes to faces
+// of interior cells (derived from the face tables, geometry.py:51-97)
+OMB_HD void used_range(int l, int& ylo, int& yhi, int& zlo, int& zhi) {
+  ylo = (l == 3 || l == 9 || l == 10) ? 2 : 3;
+  yhi = (l == 4 || l == 11 || l == 12) ? 11 : 10;
+  zlo = (l == 5 || l == 9 || l == 11) ? 2 : 3;
+  zhi = (l == 6 || l == 10 || l == 12) ? 11 : 10;
+}
+
+OMB_HD int pos10(int y, int z) { return (y - 2) * 10 + (z - 2); }
+OMB_HD int yslot(int y, int z) { return (y - 2) * 8 + (z - 3); }
+OMB_HD int zslot(int y, int z) { return (y - 3) * 9 + (z - 2); }
+OMB_HD int cslot(int a, int b) { return (a - 2) * 9 + (b - 2); }
+OMB_HD int xface(int y, int z) { return (y - 3) * 8 + (z - 3); }
+
+// RAW channels (point flux of one line for one axis), group A then B
+//   A: 0:(0,x) 1:(3,x) 2:(3,y) 3:(4,x) 4:(4,y) 5:(5,x) 6:(5,z) 7:(6,x) 8:(6,z)
+//   B: ch = 3*(l-9) + axis
+OMB_HD int chA(int l, int axis) {
+  switch (l) {
+    case 0: return 0;
+    case 3: return axis == 0 ? 1 : 2;
+    case 4: return axis == 0 ? 3 : 4;
+    case 5: return axis == 0 ? 5 : 6;
+    default: return axis == 0 ? 7 : 8;  // 6
+  }
+}
+OMB_HD int chB(int l, int axis) { return 3 * (l - 9) + axis; }
+
+// shared-memory layout (doubles)
+struct Smem {
+  static constexpr int PR = 0;                       // [5][6][14][14] prim ring
+  static constexpr int HI = PR + 5 * NF * PL;        // [9][6][100] hi of d.x=1 lines, previous plane
+  static constexpr int RAW = HI + 9 * NF * NP;       // union region
+  // RAW union members
+  static constexpr int RAWA = RAW;                   // [9][6][100]
+  static constexpr int RAWB = RAW;                   // [12][6][100]
+  static constexpr int LHI = RAW;                    // [4][2][6][100] in-plane lo/hi
+  static constexpr int IPCY = RAW + 4 * 2 * NF * NP; // [6][72]
+  static constexpr int IPCZ = IPCY + NF * NYF;       // [6][72]
+  static constexpr int IPR = IPCZ + NF * NZF;        // [2 lines][2 axes][6][81]
+  static constexpr int RAW_END_IP = IPR + 2 * 2 * NF * NCOR;
+  static constexpr int RAW_END_B = RAW + 12 * NF * NP;
+  static constexpr int RAW_SIZE = (RAW_END_IP > RAW_END_B ? RAW_END_IP : RAW_END_B) - RAW;
+  static constexpr int XPART = RAW + RAW_SIZE;       // [2][6][64] (C, edev)
+  static constexpr int FX = XPART + 2 * NF * NFACEX; // [2 ring][6][64]
+  static constexpr int BYE = FX + 2 * NF * NFACEX;   // [6][72]
+  static constexpr int BZE = BYE + NF * NYF;         // [6][72]
+  static constexpr int BV = BZE + NF * NZF;          // [2][6][81]
+  static constexpr int FP = BV + 2 * NF * NCOR;      // [2][4][6][72]
+  static constexpr int FYZ = FP + 2 * 4 * NF * NYF;  // [2][6][72]
+  static constexpr int TOTAL = FYZ + 2 * NF * NYF;
+  static constexpr int BYTES = TOTAL * 8;
+};
+static_assert(Smem::BYTES <= 232448, "stage shared memory exceeds 227 KB");
+
+struct LeafInfo {
+  int nbr[27];    // batch index of the same-level neighbour for each offset, -1 none
+  int offmask;    // bit 2a: -a side is a physical wall, bit 2a+1: +a side
+  double ox, oy, oz, dx, inv_dx;
+};
+
+struct StageArgs {
+  const double* ucur;   // [6][L][512] stage input (halo source)
+  const double* u0;     // [6][L][512] RK3 u0 snapshot
+  double* unext;        // [6][L][512] stage output
+  const double* grav;   // [4][L][512] gx gy gz dphi_dt or null
+  long long fstride;    // field stride in doubles (>= L*512)
+  const LeafInfo* info;
+  const int* run_off;   // [nruns+1]
+  const int* run_leaf;  // leaves of all runs, consecutive along +x
+  const double* dt;     // device scalar
+  double a, b;
+  double gamma, gm1, eta, inv_gamma, omega;
+  double floor_rho, floor_tau, floor_vmax;
+  int bc;               // 0 outflow, 1 reflecting, 2 periodic
+  int new_mode, quad, contact;  // quad = new_mode && !override
+  unsigned long long* amax_bits;  // per-stage accumulators
+  unsigned long long* fallback;
+};
+
+// conserved state of padded cell c (local coords in [0,14)^3) of a leaf, as
+// mesh/ghosts.py:115-150 fills it for same-level neighbours and physical
+// boundaries: region per axis, off-domain axes remapped (mirror for
+// reflecting walls with the normal momentum negated, clamp for outflow).
+OMB_HD void gather_cell(const double* U, long long fstride, const LeafInfo& LI, int bc, int cx, int cy, int cz,
+                        double* u) {
+  int c[3] = {cx, cy, cz};
+  int rd[3], idx[3], flipmask = 0;
+  for (int a = 0; a < 3; a++) {
+    int rr = c[a] < 3 ? -1 : (c[a] >= 3 + N ? 1 : 0);
+    bool off = rr != 0 && ((LI.offmask >> (2 * a + (rr > 0))) & 1);
+    if (off) {
+      rd[a] = 0;
+      if (bc == 1) {
+        idx[a] = rr > 0 ? (N - 1) - (c[a] - 3 - N) : 2 - c[a];
+        flipmask |= 1 << a;
+      } else {
+        idx[a] = rr > 0 ? N - 1 : 0;
+      }
+    } else {
+      rd[a] = rr;
+      idx[a] = rr > 0 ? c[a] - 3 - N : (rr < 0 ? c[a] + N - 3 : c[a] - 3);
+    }
+  }
+  int src = LI.nbr[(rd[0] + 1) * 9 + (rd[1] + 1) * 3 + (rd[2] + 1)];
+  long long base = (long long)src * 512 + (idx[0] * 64 + idx[1] * 8 + idx[2]);
+  for (int v = 0; v < NF; v++) u[v] = U[v * fstride + base];
+  for (int a = 0; a < 3; a++)
+    if ((flipmask >> a) & 1) u[1 + a] = -u[1 + a];
+}
+
+struct Hold {
+  double hi[2][NF];
+  int slot[2];
+};
+
+struct Stage {
+  double* S;
+  const StageArgs* A;
+  int run, R, X;
+  const int* leaves;
+  // thread-carried reductions
+  double amax;
+  long long fb;
+
+  OMB_HD double& sm(int off) { return S[off]; }
+  OMB_HD double* prp(int x, int v) { return S + Smem::PR + ((x % 5) * NF + v) * PL; }
+
+  OMB_HD int mult(int X) const {  // how many leaves of the run count plane X in [2,12)
+    int c = 0;
+    for (int r = 0; r < R; r++)
+      if (X >= 8 * r + 2 && X <= 8 * r + 11) c++;
+    return c;
+  }
+  OMB_HD bool interior(int X) const { return X >= 3 && X < 8 * R + 3; }
+
+  // ---- P0: gather + primitives of padded plane X into the ring -----------
+  OMB_HD void view_of(int X, int& leaf, int& lx) const {
+    int r;
+    if (X < 3) { r = 0; lx = X; }
+    else if (X >= 8 * R + 3) { r = R - 1; lx = X - 8 * (R - 1); }
+    else { r = (X - 3) >> 3; lx = 3 + ((X - 3) & 7); }
+    leaf = leaves[r];
+  }
+
+  OMB_HD void load_plane(int X, int tid, int nthr) {
+    int leaf, lx;
+    view_of(X, leaf, lx);
+    const LeafInfo& LI = A->info[leaf];
+    for (int it = tid; it < PL; it += nthr) {
+      double u[NF], w[NF];
+      gather_cell(A->ucur, A->fstride, LI, A->bc, lx, it / M, it % M, u);
+      prim_cell(u, A->gamma, A->gm1, A->eta, w);
+      for (int v = 0; v < NF; v++) prp(X, v)[it] = w[v];
+    }
+  }
+
+  // monotonised lo/hi of 6 fields at (X, y, z) along line l, with contact
+  // steepening and the positivity fallback (_core.pyx:61-155 for one cell)
+  OMB_HD void mono6(int l, int X, int y, int z, double* lo, double* hi) {
+    int dx = ldx(l), dy = ldy(l), dz = ldz(l);
+    int o[5];
+    for (int k = 0; k < 5; k++) o[k] = (y + (k - 2) * dy) * M + (z + (k - 2) * dz);
+    double rr[5] = {0, 0, 0, 0, 0}, pm1 = 0, pp1 = 0;
+    for (int v = 0; v < NF; v++) {
+      double s[5];
+      for (int k = 0; k < 5; k++) s[k] = prp(X + (k - 2) * dx, v)[o[k]];
+      double lv = iface(s[0], s[1], s[2], s[3]);
+      double hv = iface(s[1], s[2], s[3], s[4]);
+      mono(s[2], lv, hv);
+      lo[v] = lv;
+      hi[v] = hv;
+      if (v == 0)
+        for (int k = 0; k < 5; k++) rr[k] = s[k];
+      if (v == 4) { pm1 = s[1]; pp1 = s[3]; }
+    }
+    if (A->contact) contact_steepen(rr, pm1, pp1, A->gamma, lo[0], hi[0]);
+    int m = mult(X);
+    if (lo[0] <= 0.0 || lo[4] <= 0.0) {
+      fb += m;
+      for (int v = 0; v < NF; v++) lo[v] = prp(X, v)[o[2]];
+    }
+    if (hi[0] <= 0.0 || hi[4] <= 0.0) {
+      fb += m;
+      for (int v = 0; v < NF; v++) hi[v] = prp(X, v)[o[2]];
+    }
+  }
+
+  OMB_HD void kt_into(const KtState& sP, const KtState& sQ, int l, int axis, double* dst, int stride) {
+    int d = axis == 0 ? ldx(l) : (axis == 1 ? ldy(l) : ldz(l));
+    double f[NF];
+    double sp = d < 0 ? kt_axis(sQ, sP, axis, f) : kt_axis(sP, sQ, axis, f);
+    if (sp > amax) amax = sp;
+    for (int v = 0; v < NF; v++) dst[v * stride] = f[v];
+  }
+
+  // ---- P1: boundary lines (d.x = 1) of group g on plane X ----------------
+  OMB_HD void boundary_lines(int g, int tid, int nthr, Hold& h) {
+    int dl0 = g == 0 ? 0 : 5, ndl = g == 0 ? (A->new_mode ? 5 : 1) : 4;
+    int nitems = ndl * NP;
+    h.slot[0] = h.slot[1] = -1;
+    int k = 0;
+    for (int it = tid; it < nitems; it += nthr, k++) {
+      int dl = dl0 + it / NP, pos = it % NP;
+      int l = dl_line(dl);
+      int y = 2 + pos / 10, z = 2 + pos % 10;
+      double lo[NF], hi[NF];
+      mono6(l, X, y, z, lo, hi);
+      for (int v = 0; v < NF; v++) h.hi[k][v] = hi[v];
+      h.slot[k] = dl * NF * NP + pos;
+      bool kt = X >= 3 && (A->quad || l == 0);
+      if (!kt) continue;
+      int py = y - ldy(l), pz = z - ldz(l);
+      int ylo, yhi, zlo, zhi;
+      used_range(l, ylo, yhi, zlo, zhi);
+      if (py < ylo || py > yhi || pz < zlo || pz > zhi) continue;
+      int pp = pos10(py, pz);
+      double hp[NF];
+      for (int v = 0; v < NF; v++) hp[v] = S[Smem::HI + (dl * NF + v) * NP + pp];
+      KtState sP, sQ;
+      kt_state(hp, A->gamma, A->gm1, sP);
+      kt_state(lo, A->gamma, A->gm1, sQ);
+      if (g == 0) {
+        kt_into(sP, sQ, l, 0, S + Smem::RAWA + (chA(l, 0) * NF) * NP + pp, NP);
+        if (l != 0) {
+          int ax2 = (l == 3 || l == 4) ? 1 : 2;
+          kt_into(sP, sQ, l, ax2, S + Smem::RAWA + (chA(l, ax2) * NF) * NP + pp, NP);
+        }
+      } else {
+        for (int ax = 0; ax < 3; ax++) kt_into(sP, sQ, l, ax, S + Smem::RAWB + (chB(l, ax) * NF) * NP + pp, NP);
+      }
+    }
+  }
+
+  OMB_HD void store_hi(const Hold& h) {
+    for (int k = 0; k < 2; k++)
+      if (h.slot[k] >= 0)
+        for (int v = 0; v < NF; v++) S[Smem::HI + h.slot[k] + v * NP] = h.hi[k][v];
+  }
+
+  OMB_HD double rawA(int l, int ax, int v, int y, int z) { return S[Smem::RAWA + (chA(l, ax) * NF + v) * NP + pos10(y, z)]; }
+  OMB_HD double rawB(int l, int ax, int v, int y, int z) { return S[Smem::RAWB + (chB(l, ax) * NF + v) * NP + pos10(y, z)]; }
+  OMB_HD double vertex(int ax, int v, int a, int b) {
+    return vert_acc(rawB(9, ax, v, a, b), rawB(10, ax, v, a, b + 1), rawB(11, ax, v, a + 1, b),
+                    rawB(12, ax, v, a + 1, b + 1));
+  }
+
+  // ---- P2A: x-face centre + edges, boundary edge points for y/z faces -----
+  OMB_HD void combine_A(int tid, int nthr) {
+    double* FXc = S + Smem::FX + (X & 1) * NF * NFACEX;
+    int nx = NF * NFACEX;
+    int ntot = A->quad ? nx + NF * (NYF + NZF) : nx;
+    for (int it = tid; it < ntot; it += nthr) {
+      if (it < nx) {
+        int v = it / NFACEX, f = it % NFACEX, y = 3 + f / 8, z = 3 + f % 8;
+        double C = rawA(0, 0, v, y, z);
+        if (!A->quad) { FXc[v * NFACEX + f] = C; continue; }
+        double e0 = edge_acc(rawA(5, 0, v, y, z - 1), rawA(6, 0, v, y, z));
+        double e1 = edge_acc(rawA(5, 0, v, y, z), rawA(6, 0, v, y, z + 1));
+        double e2 = edge_acc(rawA(3, 0, v, y - 1, z), rawA(4, 0, v, y, z));
+        double e3 = edge_acc(rawA(3, 0, v, y, z), rawA(4, 0, v, y + 1, z));
+        double edev = (pdev_edge(e0, C) + pdev_edge(e1, C)) + (pdev_edge(e2, C) + pdev_edge(e3, C));
+        S[Smem::XPART + v * NFACEX + f] = C;
+        S[Smem::XPART + (NF + v) * NFACEX + f] = edev;
+      } else if (it < nx + NF * NYF) {
+        int j = it - nx, v = j / NYF, s = j % NYF, y = 2 + s / 8, z = 3 + s % 8;
+        S[Smem::BYE + v * NYF + s] = edge_acc(rawA(3, 1, v, y, z), rawA(4, 1, v, y + 1, z));
+      } else {
+        int j = it - nx - NF * NYF, v = j / NZF, s = j % NZF, y = 3 + s / 9, z = 2 + s % 9;
+        S[Smem::BZE + v * NZF + s] = edge_acc(rawA(5, 2, v, y, z), rawA(6, 2, v, y, z + 1));
+      }
+    }
+  }
+
+  // ---- P2B: x-face vertices -> final x flux; vertex points for y/z -------
+  OMB_HD void combine_B(int tid, int nthr) {
+    double* FXc = S + Smem::FX + (X & 1) * NF * NFACEX;
+    int nx = NF * NFACEX;
+    int ntot = nx + 2 * NF * NCOR;
+    for (int it = tid; it < ntot; it += nthr) {
+      if (it < nx) {
+        int v = it / NFACEX, f = it % NFACEX, y = 3 + f / 8, z = 3 + f % 8;
+        double C = S[Smem::XPART + v * NFACEX + f];
+        double edev = S[Smem::XPART + (NF + v) * NFACEX + f];
+        double vdev = (pdev_vert(vertex(0, v, y - 1, z - 1), C) + pdev_vert(vertex(0, v, y - 1, z), C)) +
+                      (pdev_vert(vertex(0, v, y, z - 1), C) + pdev_vert(vertex(0, v, y, z), C));
+        FXc[v * NFACEX + f] = face_final(C, edev, vdev);
+      } else {
+        int j = it - nx, ax = j / (NF * NCOR), rem = j % (NF * NCOR), v = rem / NCOR, c = rem % NCOR;
+        S[Smem::BV + (ax * NF + v) * NCOR + c] = vertex(1 + ax, v, 2 + c / 9, 2 + c % 9);
+      }
+    }
+  }
+
+  // ---- P3: in-plane lines 1, 2, 7, 8 on plane X --------------------------
+  OMB_HD void inplane_lines(int tid, int nthr) {
+    int nip = A->new_mode ? 4 : 2;
+    for (int it = tid; it < nip * NP; it += nthr) {
+      int ip = it / NP, pos = it % NP, l = ip_line(ip);
+      double lo[NF], hi[NF];
+      mono6(l, X, 2 + pos / 10, 2 + pos % 10, lo, hi);
+      for (int v = 0; v < NF; v++) {
+        S[Smem::LHI + ((ip * 2 + 0) * NF + v) * NP + pos] = lo[v];
+        S[Smem::LHI + ((ip * 2 + 1) * NF + v) * NP + pos] = hi[v];
+      }
+    }
+  }
+
+  OMB_HD void lhi_state(int ip, int side, int y, int z, KtState& s) {
+    double w[NF];
+    for (int v = 0; v < NF; v++) w[v] = S[Smem::LHI + ((ip * 2 + side) * NF + v) * NP + pos10(y, z)];
+    kt_state(w, A->gamma, A->gm1, s);
+  }
+
+  // ---- P4: in-plane fluxes (y/z face centres, y/z edge points) -----------
+  OMB_HD void inplane_fluxes(int tid, int nthr) {
+    int ntot = NYF + NZF + (A->quad ? 2 * NCOR : 0);
+    for (int it = tid; it < ntot; it += nthr) {
+      KtState sP, sQ;
+      if (it < NYF) {
+        int y = 2 + it / 8, z = 3 + it % 8;
+        lhi_state(0, 1, y, z, sP);
+        lhi_state(0, 0, y + 1, z, sQ);
+        kt_into(sP, sQ, 1, 1, S + Smem::IPCY + it, NYF);
+      } else if (it < NYF + NZF) {
+        int s = it - NYF, y = 3 + s / 9, z = 2 + s % 9;
+        lhi_state(1, 1, y, z, sP);
+        lhi_state(1, 0, y, z + 1, sQ);
+        kt_into(sP, sQ, 2, 2, S + Smem::IPCZ + s, NZF);
+      } else {
+        int j = it - NYF - NZF, li = j / NCOR, c = j % NCOR, a = 2 + c / 9, b = 2 + c % 9;
+        int l = li == 0 ? 7 : 8;
+        int ip = li == 0 ? 2 : 3;
+        int py = a, pz = li == 0 ? b : b + 1;
+        lhi_state(ip, 1, py, pz, sP);
+        lhi_state(ip, 0, py + 1, pz + ldz(l), sQ);
+        kt_into(sP, sQ, l, 1, S + Smem::IPR + ((li * 2 + 0) * NF) * NCOR + c, NCOR);
+        kt_into(sP, sQ, l, 2, S + Smem::IPR + ((li * 2 + 1) * NF) * NCOR + c, NCOR);
+      }
+    }
+  }
+
+  OMB_HD double ipr(int li, int axi, int v, int a, int b) { return S[Smem::IPR + ((li * 2 + axi) * NF + v) * NCOR + cslot(a, b)]; }
+  OMB_HD double bv(int axi, int v, int a, int b) { return S[Smem::BV + (axi * NF + v) * NCOR + cslot(a, b)]; }
+
+  // ---- P5: finish y/z faces of plane X-1, start those of plane X ---------
+  OMB_HD void faces_yz(int tid, int nthr) {
+    bool fin = interior(X - 1), start = interior(X);
+    bool q = A->quad;
+    for (int it = tid; it < NF * (NYF + NZF); it += nthr) {
+      int zf = it >= NF * NYF;
+      int j = zf ? it - NF * NYF : it;
+      int v = j / NYF, s = j % NYF;  // NYF == NZF
+      int y, z;
+      if (!zf) { y = 2 + s / 8; z = 3 + s % 8; }
+      else { y = 3 + s / 9; z = 2 + s % 9; }
+      double* fp = S + Smem::FP + (zf * 4 * NF) * NYF;
+      double edge_b = q ? S[(zf ? Smem::BZE : Smem::BYE) + v * NYF + s] : 0.0;
+      // corners of this face on the boundary plane X-1/2 (and in-plane edges)
+      int ca0, cb0, ca1, cb1;  // first / second corner (V0,V1 or V2,V3 order)
+      if (!zf) { ca0 = y; cb0 = z - 1; ca1 = y; cb1 = z; }
+      else { ca0 = y - 1; cb0 = z; ca1 = y; cb1 = z; }
+      if (fin) {
+        double C = fp[(0 * NF + v) * NYF + s];
+        double F = C;
+        if (q) {
+          double S01 = fp[(1 * NF + v) * NYF + s], pd2 = fp[(2 * NF + v) * NYF + s];
+          double T01 = fp[(3 * NF + v) * NYF + s];
+          double pd3 = pdev_edge(edge_b, C);
+          double pv2 = pdev_vert(bv(zf, v, ca0, cb0), C), pv3 = pdev_vert(bv(zf, v, ca1, cb1), C);
+          F = face_final(C, S01 + (pd2 + pd3), T01 + (pv2 + pv3));
+        }
+        S[Smem::FYZ + (zf * NF + v) * NYF + s] = F;
+      }
+      if (start) {
+        double C = S[(zf ? Smem::IPCZ : Smem::IPCY) + v * NYF + s];
+        fp[(0 * NF + v) * NYF + s] = C;
+        if (q) {
+          double e0 = edge_acc(ipr(0, zf, v, ca0, cb0), ipr(1, zf, v, ca0, cb0));
+          double e1 = edge_acc(ipr(0, zf, v, ca1, cb1), ipr(1, zf, v, ca1, cb1));
+          fp[(1 * NF + v) * NYF + s] = pdev_edge(e0, C) + pdev_edge(e1, C);
+          fp[(2 * NF + v) * NYF + s] = pdev_edge(edge_b, C);
+          fp[(3 * NF + v) * NYF + s] = pdev_vert(bv(zf, v, ca0, cb0), C) + pdev_vert(bv(zf, v, ca1, cb1), C);
+        }
+      }
+    }
+  }
+
+  // ---- P6: update the cells of plane X-1 ---------------------------------
+  OMB_HD void update_plane(int tid, int nthr) {
+    int Xc = X - 1;
+    int r = (Xc - 3) >> 3, lx = (Xc - 3) & 7;
+    int leaf = leaves[r];
+    const LeafInfo& LI = A->info[leaf];
+    const double* FXlo = S + Smem::FX + ((Xc) & 1) * NF * NFACEX;
+    const double* FXhi = S + Smem::FX + (X & 1) * NF * NFACEX;
+    UpdateParams P;
+    P.dt = *A->dt; P.a = A->a; P.b = A->b;
+    P.gamma = A->gamma; P.eta = A->eta; P.inv_gamma = A->inv_gamma; P.omega = A->omega;
+    P.floor_rho = A->floor_rho; P.floor_tau = A->floor_tau; P.floor_vmax = A->floor_vmax;
+    P.has_grav = A->grav != nullptr;
+    P.has_src = (A->omega != 0.0) || P.has_grav;
+    for (int it = tid; it < NFACEX; it += nthr) {
+      int y = 3 + it / 8, z = 3 + it % 8;
+      long long cell = (long long)leaf * 512 + lx * 64 + (y - 3) * 8 + (z - 3);
+      double u[NF], u0[NF], rr[NF], out[NF], g[4] = {0, 0, 0, 0};
+      for (int v = 0; v < NF; v++) {
+        u[v] = A->ucur[v * A->fstride + cell];
+        u0[v] = A->u0[v * A->fstride + cell];
+        double dfx = FXhi[v * NFACEX + it] - FXlo[v * NFACEX + it];
+        double dfy = S[Smem::FYZ + v * NYF + yslot(y, z)] - S[Smem::FYZ + v * NYF + yslot(y - 1, z)];
+        double dfz = S[Smem::FYZ + (NF + v) * NYF + zslot(y, z)] - S[Smem::FYZ + (NF + v) * NYF + zslot(y, z - 1)];
+        double t = 0.0 - dfx * LI.inv_dx;
+        t = t - dfy * LI.inv_dx;
+        t = t - dfz * LI.inv_dx;
+        rr[v] = t;
+      }
+      if (P.has_grav)
+        for (int k = 0; k < 4; k++) g[k] = A->grav[k * A->fstride + cell];
+      double xc = LI.ox + LI.dx * (double)lx;
+      double yc = LI.oy + LI.dx * (double)(y - 3);
+      update_cell(P, u, u0, rr, xc, yc, g, out);
+      for (int v = 0; v < NF; v++) A->unext[v * A->fstride + cell] = out[v];
+    }
+  }
+};
+
+}  // namespace omb

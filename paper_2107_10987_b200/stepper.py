@@ -1,0 +1,190 @@
+"""B200HydroStepper -- drop-in for ``octomini.hydro.HydroStepper``.
+
+Same constructor (``pkg/src/octomini/hydro/step.py:52-77``), same
+``cfl_dt(cfl) -> float`` (:81-92), ``rk3_step(dt) -> StepStats`` (:94-102)
+and ``stats`` contract, same ``NumericsError`` messages.  The step runs on
+the GPU: the octree's leaves are batched once (``batch.LeafBatch``), state
+lives in HBM as ``[6][L*512]`` float64, and each RK stage is ONE launch of
+the fused kernel (ghost gather + primitives + reconstruction + fluxes +
+quadrature + update, ``csrc/omb_stage.cuh``).
+
+Host synchronisation follows the reference's ownership model: the host
+``leaf.subgrid.interior`` arrays are the state of record.  With
+``host_sync=True`` (default) ``rk3_step`` uploads the host state (unless
+``cfl_dt`` just did), runs three stages and writes the result back into the
+leaves, exactly where the reference leaves it.  With ``host_sync=False`` the
+state stays resident on the device between calls (``download()`` /
+``upload()`` move it explicitly) -- the mode benchmarks use.
+
+The CFL-abort test of step.py:132-139 is evaluated after the three stages
+from the per-stage signal speeds the kernel accumulates; on abort the state
+is rolled back to the output of the last stage that passed, as the
+reference leaves it when it raises.
+"""
+
+import ctypes
+
+import numpy as np
+
+from . import _lib
+from ._abi import OmbCflDesc, OmbStageDesc
+from .batch import LeafBatch
+from .device import ptr, require_cuda, stream_handle, torch
+from .errors import NumericsError
+from .hydro import SSP_RK3_STAGES, FloorConfig, StepStats
+
+
+class B200HydroStepper:
+    def __init__(self, tree, eos, mode, executor=None, gravity=None, omega=0.0, floors=None, abort_courant=1.0,
+                 buffers=None, profiler=None, lane_pool=None, *, host_sync=True, max_run=4, device=None,
+                 leaves=None):
+        self.tree = tree
+        self.eos = eos
+        self.mode = mode
+        self.executor = executor  # accepted for signature parity; the GPU needs no task executor
+        self.gravity = gravity
+        self.omega = omega
+        self.floors = floors or FloorConfig()
+        self.abort_courant = abort_courant
+        self.buffers = buffers
+        self.profiler = profiler
+        self.lane_pool = lane_pool
+        self.stats = StepStats()
+        self.host_sync = host_sync
+        self.dev = require_cuda(device)
+        self.lib = _lib.load()
+        self.batch = LeafBatch(tree, max_run=max_run, leaves=leaves)
+        b = self.batch
+        T = torch
+        dev = self.dev
+        self._info = T.from_numpy(b.info.view(np.uint8).copy()).to(dev)
+        self._run_off = T.from_numpy(b.run_off.copy()).to(dev)
+        self._run_leaf = T.from_numpy(b.run_leaf.copy()).to(dev)
+        self._dx = T.from_numpy(b.dx.copy()).to(dev)
+        n = 6 * b.fstride
+        # A: state / u0, B, C: stage 1, 2 outputs, D: stage 3 output
+        self._buf = [T.empty(n, dtype=T.float64, device=dev) for _ in range(4)]
+        self._state = 0
+        self._dt = T.zeros(1, dtype=T.float64, device=dev)
+        self._acc = T.zeros(6, dtype=T.int64, device=dev)  # amax bits x3, fallback x3
+        self._cfl_ratio = T.empty(b.L, dtype=T.float64, device=dev)
+        self._cfl_bad = T.empty(b.L, dtype=T.int32, device=dev)
+        self._cfl_out = T.empty(2, dtype=T.float64, device=dev)
+        self._cfl_badleaf = T.empty(1, dtype=T.int32, device=dev)
+        self._pinned = T.empty(n, dtype=T.float64).pin_memory()
+        self._grav = None
+        self._fresh = False  # device state was just uploaded from the host by cfl_dt
+        self.dx_min = float(min(b.dx))
+        self.upload()
+
+    # -- host <-> device -------------------------------------------------------------
+    def upload(self):
+        """Copy the host leaves' interiors into the device state."""
+        b = self.batch
+        host = self._pinned.numpy().reshape(6, b.L, 8, 8, 8)
+        b.pack(out=host)
+        self._buf[self._state].copy_(self._pinned, non_blocking=True)
+
+    def download(self):
+        """Copy the device state back into the host leaves."""
+        b = self.batch
+        self._pinned.copy_(self._buf[self._state])
+        b.unpack(self._pinned.numpy().reshape(6, b.L, 8, 8, 8))
+
+    def state_tensor(self):
+        return self._buf[self._state]
+
+    # -- timestep ---------------------------------------------------------------------
+    def _cfl_launch(self, cfl, stream=None):
+        b = self.batch
+        g = self.eos.gamma
+        d = OmbCflDesc(u=ptr(self._buf[self._state]), fstride=b.fstride, nleaves=b.L, dx=ptr(self._dx),
+                       gamma=g, gm1=g - 1.0, eta=self.eos.dual_energy_eta, cfl=float(cfl),
+                       ratio=ptr(self._cfl_ratio), bad=ptr(self._cfl_bad), out=ptr(self._cfl_out),
+                       bad_leaf=ptr(self._cfl_badleaf), dt_dev=ptr(self._dt))
+        _lib.check(self.lib.omb_cfl(ctypes.byref(d), stream_handle(stream)), "omb_cfl")
+
+    def cfl_dt(self, cfl):
+        """dt = cfl * min over leaves of dx / max(max_axis|v| + c)  (step.py:81-92)."""
+        if self.host_sync:
+            self.upload()
+            self._fresh = True
+        self._cfl_launch(cfl)
+        out = self._cfl_out.cpu().numpy()
+        bad = int(self._cfl_badleaf.cpu().item())
+        if bad >= 0:
+            raise NumericsError(f"non-finite wave speed on leaf {self.batch.leaves[bad].path}")
+        return cfl * float(out[0])
+
+    # -- one step -----------------------------------------------------------------------
+    def _stage_desc(self, cur, nxt, s, a, bw):
+        b = self.batch
+        g = self.eos.gamma
+        fl = self.floors
+        acc = self._acc
+        return OmbStageDesc(
+            ucur=ptr(self._buf[cur]), u0=ptr(self._buf[self._state]), unext=ptr(self._buf[nxt]),
+            grav=ptr(self._grav), fstride=b.fstride, info=ptr(self._info), run_off=ptr(self._run_off),
+            run_leaf=ptr(self._run_leaf), nruns=b.nruns, dt=ptr(self._dt), a=a, b=bw, gamma=g, gm1=g - 1.0,
+            eta=self.eos.dual_energy_eta, inv_gamma=1.0 / g, omega=float(self.omega),
+            floor_rho=float(fl.rho), floor_tau=float(fl.tau), floor_vmax=float(fl.vmax), bc=b.bc,
+            new_mode=int(self.mode.is_new), override_center=int(self.mode.quadrature_override),
+            contact=int(self.mode.contact_detection), amax_bits=acc.data_ptr() + 8 * s,
+            fallback=acc.data_ptr() + 8 * (3 + s))
+
+    def launch_step(self, dt=None, stream=None, events=None):
+        """Enqueue the three stages (no host sync) and advance the device state.
+        dt=None uses the device dt written by the last cfl launch.  Returns
+        (buffer of the step-start state, [buffer of each stage's output])."""
+        if dt is not None:
+            self._dt.fill_(float(dt))
+        self._acc.zero_()
+        outs = []
+        cur = self._state
+        others = [i for i in range(4) if i != self._state]
+        for s, (a, bw) in enumerate(SSP_RK3_STAGES):
+            if self.gravity is not None:
+                fields = self.gravity.solve(self.tree, need_derivative=True)
+                self._grav = torch.from_numpy(self.batch.pack_gravity(fields).reshape(-1)).to(self.dev)
+            nxt = others[s]
+            d = self._stage_desc(cur, nxt, s, a, bw)
+            if events is not None:
+                events[s][0].record()
+            _lib.check(self.lib.omb_stage(ctypes.byref(d), stream_handle(stream)), "omb_stage")
+            if events is not None:
+                events[s][1].record()
+            outs.append(nxt)
+            cur = nxt
+        start = self._state
+        self._state = outs[2]
+        return start, outs
+
+    def rk3_step(self, dt):
+        """One SSP-RK3 step (step.py:94-102) on the device."""
+        if self.host_sync and not self._fresh:
+            self.upload()
+        self._fresh = False
+        start, outs = self.launch_step(dt)
+        acc = self._acc.cpu().numpy()
+        amax = acc[:3].view(np.float64)
+        fb = acc[3:]
+        L = self.batch.L
+        stats = StepStats()
+        u_prev = start
+        for s in range(3):
+            stats.kernel_launches += 2 * L  # the reference's logical count (step.py:128)
+            stats.fallback_count += int(fb[s])
+            stats.amax = max(stats.amax, float(amax[s]))
+            if dt * float(amax[s]) / self.dx_min > self.abort_courant:
+                self.stats = stats
+                self._state = u_prev
+                if self.host_sync:
+                    self.download()
+                raise NumericsError(
+                    f"CFL violation mid-step: dt*amax/dx = {dt * float(amax[s]) / self.dx_min:.3f} "
+                    f"exceeds {self.abort_courant}")
+            u_prev = outs[s]
+        self.stats = stats
+        if self.host_sync:
+            self.download()
+        return stats

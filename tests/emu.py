@@ -1,0 +1,80 @@
+"""Host emulation of the fused CUDA stage (tests/native/emu_stage.cpp) --
+runs the kernel's exact phase code under g++ to check its bookkeeping
+against the oracle on machines without a GPU.  Test harness only."""
+
+import ctypes
+import os
+import subprocess
+
+import numpy as np
+
+from paper_2107_10987_b200._abi import OmbStageDesc
+from paper_2107_10987_b200.batch import LeafBatch
+from paper_2107_10987_b200.hydro import SSP_RK3_STAGES
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(HERE)
+SO = os.path.join(HERE, "native", "_build", "libomb_emu.so")
+_lib = None
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        srcs = [os.path.join(HERE, "native", "emu_stage.cpp"),
+                os.path.join(ROOT, "paper_2107_10987_b200", "csrc", "omb_stage.cuh"),
+                os.path.join(ROOT, "paper_2107_10987_b200", "csrc", "omb_math.cuh")]
+        if not os.path.exists(SO) or os.path.getmtime(SO) < max(os.path.getmtime(s) for s in srcs):
+            os.makedirs(os.path.dirname(SO), exist_ok=True)
+            subprocess.run(["g++", "-O2", "-ffp-contract=off", "-fPIC", "-shared", "-std=c++17", "-o", SO, srcs[0]],
+                           check=True)
+        _lib = ctypes.CDLL(SO)
+        _lib.emu_stage.argtypes = [ctypes.POINTER(OmbStageDesc), ctypes.c_int]
+        _lib.emu_gather.argtypes = [ctypes.c_void_p, ctypes.c_longlong, ctypes.c_void_p, ctypes.c_int, ctypes.c_int,
+                                    ctypes.c_void_p]
+    return _lib
+
+
+def ptr(a):
+    return a.ctypes.data if a is not None else None
+
+
+class EmuStepper:
+    """rk3_step on packed host arrays through the emulated stage kernel."""
+
+    def __init__(self, tree, gamma, eta=1e-3, new_mode=True, override=False, contact=False, omega=0.0,
+                 grav=None, floors=(0.0, 0.0, 0.0), max_run=4, nthr=512):
+        self.b = LeafBatch(tree, max_run=max_run)
+        self.tree, self.gamma, self.eta = tree, gamma, eta
+        self.flags = (int(new_mode), int(override), int(contact))
+        self.omega, self.grav, self.floors, self.nthr = omega, grav, floors, nthr
+        self.run_off = np.ascontiguousarray(self.b.run_off)
+        self.run_leaf = np.ascontiguousarray(self.b.run_leaf)
+        self.amax = 0.0
+        self.fallback = 0
+
+    def rk3_step(self, dt):
+        b = self.b
+        U0 = np.ascontiguousarray(b.pack())
+        bufs = [U0, np.empty_like(U0), np.empty_like(U0), np.empty_like(U0)]
+        dtv = np.array([dt])
+        G = None if self.grav is None else np.ascontiguousarray(b.pack_gravity(self.grav))
+        self.amax, self.fallback = 0.0, 0
+        cur = 0
+        for s, (a, bb) in enumerate(SSP_RK3_STAGES):
+            am = np.zeros(1, dtype=np.uint64)
+            fb = np.zeros(1, dtype=np.uint64)
+            nxt = s + 1
+            d = OmbStageDesc(ucur=ptr(bufs[cur]), u0=ptr(U0), unext=ptr(bufs[nxt]), grav=ptr(G),
+                             fstride=b.fstride, info=ptr(b.info), run_off=ptr(self.run_off),
+                             run_leaf=ptr(self.run_leaf), nruns=b.nruns, dt=ptr(dtv), a=a, b=bb,
+                             gamma=self.gamma, gm1=self.gamma - 1.0, eta=self.eta, inv_gamma=1.0 / self.gamma,
+                             omega=self.omega, floor_rho=self.floors[0], floor_tau=self.floors[1],
+                             floor_vmax=self.floors[2], bc=b.bc, new_mode=self.flags[0],
+                             override_center=self.flags[1], contact=self.flags[2], amax_bits=ptr(am),
+                             fallback=ptr(fb))
+            lib().emu_stage(ctypes.byref(d), self.nthr)
+            self.amax = max(self.amax, float(am.view(np.float64)[0]))
+            self.fallback += int(fb[0])
+            cur = nxt
+        b.unpack(bufs[cur])

@@ -1,0 +1,77 @@
+// Host emulation of the fused stage kernel (k_stage in omb_kernels.cu).
+// TEST HARNESS: runs the exact phase functions of omb_stage.cuh under g++,
+// one simulated thread after another between the same barriers the CUDA
+// kernel uses, so the kernel's index bookkeeping can be checked against the
+// oracle without a GPU.  Never used by the product.
+#include <stdlib.h>
+#include <string.h>
+
+#include <vector>
+
+#include "../../include/omb200.h"
+#include "../../paper_2107_10987_b200/csrc/omb_stage.cuh"
+
+using namespace omb;
+
+extern "C" int emu_stage(const OmbStageDesc* d, int nthr) {
+  StageArgs A;
+  A.ucur = d->ucur; A.u0 = d->u0; A.unext = d->unext; A.grav = d->grav; A.fstride = d->fstride;
+  A.info = (const LeafInfo*)d->info; A.run_off = d->run_off; A.run_leaf = d->run_leaf; A.dt = d->dt;
+  A.a = d->a; A.b = d->b; A.gamma = d->gamma; A.gm1 = d->gm1; A.eta = d->eta; A.inv_gamma = d->inv_gamma;
+  A.omega = d->omega; A.floor_rho = d->floor_rho; A.floor_tau = d->floor_tau; A.floor_vmax = d->floor_vmax;
+  A.bc = d->bc; A.new_mode = d->new_mode; A.quad = d->new_mode && !d->override_center; A.contact = d->contact;
+  A.amax_bits = d->amax_bits; A.fallback = d->fallback;
+  std::vector<double> S(Smem::TOTAL);
+  for (int run = 0; run < d->nruns; run++) {
+    std::fill(S.begin(), S.end(), NAN);  // catch reads of never-written shared memory
+    std::vector<Stage> st(nthr);
+    std::vector<Hold> h(nthr);
+    int off = d->run_off[run];
+    for (int t = 0; t < nthr; t++) {
+      st[t].S = S.data(); st[t].A = &A; st[t].run = run;
+      st[t].R = d->run_off[run + 1] - off; st[t].leaves = d->run_leaf + off;
+      st[t].amax = 0.0; st[t].fb = 0;
+    }
+    int R = st[0].R;
+#define ALL(stmt) for (int t = 0; t < nthr; t++) { Stage& s = st[t]; (void)s; stmt; }
+    for (int X = 0; X < 4; X++) ALL(s.load_plane(X, t, nthr));
+    for (int X = 2; X < 8 * R + 4; X++) {
+      ALL(s.X = X);
+      if (X + 2 < 8 * R + 6) ALL(s.load_plane(X + 2, t, nthr));
+      ALL(s.boundary_lines(0, t, nthr, h[t]));
+      ALL(s.store_hi(h[t]); if (X >= 3) s.combine_A(t, nthr));
+      if (A.new_mode) {
+        ALL(s.boundary_lines(1, t, nthr, h[t]));
+        ALL(s.store_hi(h[t]); if (X >= 3 && A.quad) s.combine_B(t, nthr));
+      }
+      ALL(s.inplane_lines(t, nthr));
+      ALL(if (s.interior(X)) s.inplane_fluxes(t, nthr));
+      ALL(if (X >= 3) s.faces_yz(t, nthr));
+      ALL(if (s.interior(X - 1)) s.update_plane(t, nthr));
+    }
+    double m = 0.0;
+    long long f = 0;
+    for (int t = 0; t < nthr; t++) {
+      m = st[t].amax > m ? st[t].amax : m;
+      f += st[t].fb;
+    }
+    unsigned long long bits;
+    memcpy(&bits, &m, 8);
+    if (bits > *A.amax_bits) *A.amax_bits = bits;
+    *A.fallback += f;
+  }
+  return 0;
+}
+
+extern "C" int emu_gather(const double* U, long long fstride, const OmbLeafInfo* info, int leaf, int bc, double* out) {
+  for (int c = 0; c < M * M * M; c++) {
+    double u[NF];
+    gather_cell(U, fstride, ((const LeafInfo*)info)[leaf], bc, c / (M * M), (c / M) % M, c % M, u);
+    for (int v = 0; v < NF; v++) out[v * M * M * M + c] = u[v];
+  }
+  return 0;
+}
+
+extern "C" double emu_speed(const double* u6, double gamma, double gm1, double eta) {
+  return speed_cell(u6, gamma, gm1, eta);
+}

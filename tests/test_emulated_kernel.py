@@ -1,0 +1,68 @@
+"""The fused stage kernel's logic (compiled for the host, tests/native) against
+the golden fixtures made by the reference -- CPU only, no GPU needed."""
+
+import numpy as np
+import pytest
+
+from _cases import bitwise_mismatch, case_tree, golden, sources_gravity, state_of
+from emu import EmuStepper, lib
+
+import oracle
+from oracle.step import OracleStepper
+
+
+@pytest.mark.parametrize("name", ["smooth_periodic", "smooth_reflecting"])
+@pytest.mark.parametrize("max_run", [1, 2])
+def test_emulated_step_matches_golden(name, max_run):
+    t, g = case_tree(name)
+    dt = float(g["dts"][0])
+    em = EmuStepper(t, 1.4, max_run=max_run)
+    em.rk3_step(dt)
+    got = state_of(t)
+    assert bitwise_mismatch(got[:, :5], g["state1"][:, :5]) == 0
+    assert bitwise_mismatch(got, g["state1"]) == 0
+    assert em.amax == float(g["amax"][0])
+    assert em.fallback == int(g["fallback"][0])
+
+
+def test_emulated_old_scheme():
+    t, g = case_tree("smooth_old")
+    em = EmuStepper(t, 1.4, new_mode=False)
+    em.rk3_step(float(g["dts"][0]))
+    assert bitwise_mismatch(state_of(t), g["state1"]) == 0
+    assert em.amax == float(g["amax"][0])
+
+
+def test_emulated_sedov_c1():
+    t, g = case_tree("sedov_c1")
+    em = EmuStepper(t, 1.4, max_run=4)
+    em.rk3_step(float(g["dts"][0]))
+    assert bitwise_mismatch(state_of(t), g["state1"]) == 0
+    assert em.amax == float(g["amax"][0])
+
+
+def test_emulated_sources_and_floors():
+    t, g = case_tree("sources")
+    grav = sources_gravity(t, g)
+    fl = tuple(float(x) for x in g["floors"])
+    em = EmuStepper(t, float(g["gamma"]), omega=float(g["omega"]), grav=grav.fields, floors=fl)
+    em.rk3_step(float(g["dts"][0]))
+    assert bitwise_mismatch(state_of(t), g["state1"]) == 0
+
+
+def test_emulated_gather_matches_ghost_golden():
+    import ctypes
+    from paper_2107_10987_b200 import mesh
+    from paper_2107_10987_b200.batch import LeafBatch
+
+    g = golden("ghosts")
+    for bnd in ("periodic", "reflecting", "outflow"):
+        t = mesh.build_uniform_tree(1, 8, boundary=bnd)
+        for lf, u in zip(t.sorted_leaves(), g[bnd]):
+            lf.subgrid.interior[:] = u[:, 3:11, 3:11, 3:11]
+        b = LeafBatch(t)
+        U = np.ascontiguousarray(b.pack())
+        for i in range(b.L):
+            out = np.empty((6, 14, 14, 14))
+            lib().emu_gather(U.ctypes.data, b.fstride, b.info.ctypes.data, i, b.bc, out.ctypes.data)
+            assert bitwise_mismatch(out, g[bnd][i]) == 0, (bnd, i)
