@@ -251,7 +251,7 @@ __global__ void __launch_bounds__(STAGE_THREADS, 1) k_stage(StageArgs A) {
   const int tid = threadIdx.x, nthr = blockDim.x;
   Stage st;
   st.S = S;
-  st.A = &A;
+  st.A = A;
   st.run = blockIdx.x;
   int off = A.run_off[blockIdx.x];
   st.R = A.run_off[blockIdx.x + 1] - off;
@@ -263,7 +263,7 @@ __global__ void __launch_bounds__(STAGE_THREADS, 1) k_stage(StageArgs A) {
   for (int X = 0; X < 4; X++) st.load_plane(X, tid, nthr);
   __syncthreads();
   for (int X = 2; X < 8 * R + 4; X++) {
-    st.X = X;
+    st.set_plane(X);
     if (X + 2 < 8 * R + 6) st.load_plane(X + 2, tid, nthr);
     __syncthreads();
     st.boundary_lines(0, tid, nthr, h);

@@ -147,17 +147,20 @@ OMB_HD void kt_state(const double* w, double gamma, double gm1, KtState& s) {
 // flux through an `axis` face from left state L to right state R; returns
 // the signal speed max(a+, -a-).  out: 6 conserved-flux components.
 OMB_HD double kt_axis(const KtState& L, const KtState& R, int axis, double* out) {
-  double vnl = L.v[axis], vnr = R.v[axis];
+  // axis is selected with compares (no dynamic register-array indexing,
+  // which would push the states to local memory)
+  double vnl = axis == 0 ? L.v[0] : (axis == 1 ? L.v[1] : L.v[2]);
+  double vnr = axis == 0 ? R.v[0] : (axis == 1 ? R.v[1] : R.v[2]);
   double ap = dmax(0.0, dmax(vnl + L.c, vnr + R.c));
   double am = dmin(0.0, dmin(vnl - L.c, vnr - R.c));
   double fl[NF], fr[NF];
 #pragma unroll
   for (int v = 0; v < NF; v++) {
-    fl[v] = L.u[v] * vnl;
-    fr[v] = R.u[v] * vnr;
+    double tl = L.u[v] * vnl, tr = R.u[v] * vnr;
+    bool nrm = (v == 1 + axis);  // normal momentum picks up the pressure
+    fl[v] = nrm ? tl + L.p : tl;
+    fr[v] = nrm ? tr + R.p : tr;
   }
-  fl[1 + axis] += L.p;
-  fr[1 + axis] += R.p;
   fl[4] += L.p * vnl;
   fr[4] += R.p * vnr;
   double denom = ap - am;

@@ -131,6 +131,7 @@ OMB_HD void gather_cell(const double* U, long long fstride, const LeafInfo& LI, 
                         double* u) {
   int c[3] = {cx, cy, cz};
   int rd[3], idx[3], flipmask = 0;
+#pragma unroll
   for (int a = 0; a < 3; a++) {
     int rr = c[a] < 3 ? -1 : (c[a] >= 3 + N ? 1 : 0);
     bool off = rr != 0 && ((LI.offmask >> (2 * a + (rr > 0))) & 1);
@@ -149,20 +150,25 @@ OMB_HD void gather_cell(const double* U, long long fstride, const LeafInfo& LI, 
   }
   int src = LI.nbr[(rd[0] + 1) * 9 + (rd[1] + 1) * 3 + (rd[2] + 1)];
   long long base = (long long)src * 512 + (idx[0] * 64 + idx[1] * 8 + idx[2]);
+#pragma unroll
   for (int v = 0; v < NF; v++) u[v] = U[v * fstride + base];
+#pragma unroll
   for (int a = 0; a < 3; a++)
     if ((flipmask >> a) & 1) u[1 + a] = -u[1 + a];
 }
 
+// values a thread carries across the barrier after P1 (one item per thread:
+// the kernel runs >= 512 threads and P1 has <= 500 items)
 struct Hold {
-  double hi[2][NF];
-  int slot[2];
+  double hi[NF];
+  int slot;
 };
 
 struct Stage {
   double* S;
-  const StageArgs* A;
+  StageArgs A;
   int run, R, X;
+  int ring[5];  // shared-memory offsets of planes X-2 .. X+2 in the prim ring
   const int* leaves;
   // thread-carried reductions
   double amax;
@@ -170,6 +176,12 @@ struct Stage {
 
   OMB_HD double& sm(int off) { return S[off]; }
   OMB_HD double* prp(int x, int v) { return S + Smem::PR + ((x % 5) * NF + v) * PL; }
+  OMB_HD void set_plane(int x) {
+    X = x;
+#pragma unroll
+    for (int k = 0; k < 5; k++) ring[k] = Smem::PR + (((x + 3 + k) % 5) * NF) * PL;  // (x-2+k) mod 5
+  }
+  OMB_HD const double* ringp(int k, int v) const { return S + ring[k] + v * PL; }
 
   OMB_HD int mult(int X) const {  // how many leaves of the run count plane X in [2,12)
     int c = 0;
@@ -191,11 +203,12 @@ struct Stage {
   OMB_HD void load_plane(int X, int tid, int nthr) {
     int leaf, lx;
     view_of(X, leaf, lx);
-    const LeafInfo& LI = A->info[leaf];
+    const LeafInfo& LI = A.info[leaf];
     for (int it = tid; it < PL; it += nthr) {
       double u[NF], w[NF];
-      gather_cell(A->ucur, A->fstride, LI, A->bc, lx, it / M, it % M, u);
-      prim_cell(u, A->gamma, A->gm1, A->eta, w);
+      gather_cell(A.ucur, A.fstride, LI, A.bc, lx, it / M, it % M, u);
+      prim_cell(u, A.gamma, A.gm1, A.eta, w);
+#pragma unroll
       for (int v = 0; v < NF; v++) prp(X, v)[it] = w[v];
     }
   }
@@ -205,29 +218,34 @@ struct Stage {
   OMB_HD void mono6(int l, int X, int y, int z, double* lo, double* hi) {
     int dx = ldx(l), dy = ldy(l), dz = ldz(l);
     int o[5];
+#pragma unroll
     for (int k = 0; k < 5; k++) o[k] = (y + (k - 2) * dy) * M + (z + (k - 2) * dz);
     double rr[5] = {0, 0, 0, 0, 0}, pm1 = 0, pp1 = 0;
+#pragma unroll
     for (int v = 0; v < NF; v++) {
       double s[5];
-      for (int k = 0; k < 5; k++) s[k] = prp(X + (k - 2) * dx, v)[o[k]];
+#pragma unroll
+      for (int k = 0; k < 5; k++) s[k] = S[(dx ? ring[k] : ring[2]) + v * PL + o[k]];
       double lv = iface(s[0], s[1], s[2], s[3]);
       double hv = iface(s[1], s[2], s[3], s[4]);
       mono(s[2], lv, hv);
       lo[v] = lv;
       hi[v] = hv;
       if (v == 0)
+#pragma unroll
         for (int k = 0; k < 5; k++) rr[k] = s[k];
       if (v == 4) { pm1 = s[1]; pp1 = s[3]; }
     }
-    if (A->contact) contact_steepen(rr, pm1, pp1, A->gamma, lo[0], hi[0]);
-    int m = mult(X);
+    if (A.contact) contact_steepen(rr, pm1, pp1, A.gamma, lo[0], hi[0]);
     if (lo[0] <= 0.0 || lo[4] <= 0.0) {
-      fb += m;
-      for (int v = 0; v < NF; v++) lo[v] = prp(X, v)[o[2]];
+      fb += mult(X);
+#pragma unroll
+      for (int v = 0; v < NF; v++) lo[v] = ringp(2, v)[o[2]];
     }
     if (hi[0] <= 0.0 || hi[4] <= 0.0) {
-      fb += m;
-      for (int v = 0; v < NF; v++) hi[v] = prp(X, v)[o[2]];
+      fb += mult(X);
+#pragma unroll
+      for (int v = 0; v < NF; v++) hi[v] = ringp(2, v)[o[2]];
     }
   }
 
@@ -236,24 +254,25 @@ struct Stage {
     double f[NF];
     double sp = d < 0 ? kt_axis(sQ, sP, axis, f) : kt_axis(sP, sQ, axis, f);
     if (sp > amax) amax = sp;
+#pragma unroll
     for (int v = 0; v < NF; v++) dst[v * stride] = f[v];
   }
 
   // ---- P1: boundary lines (d.x = 1) of group g on plane X ----------------
   OMB_HD void boundary_lines(int g, int tid, int nthr, Hold& h) {
-    int dl0 = g == 0 ? 0 : 5, ndl = g == 0 ? (A->new_mode ? 5 : 1) : 4;
+    int dl0 = g == 0 ? 0 : 5, ndl = g == 0 ? (A.new_mode ? 5 : 1) : 4;
     int nitems = ndl * NP;
-    h.slot[0] = h.slot[1] = -1;
-    int k = 0;
-    for (int it = tid; it < nitems; it += nthr, k++) {
+    h.slot = -1;
+    for (int it = tid; it < nitems; it += nthr) {
       int dl = dl0 + it / NP, pos = it % NP;
       int l = dl_line(dl);
       int y = 2 + pos / 10, z = 2 + pos % 10;
       double lo[NF], hi[NF];
       mono6(l, X, y, z, lo, hi);
-      for (int v = 0; v < NF; v++) h.hi[k][v] = hi[v];
-      h.slot[k] = dl * NF * NP + pos;
-      bool kt = X >= 3 && (A->quad || l == 0);
+#pragma unroll
+      for (int v = 0; v < NF; v++) h.hi[v] = hi[v];
+      h.slot = dl * NF * NP + pos;
+      bool kt = X >= 3 && (A.quad || l == 0);
       if (!kt) continue;
       int py = y - ldy(l), pz = z - ldz(l);
       int ylo, yhi, zlo, zhi;
@@ -261,10 +280,11 @@ struct Stage {
       if (py < ylo || py > yhi || pz < zlo || pz > zhi) continue;
       int pp = pos10(py, pz);
       double hp[NF];
+#pragma unroll
       for (int v = 0; v < NF; v++) hp[v] = S[Smem::HI + (dl * NF + v) * NP + pp];
       KtState sP, sQ;
-      kt_state(hp, A->gamma, A->gm1, sP);
-      kt_state(lo, A->gamma, A->gm1, sQ);
+      kt_state(hp, A.gamma, A.gm1, sP);
+      kt_state(lo, A.gamma, A.gm1, sQ);
       if (g == 0) {
         kt_into(sP, sQ, l, 0, S + Smem::RAWA + (chA(l, 0) * NF) * NP + pp, NP);
         if (l != 0) {
@@ -278,9 +298,10 @@ struct Stage {
   }
 
   OMB_HD void store_hi(const Hold& h) {
-    for (int k = 0; k < 2; k++)
-      if (h.slot[k] >= 0)
-        for (int v = 0; v < NF; v++) S[Smem::HI + h.slot[k] + v * NP] = h.hi[k][v];
+    if (h.slot >= 0) {
+#pragma unroll
+      for (int v = 0; v < NF; v++) S[Smem::HI + h.slot + v * NP] = h.hi[v];
+    }
   }
 
   OMB_HD double rawA(int l, int ax, int v, int y, int z) { return S[Smem::RAWA + (chA(l, ax) * NF + v) * NP + pos10(y, z)]; }
@@ -294,12 +315,12 @@ struct Stage {
   OMB_HD void combine_A(int tid, int nthr) {
     double* FXc = S + Smem::FX + (X & 1) * NF * NFACEX;
     int nx = NF * NFACEX;
-    int ntot = A->quad ? nx + NF * (NYF + NZF) : nx;
+    int ntot = A.quad ? nx + NF * (NYF + NZF) : nx;
     for (int it = tid; it < ntot; it += nthr) {
       if (it < nx) {
         int v = it / NFACEX, f = it % NFACEX, y = 3 + f / 8, z = 3 + f % 8;
         double C = rawA(0, 0, v, y, z);
-        if (!A->quad) { FXc[v * NFACEX + f] = C; continue; }
+        if (!A.quad) { FXc[v * NFACEX + f] = C; continue; }
         double e0 = edge_acc(rawA(5, 0, v, y, z - 1), rawA(6, 0, v, y, z));
         double e1 = edge_acc(rawA(5, 0, v, y, z), rawA(6, 0, v, y, z + 1));
         double e2 = edge_acc(rawA(3, 0, v, y - 1, z), rawA(4, 0, v, y, z));
@@ -339,11 +360,12 @@ struct Stage {
 
   // ---- P3: in-plane lines 1, 2, 7, 8 on plane X --------------------------
   OMB_HD void inplane_lines(int tid, int nthr) {
-    int nip = A->new_mode ? 4 : 2;
+    int nip = A.new_mode ? 4 : 2;
     for (int it = tid; it < nip * NP; it += nthr) {
       int ip = it / NP, pos = it % NP, l = ip_line(ip);
       double lo[NF], hi[NF];
       mono6(l, X, 2 + pos / 10, 2 + pos % 10, lo, hi);
+#pragma unroll
       for (int v = 0; v < NF; v++) {
         S[Smem::LHI + ((ip * 2 + 0) * NF + v) * NP + pos] = lo[v];
         S[Smem::LHI + ((ip * 2 + 1) * NF + v) * NP + pos] = hi[v];
@@ -353,13 +375,14 @@ struct Stage {
 
   OMB_HD void lhi_state(int ip, int side, int y, int z, KtState& s) {
     double w[NF];
+#pragma unroll
     for (int v = 0; v < NF; v++) w[v] = S[Smem::LHI + ((ip * 2 + side) * NF + v) * NP + pos10(y, z)];
-    kt_state(w, A->gamma, A->gm1, s);
+    kt_state(w, A.gamma, A.gm1, s);
   }
 
   // ---- P4: in-plane fluxes (y/z face centres, y/z edge points) -----------
   OMB_HD void inplane_fluxes(int tid, int nthr) {
-    int ntot = NYF + NZF + (A->quad ? 2 * NCOR : 0);
+    int ntot = NYF + NZF + (A.quad ? 2 * NCOR : 0);
     for (int it = tid; it < ntot; it += nthr) {
       KtState sP, sQ;
       if (it < NYF) {
@@ -391,7 +414,7 @@ struct Stage {
   // ---- P5: finish y/z faces of plane X-1, start those of plane X ---------
   OMB_HD void faces_yz(int tid, int nthr) {
     bool fin = interior(X - 1), start = interior(X);
-    bool q = A->quad;
+    bool q = A.quad;
     for (int it = tid; it < NF * (NYF + NZF); it += nthr) {
       int zf = it >= NF * NYF;
       int j = zf ? it - NF * NYF : it;
@@ -436,22 +459,23 @@ struct Stage {
     int Xc = X - 1;
     int r = (Xc - 3) >> 3, lx = (Xc - 3) & 7;
     int leaf = leaves[r];
-    const LeafInfo& LI = A->info[leaf];
+    const LeafInfo& LI = A.info[leaf];
     const double* FXlo = S + Smem::FX + ((Xc) & 1) * NF * NFACEX;
     const double* FXhi = S + Smem::FX + (X & 1) * NF * NFACEX;
     UpdateParams P;
-    P.dt = *A->dt; P.a = A->a; P.b = A->b;
-    P.gamma = A->gamma; P.eta = A->eta; P.inv_gamma = A->inv_gamma; P.omega = A->omega;
-    P.floor_rho = A->floor_rho; P.floor_tau = A->floor_tau; P.floor_vmax = A->floor_vmax;
-    P.has_grav = A->grav != nullptr;
-    P.has_src = (A->omega != 0.0) || P.has_grav;
+    P.dt = *A.dt; P.a = A.a; P.b = A.b;
+    P.gamma = A.gamma; P.eta = A.eta; P.inv_gamma = A.inv_gamma; P.omega = A.omega;
+    P.floor_rho = A.floor_rho; P.floor_tau = A.floor_tau; P.floor_vmax = A.floor_vmax;
+    P.has_grav = A.grav != nullptr;
+    P.has_src = (A.omega != 0.0) || P.has_grav;
     for (int it = tid; it < NFACEX; it += nthr) {
       int y = 3 + it / 8, z = 3 + it % 8;
       long long cell = (long long)leaf * 512 + lx * 64 + (y - 3) * 8 + (z - 3);
       double u[NF], u0[NF], rr[NF], out[NF], g[4] = {0, 0, 0, 0};
+#pragma unroll
       for (int v = 0; v < NF; v++) {
-        u[v] = A->ucur[v * A->fstride + cell];
-        u0[v] = A->u0[v * A->fstride + cell];
+        u[v] = A.ucur[v * A.fstride + cell];
+        u0[v] = A.u0[v * A.fstride + cell];
         double dfx = FXhi[v * NFACEX + it] - FXlo[v * NFACEX + it];
         double dfy = S[Smem::FYZ + v * NYF + yslot(y, z)] - S[Smem::FYZ + v * NYF + yslot(y - 1, z)];
         double dfz = S[Smem::FYZ + (NF + v) * NYF + zslot(y, z)] - S[Smem::FYZ + (NF + v) * NYF + zslot(y, z - 1)];
@@ -461,11 +485,13 @@ struct Stage {
         rr[v] = t;
       }
       if (P.has_grav)
-        for (int k = 0; k < 4; k++) g[k] = A->grav[k * A->fstride + cell];
+#pragma unroll
+        for (int k = 0; k < 4; k++) g[k] = A.grav[k * A.fstride + cell];
       double xc = LI.ox + LI.dx * (double)lx;
       double yc = LI.oy + LI.dx * (double)(y - 3);
       update_cell(P, u, u0, rr, xc, yc, g, out);
-      for (int v = 0; v < NF; v++) A->unext[v * A->fstride + cell] = out[v];
+#pragma unroll
+      for (int v = 0; v < NF; v++) A.unext[v * A.fstride + cell] = out[v];
     }
   }
 };

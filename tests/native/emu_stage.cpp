@@ -28,7 +28,7 @@ extern "C" int emu_stage(const OmbStageDesc* d, int nthr) {
     std::vector<Hold> h(nthr);
     int off = d->run_off[run];
     for (int t = 0; t < nthr; t++) {
-      st[t].S = S.data(); st[t].A = &A; st[t].run = run;
+      st[t].S = S.data(); st[t].A = A; st[t].run = run;
       st[t].R = d->run_off[run + 1] - off; st[t].leaves = d->run_leaf + off;
       st[t].amax = 0.0; st[t].fb = 0;
     }
@@ -36,7 +36,7 @@ extern "C" int emu_stage(const OmbStageDesc* d, int nthr) {
 #define ALL(stmt) for (int t = 0; t < nthr; t++) { Stage& s = st[t]; (void)s; stmt; }
     for (int X = 0; X < 4; X++) ALL(s.load_plane(X, t, nthr));
     for (int X = 2; X < 8 * R + 4; X++) {
-      ALL(s.X = X);
+      ALL(s.set_plane(X));
       if (X + 2 < 8 * R + 6) ALL(s.load_plane(X + 2, t, nthr));
       ALL(s.boundary_lines(0, t, nthr, h[t]));
       ALL(s.store_hi(h[t]); if (X >= 3) s.combine_A(t, nthr));
