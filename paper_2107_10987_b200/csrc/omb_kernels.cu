@@ -264,7 +264,14 @@ __global__ void __launch_bounds__(STAGE_THREADS, 1) k_stage(StageArgs A) {
   __syncthreads();
   for (int X = 2; X < 8 * R + 4; X++) {
     st.set_plane(X);
+    // P0 of this step shares a phase with P6 of the previous one: the load
+    // writes the ring slot of plane X-3, the update reads only FX/FYZ
     if (X + 2 < 8 * R + 6) st.load_plane(X + 2, tid, nthr);
+    if (X >= 3 && st.interior(X - 2)) {
+      st.set_plane(X - 1);
+      st.update_plane(tid, nthr);
+      st.set_plane(X);
+    }
     __syncthreads();
     st.boundary_lines(0, tid, nthr, h);
     __syncthreads();
@@ -284,9 +291,10 @@ __global__ void __launch_bounds__(STAGE_THREADS, 1) k_stage(StageArgs A) {
     __syncthreads();
     if (X >= 3) st.faces_yz(tid, nthr);
     __syncthreads();
-    if (st.interior(X - 1)) st.update_plane(tid, nthr);
-    __syncthreads();
   }
+  // P6 of the last plane
+  st.set_plane(8 * R + 3);
+  st.update_plane(tid, nthr);
   block_reduce(st.amax, st.fb, A.amax_bits, A.fallback);
 }
 

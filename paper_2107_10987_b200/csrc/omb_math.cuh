@@ -44,6 +44,17 @@ OMB_HD int ldz(int l) {
   }
 }
 
+// IEEE a/b that never takes CUDA's division slow path for a zero numerator
+// (CUDA routes 0/b through a called subroutine; zero momenta and zero
+// deviations are everywhere in the Sedov ambient).  For a == 0, a/b equals
+// a*(1/b) exactly for every b (finite, 0, inf, NaN), so the numerator is
+// replaced by 1 and the quotient rebuilt -- branch-free, bit-identical.
+OMB_HD double div_nz(double a, double b) {
+  bool z = (a == 0.0);
+  double q = (z ? 1.0 : a) / b;
+  return z ? a * q : q;
+}
+
 // NaN-faithful helpers: C fmin/fmax semantics (IEEE minNum/maxNum), as libm.
 OMB_HD double dmin(double a, double b) { return fmin(a, b); }
 OMB_HD double dmax(double a, double b) { return fmax(a, b); }
@@ -134,13 +145,13 @@ OMB_HD void kt_state(const double* w, double gamma, double gm1, KtState& s) {
   s.v[1] = w[2];
   s.v[2] = w[3];
   s.p = w[4];
-  s.c = sqrt(gamma * s.p / s.r);
+  s.c = sqrt(div_nz(gamma * s.p, s.r));
   double kin = 0.5 * s.r * (s.v[0] * s.v[0] + s.v[1] * s.v[1] + s.v[2] * s.v[2]);
   s.u[0] = s.r;
   s.u[1] = s.r * s.v[0];
   s.u[2] = s.r * s.v[1];
   s.u[3] = s.r * s.v[2];
-  s.u[4] = s.p / gm1 + kin;
+  s.u[4] = div_nz(s.p, gm1) + kin;
   s.u[5] = w[5];
 }
 
@@ -167,7 +178,7 @@ OMB_HD double kt_axis(const KtState& L, const KtState& R, int axis, double* out)
   if (denom > 0.0) {
     double apam = ap * am;
 #pragma unroll
-    for (int v = 0; v < NF; v++) out[v] = (ap * fl[v] - am * fr[v] + apam * (R.u[v] - L.u[v])) / denom;
+    for (int v = 0; v < NF; v++) out[v] = div_nz(ap * fl[v] - am * fr[v] + apam * (R.u[v] - L.u[v]), denom);
   } else {
 #pragma unroll
     for (int v = 0; v < NF; v++) out[v] = fl[v];
@@ -179,7 +190,7 @@ OMB_HD double kt_axis(const KtState& L, const KtState& R, int axis, double* out)
 // F = C + (4 edev + vdev)/36 with edev = (e0+e1)+(e2+e3), e_i = 0.5 acc_i - C
 OMB_HD double pdev_edge(double acc, double c) { return 0.5 * acc - c; }
 OMB_HD double pdev_vert(double acc, double c) { return 0.25 * acc - c; }
-OMB_HD double face_final(double c, double edev, double vdev) { return c + (4.0 * edev + vdev) / 36.0; }
+OMB_HD double face_final(double c, double edev, double vdev) { return c + div_nz(4.0 * edev + vdev, 36.0); }
 // point accumulators exactly as the Cython loop builds them
 OMB_HD double edge_acc(double f0, double f1) { return (0.0 + f0) + f1; }
 OMB_HD double vert_acc(double f0, double f1, double f2, double f3) { return (0.0 + (f0 + f1)) + (f2 + f3); }
@@ -211,8 +222,8 @@ OMB_HD double nanmax(double a, double b) {
 }
 OMB_HD double speed_cell(const double* u, double gamma, double gm1, double eta) {
   double rho = u[0];
-  double vm = nanmax(nanmax(fabs(u[1]) / rho, fabs(u[2]) / rho), fabs(u[3]) / rho);
-  double kin = 0.5 * ((u[1] * u[1] + u[2] * u[2]) + u[3] * u[3]) / rho;
+  double vm = nanmax(nanmax(div_nz(fabs(u[1]), rho), div_nz(fabs(u[2]), rho)), div_nz(fabs(u[3]), rho));
+  double kin = div_nz(0.5 * ((u[1] * u[1] + u[2] * u[2]) + u[3] * u[3]), rho);
   double e1 = u[4] - kin;
   double eint = (e1 >= eta * u[4]) ? e1 : pow(u[5], gamma);
   double p = gm1 * eint;
@@ -263,7 +274,7 @@ OMB_HD void update_cell(const UpdateParams& P, const double* u, const double* u0
     nw[v] = (P.a != 0.0) ? P.a * u0[v] + P.b * st : st;
   }
   {  // dual_energy_sync
-    double kin = 0.5 * ((nw[1] * nw[1] + nw[2] * nw[2]) + nw[3] * nw[3]) / nw[0];
+    double kin = div_nz(0.5 * ((nw[1] * nw[1] + nw[2] * nw[2]) + nw[3] * nw[3]), nw[0]);
     double e1 = nw[4] - kin;
     if (e1 >= P.eta * nw[4]) nw[5] = pow(fabs(e1), P.inv_gamma);
   }

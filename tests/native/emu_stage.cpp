@@ -37,7 +37,8 @@ extern "C" int emu_stage(const OmbStageDesc* d, int nthr) {
     for (int X = 0; X < 4; X++) ALL(s.load_plane(X, t, nthr));
     for (int X = 2; X < 8 * R + 4; X++) {
       ALL(s.set_plane(X));
-      if (X + 2 < 8 * R + 6) ALL(s.load_plane(X + 2, t, nthr));
+      ALL(if (X + 2 < 8 * R + 6) s.load_plane(X + 2, t, nthr);
+          if (X >= 3 && s.interior(X - 2)) { s.set_plane(X - 1); s.update_plane(t, nthr); s.set_plane(X); });
       ALL(s.boundary_lines(0, t, nthr, h[t]));
       ALL(s.store_hi(h[t]); if (X >= 3) s.combine_A(t, nthr));
       if (A.new_mode) {
@@ -47,8 +48,8 @@ extern "C" int emu_stage(const OmbStageDesc* d, int nthr) {
       ALL(s.inplane_lines(t, nthr));
       ALL(if (s.interior(X)) s.inplane_fluxes(t, nthr));
       ALL(if (X >= 3) s.faces_yz(t, nthr));
-      ALL(if (s.interior(X - 1)) s.update_plane(t, nthr));
     }
+    ALL(s.set_plane(8 * R + 3); s.update_plane(t, nthr));
     double m = 0.0;
     long long f = 0;
     for (int t = 0; t < nthr; t++) {
