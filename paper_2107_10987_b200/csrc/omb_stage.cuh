@@ -251,8 +251,11 @@ struct Stage {
 
   OMB_HD void kt_into(const KtState& sP, const KtState& sQ, int l, int axis, double* dst, int stride) {
     int d = axis == 0 ? ldx(l) : (axis == 1 ? ldy(l) : ldz(l));
+    // the canonical line direction runs against the face normal: the stored
+    // lo/hi states swap roles (_core.pyx:299-306)
+    bool flip = d < 0;
     double f[NF];
-    double sp = d < 0 ? kt_axis(sQ, sP, axis, f) : kt_axis(sP, sQ, axis, f);
+    double sp = kt_axis(flip ? sQ : sP, flip ? sP : sQ, axis, f);
     if (sp > amax) amax = sp;
 #pragma unroll
     for (int v = 0; v < NF; v++) dst[v * stride] = f[v];
@@ -285,14 +288,14 @@ struct Stage {
       KtState sP, sQ;
       kt_state(hp, A.gamma, A.gm1, sP);
       kt_state(lo, A.gamma, A.gm1, sQ);
-      if (g == 0) {
-        kt_into(sP, sQ, l, 0, S + Smem::RAWA + (chA(l, 0) * NF) * NP + pp, NP);
-        if (l != 0) {
-          int ax2 = (l == 3 || l == 4) ? 1 : 2;
-          kt_into(sP, sQ, l, ax2, S + Smem::RAWA + (chA(l, ax2) * NF) * NP + pp, NP);
-        }
-      } else {
-        for (int ax = 0; ax < 3; ax++) kt_into(sP, sQ, l, ax, S + Smem::RAWB + (chB(l, ax) * NF) * NP + pp, NP);
+      // axes served by this line: x always; y for lines 3,4; z for 5,6; all for 9..12
+      int ax_second = (l == 3 || l == 4) ? 1 : 2;
+      int nax = l == 0 ? 1 : (l >= 9 ? 3 : 2);
+#pragma unroll 1
+      for (int k = 0; k < nax; k++) {
+        int ax = k == 0 ? 0 : (l >= 9 ? k : ax_second);
+        double* dst = g == 0 ? S + Smem::RAWA + (chA(l, ax) * NF) * NP + pp : S + Smem::RAWB + (chB(l, ax) * NF) * NP + pp;
+        kt_into(sP, sQ, l, ax, dst, NP);
       }
     }
   }
@@ -384,27 +387,28 @@ struct Stage {
   OMB_HD void inplane_fluxes(int tid, int nthr) {
     int ntot = NYF + NZF + (A.quad ? 2 * NCOR : 0);
     for (int it = tid; it < ntot; it += nthr) {
-      KtState sP, sQ;
-      if (it < NYF) {
-        int y = 2 + it / 8, z = 3 + it % 8;
-        lhi_state(0, 1, y, z, sP);
-        lhi_state(0, 0, y + 1, z, sQ);
-        kt_into(sP, sQ, 1, 1, S + Smem::IPCY + it, NYF);
-      } else if (it < NYF + NZF) {
-        int s = it - NYF, y = 3 + s / 9, z = 2 + s % 9;
-        lhi_state(1, 1, y, z, sP);
-        lhi_state(1, 0, y, z + 1, sQ);
-        kt_into(sP, sQ, 2, 2, S + Smem::IPCZ + s, NZF);
-      } else {
+      int ip, py, pz, qy, qz, l, ax0, nax, stride;
+      double* dst;
+      if (it < NYF) {  // y-face centre: line 1, axis y
+        ip = 0; l = 1; py = 2 + it / 8; pz = 3 + it % 8; qy = py + 1; qz = pz;
+        ax0 = 1; nax = 1; dst = S + Smem::IPCY + it; stride = NYF;
+      } else if (it < NYF + NZF) {  // z-face centre: line 2, axis z
+        int s2 = it - NYF;
+        ip = 1; l = 2; py = 3 + s2 / 9; pz = 2 + s2 % 9; qy = py; qz = pz + 1;
+        ax0 = 2; nax = 1; dst = S + Smem::IPCZ + s2; stride = NZF;
+      } else {  // edge point (a+1/2, b+1/2) of lines 7 / 8, axes y and z
         int j = it - NYF - NZF, li = j / NCOR, c = j % NCOR, a = 2 + c / 9, b = 2 + c % 9;
-        int l = li == 0 ? 7 : 8;
-        int ip = li == 0 ? 2 : 3;
-        int py = a, pz = li == 0 ? b : b + 1;
-        lhi_state(ip, 1, py, pz, sP);
-        lhi_state(ip, 0, py + 1, pz + ldz(l), sQ);
-        kt_into(sP, sQ, l, 1, S + Smem::IPR + ((li * 2 + 0) * NF) * NCOR + c, NCOR);
-        kt_into(sP, sQ, l, 2, S + Smem::IPR + ((li * 2 + 1) * NF) * NCOR + c, NCOR);
+        l = li == 0 ? 7 : 8;
+        ip = li + 2;
+        py = a; pz = li == 0 ? b : b + 1;
+        qy = py + 1; qz = pz + ldz(l);
+        ax0 = 1; nax = 2; dst = S + Smem::IPR + ((li * 2) * NF) * NCOR + c; stride = NCOR;
       }
+      KtState sP, sQ;
+      lhi_state(ip, 1, py, pz, sP);
+      lhi_state(ip, 0, qy, qz, sQ);
+#pragma unroll 1
+      for (int k = 0; k < nax; k++) kt_into(sP, sQ, l, ax0 + k, dst + k * NF * NCOR, stride);
     }
   }
 
