@@ -181,7 +181,7 @@ __global__ void k_fluxes(const double* __restrict__ lo, const double* __restrict
         kt_state(wP, gamma, gm1, sP);
         kt_state(wQ, gamma, gm1, sQ);
         double fv[NF];
-        double sp = T.flip[rr0 + r] ? kt_axis(sQ, sP, axis, fv) : kt_axis(sP, sQ, axis, fv);
+        double sp = kt_axis(sP, sQ, axis, T.flip[rr0 + r] != 0, fv);
         if (sp > amax) amax = sp;
         if (nrow == 4) {
           if (r == 0 || r == 2) {

@@ -155,33 +155,42 @@ OMB_HD void kt_state(const double* w, double gamma, double gm1, KtState& s) {
   s.u[5] = w[5];
 }
 
-// flux through an `axis` face from left state L to right state R; returns
-// the signal speed max(a+, -a-).  out: 6 conserved-flux components.
-OMB_HD double kt_axis(const KtState& L, const KtState& R, int axis, double* out) {
-  // axis is selected with compares (no dynamic register-array indexing,
-  // which would push the states to local memory)
-  double vnl = axis == 0 ? L.v[0] : (axis == 1 ? L.v[1] : L.v[2]);
-  double vnr = axis == 0 ? R.v[0] : (axis == 1 ? R.v[1] : R.v[2]);
-  double ap = dmax(0.0, dmax(vnl + L.c, vnr + R.c));
-  double am = dmin(0.0, dmin(vnl - L.c, vnr - R.c));
-  double fl[NF], fr[NF];
+// Flux through an `axis` face across the interface P -> Q (P = cell the
+// `hi` state belongs to, Q = P + line direction, whose `lo` state is used).
+// When the line runs against the face normal (`flip`) the reference swaps
+// the roles: left = Q, right = P (_core.pyx:299-306).  The swap is folded
+// into scalar coefficients instead of selecting whole states:
+//   ap*fl - am*fr + (ap*am)*(ur-ul)
+//     = cP*fP + cQ*fQ + s*(uQ-uP),  (cP,cQ,s) = (ap,-am,ap*am) or (-am,ap,-(ap*am))
+// which is bit-identical (IEEE + commutes, x-y = x+(-y), products negate
+// exactly).  Returns the signal speed max(a+, -a-).
+OMB_HD double kt_axis(const KtState& P, const KtState& Q, int axis, bool flip, double* out) {
+  double vnP = axis == 0 ? P.v[0] : (axis == 1 ? P.v[1] : P.v[2]);
+  double vnQ = axis == 0 ? Q.v[0] : (axis == 1 ? Q.v[1] : Q.v[2]);
+  double eP = vnP + P.c, eQ = vnQ + Q.c;
+  double mP = vnP - P.c, mQ = vnQ - Q.c;
+  double ap = dmax(0.0, flip ? dmax(eQ, eP) : dmax(eP, eQ));
+  double am = dmin(0.0, flip ? dmin(mQ, mP) : dmin(mP, mQ));
+  double denom = ap - am;
+  double apam = ap * am;
+  double cP = flip ? -am : ap;
+  double cQ = flip ? ap : -am;
+  double sg = flip ? -apam : apam;
+  bool ok = denom > 0.0;
 #pragma unroll
   for (int v = 0; v < NF; v++) {
-    double tl = L.u[v] * vnl, tr = R.u[v] * vnr;
-    bool nrm = (v == 1 + axis);  // normal momentum picks up the pressure
-    fl[v] = nrm ? tl + L.p : tl;
-    fr[v] = nrm ? tr + R.p : tr;
-  }
-  fl[4] += L.p * vnl;
-  fr[4] += R.p * vnr;
-  double denom = ap - am;
-  if (denom > 0.0) {
-    double apam = ap * am;
-#pragma unroll
-    for (int v = 0; v < NF; v++) out[v] = div_nz(ap * fl[v] - am * fr[v] + apam * (R.u[v] - L.u[v]), denom);
-  } else {
-#pragma unroll
-    for (int v = 0; v < NF; v++) out[v] = fl[v];
+    double fP = P.u[v] * vnP, fQ = Q.u[v] * vnQ;
+    if (v == 1 || v == 2 || v == 3) {  // normal momentum picks up the pressure
+      bool nrm = (v == 1 + axis);
+      fP = nrm ? fP + P.p : fP;
+      fQ = nrm ? fQ + Q.p : fQ;
+    }
+    if (v == 4) {
+      fP = fP + P.p * vnP;
+      fQ = fQ + Q.p * vnQ;
+    }
+    double num = (cP * fP + cQ * fQ) + sg * (Q.u[v] - P.u[v]);
+    out[v] = ok ? div_nz(num, denom) : (flip ? fQ : fP);
   }
   return dmax(ap, -am);
 }

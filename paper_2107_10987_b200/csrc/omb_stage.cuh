@@ -255,7 +255,7 @@ struct Stage {
     // lo/hi states swap roles (_core.pyx:299-306)
     bool flip = d < 0;
     double f[NF];
-    double sp = kt_axis(flip ? sQ : sP, flip ? sP : sQ, axis, f);
+    double sp = kt_axis(sP, sQ, axis, flip, f);
     if (sp > amax) amax = sp;
 #pragma unroll
     for (int v = 0; v < NF; v++) dst[v * stride] = f[v];
