@@ -3,6 +3,7 @@
 // (nvcc -gencode arch=compute_100a,code=sm_100a -fmad=false ...).
 #include <cuda_runtime.h>
 #include <stdio.h>
+#include <stdlib.h>
 #include <string.h>
 
 #include <mutex>
@@ -217,7 +218,7 @@ __global__ void k_fluxes(const double* __restrict__ lo, const double* __restrict
 // ---------------------------------------------------------------------------
 // fused stage: one CTA per run
 // ---------------------------------------------------------------------------
-constexpr int STAGE_THREADS = 512;
+constexpr int STAGE_THREADS = 512;  // max threads of any k_stage variant
 
 __device__ __forceinline__ void block_reduce(double amax, long long fb, unsigned long long* amax_bits,
                                              unsigned long long* fallback) {
@@ -246,7 +247,8 @@ __device__ __forceinline__ void block_reduce(double amax, long long fb, unsigned
   }
 }
 
-__global__ void __launch_bounds__(STAGE_THREADS, 1) k_stage(StageArgs A) {
+template <int NT>
+__global__ void __launch_bounds__(NT, 1) k_stage(StageArgs A) {
   extern __shared__ double S[];
   const int tid = threadIdx.x, nthr = blockDim.x;
   Stage st;
@@ -442,9 +444,16 @@ int omb_stage(const OmbStageDesc* d, void* stream) {
   if (d->ucur == d->unext) return set_err("omb_stage: unext must not alias ucur");
   static bool attr_set = false;
   if (!attr_set) {
-    CK(cudaFuncSetAttribute(k_stage, cudaFuncAttributeMaxDynamicSharedMemorySize, Smem::BYTES), "smem attribute");
+    CK(cudaFuncSetAttribute(k_stage<512>, cudaFuncAttributeMaxDynamicSharedMemorySize, Smem::BYTES), "smem attribute");
+    CK(cudaFuncSetAttribute(k_stage<384>, cudaFuncAttributeMaxDynamicSharedMemorySize, Smem::BYTES), "smem attribute");
+    CK(cudaFuncSetAttribute(k_stage<256>, cudaFuncAttributeMaxDynamicSharedMemorySize, Smem::BYTES), "smem attribute");
     attr_set = true;
   }
+  static int nt = [] {
+    const char* e = getenv("OMB_STAGE_THREADS");
+    int v = e ? atoi(e) : 512;
+    return (v == 256 || v == 384) ? v : 512;
+  }();
   StageArgs A;
   A.ucur = d->ucur;
   A.u0 = d->u0;
@@ -472,7 +481,9 @@ int omb_stage(const OmbStageDesc* d, void* stream) {
   A.amax_bits = d->amax_bits;
   A.fallback = d->fallback;
   if (d->nruns <= 0) return 0;
-  k_stage<<<d->nruns, STAGE_THREADS, Smem::BYTES, (cudaStream_t)stream>>>(A);
+  if (nt == 512) k_stage<512><<<d->nruns, 512, Smem::BYTES, (cudaStream_t)stream>>>(A);
+  else if (nt == 384) k_stage<384><<<d->nruns, 384, Smem::BYTES, (cudaStream_t)stream>>>(A);
+  else k_stage<256><<<d->nruns, 256, Smem::BYTES, (cudaStream_t)stream>>>(A);
   CK(cudaGetLastError(), "omb_stage launch");
   return 0;
 }

@@ -157,11 +157,11 @@ OMB_HD void gather_cell(const double* U, long long fstride, const LeafInfo& LI, 
     if ((flipmask >> a) & 1) u[1 + a] = -u[1 + a];
 }
 
-// values a thread carries across the barrier after P1 (one item per thread:
-// the kernel runs >= 512 threads and P1 has <= 500 items)
+// values a thread carries across the barrier after P1 (<= 2 items per
+// thread: P1 has <= 500 items and the kernel runs >= 256 threads)
 struct Hold {
-  double hi[NF];
-  int slot;
+  double h0[NF], h1[NF];
+  int s0, s1;
 };
 
 struct Stage {
@@ -265,16 +265,25 @@ struct Stage {
   OMB_HD void boundary_lines(int g, int tid, int nthr, Hold& h) {
     int dl0 = g == 0 ? 0 : 5, ndl = g == 0 ? (A.new_mode ? 5 : 1) : 4;
     int nitems = ndl * NP;
-    h.slot = -1;
-    for (int it = tid; it < nitems; it += nthr) {
+    h.s0 = h.s1 = -1;
+#pragma unroll 1
+    for (int k = 0; k < 2; k++) {
+      int it = tid + k * nthr;
+      if (it >= nitems) break;
       int dl = dl0 + it / NP, pos = it % NP;
       int l = dl_line(dl);
       int y = 2 + pos / 10, z = 2 + pos % 10;
       double lo[NF], hi[NF];
       mono6(l, X, y, z, lo, hi);
+      if (k == 0) {
 #pragma unroll
-      for (int v = 0; v < NF; v++) h.hi[v] = hi[v];
-      h.slot = dl * NF * NP + pos;
+        for (int v = 0; v < NF; v++) h.h0[v] = hi[v];
+        h.s0 = dl * NF * NP + pos;
+      } else {
+#pragma unroll
+        for (int v = 0; v < NF; v++) h.h1[v] = hi[v];
+        h.s1 = dl * NF * NP + pos;
+      }
       bool kt = X >= 3 && (A.quad || l == 0);
       if (!kt) continue;
       int py = y - ldy(l), pz = z - ldz(l);
@@ -292,8 +301,8 @@ struct Stage {
       int ax_second = (l == 3 || l == 4) ? 1 : 2;
       int nax = l == 0 ? 1 : (l >= 9 ? 3 : 2);
 #pragma unroll 1
-      for (int k = 0; k < nax; k++) {
-        int ax = k == 0 ? 0 : (l >= 9 ? k : ax_second);
+      for (int q = 0; q < nax; q++) {
+        int ax = q == 0 ? 0 : (l >= 9 ? q : ax_second);
         double* dst = g == 0 ? S + Smem::RAWA + (chA(l, ax) * NF) * NP + pp : S + Smem::RAWB + (chB(l, ax) * NF) * NP + pp;
         kt_into(sP, sQ, l, ax, dst, NP);
       }
@@ -301,9 +310,13 @@ struct Stage {
   }
 
   OMB_HD void store_hi(const Hold& h) {
-    if (h.slot >= 0) {
+    if (h.s0 >= 0) {
 #pragma unroll
-      for (int v = 0; v < NF; v++) S[Smem::HI + h.slot + v * NP] = h.hi[v];
+      for (int v = 0; v < NF; v++) S[Smem::HI + h.s0 + v * NP] = h.h0[v];
+    }
+    if (h.s1 >= 0) {
+#pragma unroll
+      for (int v = 0; v < NF; v++) S[Smem::HI + h.s1 + v * NP] = h.h1[v];
     }
   }
 

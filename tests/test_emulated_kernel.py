@@ -12,11 +12,11 @@ from oracle.step import OracleStepper
 
 
 @pytest.mark.parametrize("name", ["smooth_periodic", "smooth_reflecting"])
-@pytest.mark.parametrize("max_run", [1, 2])
-def test_emulated_step_matches_golden(name, max_run):
+@pytest.mark.parametrize("max_run,nthr", [(1, 512), (2, 512), (2, 256), (3, 384)])
+def test_emulated_step_matches_golden(name, max_run, nthr):
     t, g = case_tree(name)
     dt = float(g["dts"][0])
-    em = EmuStepper(t, 1.4, max_run=max_run)
+    em = EmuStepper(t, 1.4, max_run=max_run, nthr=nthr)
     em.rk3_step(dt)
     got = state_of(t)
     assert bitwise_mismatch(got[:, :5], g["state1"][:, :5]) == 0
