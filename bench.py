@@ -141,7 +141,7 @@ def cpu_run(level, nleaves, steps, warmup):
 def reference_arm(args, rank, world):
     if rank != 0:
         return
-    level = args.level if args.level is not None else 4
+    level = args.level if args.level is not None else (4 if world == 1 else 5)
     # size the per-step sample so the whole run stays within ~3 minutes
     probe_v, nthr, _, _ = cpu_run(level, 8, 1, 0)
     budget = 150.0 / max(1, args.steps + args.warmup)
@@ -193,12 +193,19 @@ def gpu_arm(args, rank, world):
     if world > 1:
         import torch.distributed as dist
 
-    level = args.level if args.level is not None else 4
+    # N=1: config c2 (128^3, level 4); N>1: config c3 (256^3, level 5) partitioned by leaf
+    level = args.level if args.level is not None else (4 if world == 1 else 5)
     tree = sedov_tree(level)
     eos = EosConfig(gamma=1.4)
-    st = B200HydroStepper(tree, eos, HydroMode("new"), host_sync=False, max_run=args.max_run)
+    part = None
+    if world > 1:
+        from paper_2107_10987_b200.partition import Partition
+
+        part = Partition(tree, world, rank)
+    st = B200HydroStepper(tree, eos, HydroMode("new"), host_sync=False, max_run=args.max_run, partition=part)
     lib = _lib.load()
-    cells = st.batch.L * 512
+    cells = st.nglobal * 512  # whole job
+    local_cells = st.batch.ncompute * 512
     peak64 = fp64_peak(lib, torch)
 
     # warm-up
@@ -246,7 +253,8 @@ def gpu_arm(args, rank, world):
     e2e = None
     if args.e2e_steps > 0:
         t2 = sedov_tree(level)
-        st2 = B200HydroStepper(t2, eos, HydroMode("new"), host_sync=True, max_run=args.max_run)
+        p2 = Partition(t2, world, rank) if world > 1 else None
+        st2 = B200HydroStepper(t2, eos, HydroMode("new"), host_sync=True, max_run=args.max_run, partition=p2)
         for _ in range(2):
             st2.rk3_step(st2.cfl_dt(0.4))
         torch.cuda.synchronize()
@@ -256,19 +264,24 @@ def gpu_arm(args, rank, world):
             st2.rk3_step(dt)
         torch.cuda.synchronize()
         w1 = time.perf_counter()
+        wall = w1 - w0
+        if dist is not None:
+            t = torch.tensor([wall], dtype=torch.float64, device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            wall = float(t.item())
         nbytes = 6 * st2.batch.L * 512 * 8
-        e2e = {"value": cells * args.e2e_steps / (w1 - w0) * world, "unit": UNIT,
+        e2e = {"value": cells * args.e2e_steps / wall, "unit": UNIT,
                "h2d_bytes_per_step": nbytes, "d2h_bytes_per_step": nbytes + 2 * 8 + 4 + 6 * 8,
                "steps": args.e2e_steps, "api": "B200HydroStepper.cfl_dt + rk3_step (host_sync=True)"}
 
     if rank != 0:
         return
-    value = cells * K * world / (ms / 1e3)
+    value = cells * K / (ms / 1e3)
     mean_stage = sum(stage_ms) / len(stage_ms)
-    achieved_tf = FLOPS_PER_CELL_STAGE * cells / (mean_stage / 1e3) / 1e12
+    achieved_tf = FLOPS_PER_CELL_STAGE * local_cells / (mean_stage / 1e3) / 1e12
     pk = peaks()
     hbm_peak = pk.get("hbm_gbs", 6650.0)
-    achieved_gbs = BYTES_PER_CELL_STAGE * cells / (mean_stage / 1e3) / 1e9
+    achieved_gbs = BYTES_PER_CELL_STAGE * local_cells / (mean_stage / 1e3) / 1e9
     traffic = None
     tf = os.path.join(ROOT, "profiles", "stage_traffic.json")
     if os.path.exists(tf):
@@ -276,26 +289,28 @@ def gpu_arm(args, rank, world):
             traffic = json.load(f).get("bytes_per_launch")
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K, "warmup": args.warmup,
-        "ms_per_step": ms / K, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "ms_per_step": ms / K, "higher_is_better": True, "scaling": "weak" if world == 1 else "strong",
+        "vs_baseline": None,
         "dtype": "f64", "data": "synthetic (init_sedov Sedov-Taylor, no RNG)",
         "config": {"workload": f"sedov_uniform_L{level}_n8: {st.batch.L} sub-grids of 8^3 = {cells} cells "
                                f"({int(round(cells ** (1 / 3)))}^3), reflecting, cfl 0.4, scheme new",
                    "step": "cfl_dt + 3 fused RK stages, dt on device",
                    "l2": "working set (3 x 6 x cells x 8 B = %.0f MB) > 126 MB L2; no flush" % (3 * 48 * cells / 1e6),
-                   "runs": st.batch.nruns, "max_run": args.max_run, "parallelism": f"leaf-partitioned x{world}"},
+                   "runs": st.batch.nruns, "max_run": args.max_run, "parallelism": f"leaf-partitioned x{world}",
+                   "halo_leaves_per_rank": int(st.batch.L - st.batch.ncompute)},
         "roofline": {"bound": "fp64", "achieved": achieved_tf, "peak": peak64, "unit": "TFLOP/s",
                      "frac": achieved_tf / peak64, "traffic": traffic,
                      "kernel": "k_stage (fused RK stage)", "stage_ms": mean_stage,
-                     "flops_per_launch": FLOPS_PER_CELL_STAGE * cells,
+                     "flops_per_launch": FLOPS_PER_CELL_STAGE * local_cells,
                      "peak_source": "in-run DFMA probe (omb_fp64_peak); MEASURED_PEAKS.json has no FP64 entry",
                      "hbm": {"achieved_gbs": achieved_gbs, "peak_gbs": hbm_peak, "frac": achieved_gbs / hbm_peak,
-                             "algorithmic_bytes_per_launch": BYTES_PER_CELL_STAGE * cells}},
+                             "algorithmic_bytes_per_launch": BYTES_PER_CELL_STAGE * local_cells}},
         "clocks": clocks,
         "e2e": e2e,
-        "gpu_launches": K * 5,
+        "gpu_launches": K * (5 + (6 if world > 1 else 0)),
         "cfl_abort_in_timed_steps": aborted,
     }
-    if not args.no_cpu_baseline:
+    if not args.no_cpu_baseline and world == 1:
         v, nthr, sample, _ = cpu_run(level, min(args.cpu_leaves, st.batch.L), 1, 0)
         line["cpu_baseline"] = {"value": v, "unit": UNIT, "cores": nthr, "kind": "port", "sample": sample}
     print(json.dumps(line), flush=True)
@@ -305,17 +320,16 @@ def main():
     args = parse()
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
+    if args.impl == "reference":  # CPU only, rank 0 alone; no collectives needed
+        reference_arm(args, rank, world)
+        return
     if world > 1:
         import torch
         import torch.distributed as dist
 
-        if args.impl == "b200":
-            torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", 0)))
-        dist.init_process_group("nccl" if args.impl == "b200" else "gloo")
-    if args.impl == "reference":
-        reference_arm(args, rank, world)
-    else:
-        gpu_arm(args, rank, world)
+        torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", 0)))
+        dist.init_process_group("nccl", device_id=torch.device("cuda", int(os.environ.get("LOCAL_RANK", 0))))
+    gpu_arm(args, rank, world)
     if world > 1:
         import torch.distributed as dist
 

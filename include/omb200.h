@@ -78,6 +78,11 @@ int omb_fluxes(const double *lo, const double *hi, int n, double gamma, int new_
                double *fx, double *fy, double *fz, unsigned long long *amax_bits, void *stream);
 int omb_stage(const OmbStageDesc *desc, void *stream);
 int omb_cfl(const OmbCflDesc *desc, void *stream);
+/* multi-GPU halo exchange (replaces the cross-rank part of fill_leaf_ghosts, ghosts.py:115-150):
+ * pack whole leaves idx[0..n) of a [6][fstride] state into a leaf-major [n][6][512] message, and
+ * unpack such a message into leaf slots first..first+n of a state */
+int omb_pack_leaves(const double *u, long long fstride, const int *idx, int n, double *out, void *stream);
+int omb_unpack_leaves(const double *in, int n, double *u, long long fstride, int first, void *stream);
 /* FP64 DFMA throughput probe (roofline denominator): blocks*256*8*iters DFMAs */
 int omb_fp64_peak(double *scratch, int blocks, int iters, void *stream);
 /* padded (6,14,14,14) conserved block of one leaf as the ghost fill would produce it */

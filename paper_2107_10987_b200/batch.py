@@ -27,8 +27,57 @@ class UnsupportedTree(NotImplementedError):
     pass
 
 
+def neighbor_table(tree, leaves):
+    """(len(leaves), 27) global indices (into `leaves`) of the same-level
+    neighbour at each offset (OFFS order; centre = self), -1 where the
+    offset leaves the domain (non-periodic).  Uses Octree.neighbor_ipos /
+    find_leaf_region semantics (tree.py:161-195); raises UnsupportedTree for
+    coarse/fine neighbours.  Uniform trees take a vectorised lattice path."""
+    G = len(leaves)
+    levels = {lf.level for lf in leaves}
+    index = {lf.path: i for i, lf in enumerate(leaves)}
+    out = np.full((G, 27), -1, dtype=np.int64)
+    if len(levels) == 1 and len(tree.leaves()) == G and G == 8 ** next(iter(levels)):
+        lev = next(iter(levels))
+        span = 2 ** lev
+        ip = np.array([lf.ipos for lf in leaves], dtype=np.int64)
+        lut = np.empty((span, span, span), dtype=np.int64)
+        lut[ip[:, 0], ip[:, 1], ip[:, 2]] = np.arange(G)
+        for q, o in enumerate(OFFS):
+            pos = ip + np.array(o)
+            if tree.boundary == "periodic":
+                pos %= span
+                out[:, q] = lut[pos[:, 0], pos[:, 1], pos[:, 2]]
+            else:
+                ok = np.all((pos >= 0) & (pos < span), axis=1)
+                pc = np.clip(pos, 0, span - 1)
+                out[:, q] = np.where(ok, lut[pc[:, 0], pc[:, 1], pc[:, 2]], -1)
+        return out
+    for i, lf in enumerate(leaves):
+        for q, o in enumerate(OFFS):
+            if o == (0, 0, 0):
+                out[i, q] = i
+                continue
+            pos = tree.neighbor_ipos(lf, o)
+            if pos is None:
+                continue
+            cover = tree.find_leaf_region(lf.level, pos)
+            if cover[0][1] != "same":
+                raise UnsupportedTree("coarse/fine neighbours (AMR) are not handled by the fused kernel yet")
+            j = index.get(cover[0][0].path)
+            if j is None:
+                raise UnsupportedTree("neighbour outside the leaf set")
+            out[i, q] = j
+    return out
+
+
 class LeafBatch:
-    def __init__(self, tree, max_run=4, leaves=None):
+    """Device batch of leaves.  The first ``ncompute`` leaves are advanced by
+    the stage kernel; the rest (multi-GPU halo leaves owned by other ranks)
+    only provide ghost data.  ``gnbr`` optionally supplies the neighbour
+    table in global indices with ``gids`` the global index of each leaf."""
+
+    def __init__(self, tree, max_run=4, leaves=None, ncompute=None, gnbr=None, gids=None):
         self.tree = tree
         self.n = tree.n
         if self.n != 8:
@@ -38,7 +87,11 @@ class LeafBatch:
         self.bc = BC_CODES[tree.boundary]
         self.leaves = leaves if leaves is not None else tree.sorted_leaves()
         self.L = len(self.leaves)
-        self.index = {lf.path: i for i, lf in enumerate(self.leaves)}
+        self.ncompute = self.L if ncompute is None else ncompute
+        if gnbr is None:
+            gnbr = neighbor_table(tree, self.leaves)
+            gids = np.arange(self.L)
+        local = {int(g): i for i, g in enumerate(gids)}
         self.info = np.zeros(self.L, dtype=LEAF_INFO_DTYPE)
         self.dx = np.empty(self.L)
         for i, lf in enumerate(self.leaves):
@@ -46,29 +99,18 @@ class LeafBatch:
             rec = self.info[i]
             span = 2 ** lf.level
             off = 0
-            for a in range(3):
-                if tree.boundary != "periodic":
+            if tree.boundary != "periodic":
+                for a in range(3):
                     if lf.ipos[a] - 1 < 0:
                         off |= 1 << (2 * a)
                     if lf.ipos[a] + 1 >= span:
                         off |= 1 << (2 * a + 1)
             rec["offmask"] = off
-            nbr = np.full(27, -1, dtype=np.int32)
-            for q, o in enumerate(OFFS):
-                if o == (0, 0, 0):
-                    nbr[q] = i
-                    continue
-                pos = tree.neighbor_ipos(lf, o)
-                if pos is None:
-                    continue
-                cover = tree.find_leaf_region(lf.level, pos)
-                if cover[0][1] != "same":
-                    raise UnsupportedTree("coarse/fine neighbours (AMR) are not handled by the fused kernel yet")
-                j = self.index.get(cover[0][0].path)
-                if j is None:
-                    raise UnsupportedTree("neighbour outside the batch")
-                nbr[q] = j
-            rec["nbr"] = nbr
+            if i < self.ncompute:
+                row = gnbr[int(gids[i])]
+                rec["nbr"] = [local[int(g)] if g >= 0 else -1 for g in row]
+            else:
+                rec["nbr"] = -1
             rec["ox"], rec["oy"], rec["oz"] = (float(x) for x in sg.origin)
             rec["dx"] = sg.dx
             rec["inv_dx"] = 1.0 / sg.dx
@@ -80,16 +122,16 @@ class LeafBatch:
         xp = OFFS.index((1, 0, 0))
         xm = OFFS.index((-1, 0, 0))
         runs = []
-        for i, lf in enumerate(self.leaves):
+        for i, lf in enumerate(self.leaves[:self.ncompute]):
             prev = self.info[i]["nbr"][xm]
-            # a run starts where there is no same-level -x neighbour inside the domain
-            if prev >= 0 and lf.ipos[0] > 0:
+            # a run starts where there is no computed same-level -x neighbour inside the domain
+            if prev >= 0 and prev < self.ncompute and lf.ipos[0] > 0:
                 continue
             chain = [i]
             while True:
                 cur = chain[-1]
                 nxt = self.info[cur]["nbr"][xp]
-                if nxt < 0 or self.leaves[cur].ipos[0] + 1 >= 2 ** self.leaves[cur].level:
+                if nxt < 0 or nxt >= self.ncompute or self.leaves[cur].ipos[0] + 1 >= 2 ** self.leaves[cur].level:
                     break
                 chain.append(int(nxt))
             # balanced split into pieces of <= max_run
@@ -100,7 +142,7 @@ class LeafBatch:
                 w = base + (1 if p < extra else 0)
                 runs.append(chain[s:s + w])
                 s += w
-        assert sum(len(r) for r in runs) == self.L
+        assert sum(len(r) for r in runs) == self.ncompute
         self.runs = runs
         self.run_off = np.zeros(len(runs) + 1, dtype=np.int32)
         self.run_off[1:] = np.cumsum([len(r) for r in runs])
@@ -115,7 +157,8 @@ class LeafBatch:
         return U
 
     def unpack(self, U):
-        for i, lf in enumerate(self.leaves):
+        """Write the computed leaves back (halo leaves belong to other ranks)."""
+        for i, lf in enumerate(self.leaves[:self.ncompute]):
             lf.subgrid.interior[:] = U[:, i]
 
     def pack_gravity(self, fields):

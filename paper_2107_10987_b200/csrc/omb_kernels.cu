@@ -385,6 +385,30 @@ __global__ void k_gather(const double* U, long long fstride, const LeafInfo* inf
   }
 }
 
+// halo exchange packing: whole 8^3 leaves, field-major state <-> leaf-major message
+__global__ void k_pack(const double* __restrict__ U, long long fstride, const int* __restrict__ idx, int n,
+                       double* __restrict__ out) {
+  long long total = (long long)n * NF * 512;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total; i += (long long)gridDim.x * blockDim.x) {
+    int c = (int)(i & 511);
+    long long kv = i >> 9;
+    int v = (int)(kv % NF);
+    long long k = kv / NF;
+    out[i] = U[v * fstride + (long long)idx[k] * 512 + c];
+  }
+}
+
+__global__ void k_unpack(const double* __restrict__ in, int n, double* __restrict__ U, long long fstride, int first) {
+  long long total = (long long)n * NF * 512;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total; i += (long long)gridDim.x * blockDim.x) {
+    int c = (int)(i & 511);
+    long long kv = i >> 9;
+    int v = (int)(kv % NF);
+    long long k = kv / NF;
+    U[v * fstride + (first + k) * 512 + c] = in[i];
+  }
+}
+
 // FP64 pipe peak probe (roofline denominator; MEASURED_PEAKS.json has no FP64 entry):
 // 8 independent DFMA chains per thread, 2 flops per DFMA.
 __global__ void k_dfma_peak(double* out, int iters) {
@@ -497,6 +521,24 @@ int omb_cfl(const OmbCflDesc* d, void* stream) {
   k_cfl_reduce<<<1, 1024, 0, (cudaStream_t)stream>>>(d->nleaves, d->ratio, d->bad, d->cfl, d->out, d->bad_leaf,
                                                      d->dt_dev);
   CK(cudaGetLastError(), "omb_cfl reduce launch");
+  return 0;
+}
+
+int omb_pack_leaves(const double* U, long long fstride, const int* idx, int n, double* out, void* stream) {
+  if (n <= 0) return 0;
+  long long total = (long long)n * NF * 512;
+  int blocks = (int)((total + 255) / 256);
+  k_pack<<<blocks < 148 * 16 ? blocks : 148 * 16, 256, 0, (cudaStream_t)stream>>>(U, fstride, idx, n, out);
+  CK(cudaGetLastError(), "omb_pack_leaves launch");
+  return 0;
+}
+
+int omb_unpack_leaves(const double* in, int n, double* U, long long fstride, int first, void* stream) {
+  if (n <= 0) return 0;
+  long long total = (long long)n * NF * 512;
+  int blocks = (int)((total + 255) / 256);
+  k_unpack<<<blocks < 148 * 16 ? blocks : 148 * 16, 256, 0, (cudaStream_t)stream>>>(in, n, U, fstride, first);
+  CK(cudaGetLastError(), "omb_unpack_leaves launch");
   return 0;
 }
 

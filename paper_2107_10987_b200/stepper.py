@@ -37,7 +37,7 @@ from .hydro import SSP_RK3_STAGES, FloorConfig, StepStats
 class B200HydroStepper:
     def __init__(self, tree, eos, mode, executor=None, gravity=None, omega=0.0, floors=None, abort_courant=1.0,
                  buffers=None, profiler=None, lane_pool=None, *, host_sync=True, max_run=4, device=None,
-                 leaves=None):
+                 leaves=None, partition=None, group=None):
         self.tree = tree
         self.eos = eos
         self.mode = mode
@@ -53,7 +53,16 @@ class B200HydroStepper:
         self.host_sync = host_sync
         self.dev = require_cuda(device)
         self.lib = _lib.load()
-        self.batch = LeafBatch(tree, max_run=max_run, leaves=leaves)
+        self.part = partition
+        self.group = group
+        if partition is not None:
+            import torch.distributed as dist
+
+            self.dist = dist
+            self.batch = partition.batch(tree, max_run=max_run)
+        else:
+            self.dist = None
+            self.batch = LeafBatch(tree, max_run=max_run, leaves=leaves)
         b = self.batch
         T = torch
         dev = self.dev
@@ -74,7 +83,13 @@ class B200HydroStepper:
         self._pinned = T.empty(n, dtype=T.float64).pin_memory()
         self._grav = None
         self._fresh = False  # device state was just uploaded from the host by cfl_dt
-        self.dx_min = float(min(b.dx))
+        self.dx_min = float(min(lf.subgrid.dx for lf in tree.leaves()))
+        self.nglobal = partition.G if partition is not None else b.L
+        if partition is not None:
+            self._send_idx = T.from_numpy(partition.send_local.copy()).to(dev)
+            self._sendbuf = T.empty(max(1, sum(partition.send_counts)) * 3072, dtype=T.float64, device=dev)
+            self._recvbuf = T.empty(max(1, sum(partition.recv_counts)) * 3072, dtype=T.float64, device=dev)
+            self._gids = partition.gids
         self.upload()
 
     # -- host <-> device -------------------------------------------------------------
@@ -94,15 +109,40 @@ class B200HydroStepper:
     def state_tensor(self):
         return self._buf[self._state]
 
+    # -- multi-GPU halo exchange ------------------------------------------------------
+    def _exchange(self, buf_index, stream=None):
+        if self.part is None:
+            return
+        from .partition import exchange
+
+        L = self.lib
+        sh = stream_handle(stream)
+        fs = self.batch.fstride
+
+        def pack(state, idx, out):
+            _lib.check(L.omb_pack_leaves(ptr(state), fs, ptr(idx), int(idx.numel()), ptr(out), sh), "omb_pack_leaves")
+
+        def unpack(inp, state, first):
+            n = sum(self.part.recv_counts)
+            _lib.check(L.omb_unpack_leaves(ptr(inp), n, ptr(state), fs, first, sh), "omb_unpack_leaves")
+
+        p = self.part
+        exchange(self.dist, self.group, self._buf[buf_index], self._send_idx, p.send_counts, p.recv_counts, p.nown,
+                 pack, unpack, self._sendbuf, self._recvbuf)
+
     # -- timestep ---------------------------------------------------------------------
     def _cfl_launch(self, cfl, stream=None):
         b = self.batch
         g = self.eos.gamma
-        d = OmbCflDesc(u=ptr(self._buf[self._state]), fstride=b.fstride, nleaves=b.L, dx=ptr(self._dx),
+        d = OmbCflDesc(u=ptr(self._buf[self._state]), fstride=b.fstride, nleaves=b.ncompute, dx=ptr(self._dx),
                        gamma=g, gm1=g - 1.0, eta=self.eos.dual_energy_eta, cfl=float(cfl),
                        ratio=ptr(self._cfl_ratio), bad=ptr(self._cfl_bad), out=ptr(self._cfl_out),
                        bad_leaf=ptr(self._cfl_badleaf), dt_dev=ptr(self._dt))
         _lib.check(self.lib.omb_cfl(ctypes.byref(d), stream_handle(stream)), "omb_cfl")
+        if self.part is not None:
+            # min over ranks of (worst, cfl*worst): RN(cfl*w) is monotone in w, so this is exact
+            self.dist.all_reduce(self._cfl_out, op=self.dist.ReduceOp.MIN, group=self.group)
+            self._dt.copy_(self._cfl_out[1:2])
 
     def cfl_dt(self, cfl):
         """dt = cfl * min over leaves of dx / max(max_axis|v| + c)  (step.py:81-92)."""
@@ -112,7 +152,14 @@ class B200HydroStepper:
         self._cfl_launch(cfl)
         out = self._cfl_out.cpu().numpy()
         bad = int(self._cfl_badleaf.cpu().item())
-        if bad >= 0:
+        if self.part is not None:
+            big = 1 << 62
+            gb = torch.tensor([int(self._gids[bad]) if bad >= 0 else big], dtype=torch.int64, device=self.dev)
+            self.dist.all_reduce(gb, op=self.dist.ReduceOp.MIN, group=self.group)
+            g = int(gb.item())
+            if g < big:
+                raise NumericsError(f"non-finite wave speed on leaf {self.tree.sorted_leaves()[g].path}")
+        elif bad >= 0:
             raise NumericsError(f"non-finite wave speed on leaf {self.batch.leaves[bad].path}")
         return cfl * float(out[0])
 
@@ -147,6 +194,7 @@ class B200HydroStepper:
                 fields = self.gravity.solve(self.tree, need_derivative=True)
                 self._grav = torch.from_numpy(self.batch.pack_gravity(fields).reshape(-1)).to(self.dev)
             nxt = others[s]
+            self._exchange(cur, stream)
             d = self._stage_desc(cur, nxt, s, a, bw)
             if events is not None:
                 events[s][0].record()
@@ -159,16 +207,22 @@ class B200HydroStepper:
         self._state = outs[2]
         return start, outs
 
+    def _reduce_stats(self):
+        if self.part is not None:
+            self.dist.all_reduce(self._acc[:3], op=self.dist.ReduceOp.MAX, group=self.group)
+            self.dist.all_reduce(self._acc[3:], op=self.dist.ReduceOp.SUM, group=self.group)
+
     def rk3_step(self, dt):
         """One SSP-RK3 step (step.py:94-102) on the device."""
         if self.host_sync and not self._fresh:
             self.upload()
         self._fresh = False
         start, outs = self.launch_step(dt)
+        self._reduce_stats()
         acc = self._acc.cpu().numpy()
         amax = acc[:3].view(np.float64)
         fb = acc[3:]
-        L = self.batch.L
+        L = self.nglobal
         stats = StepStats()
         u_prev = start
         for s in range(3):

@@ -78,3 +78,66 @@ class EmuStepper:
             self.fallback += int(fb[0])
             cur = nxt
         b.unpack(bufs[cur])
+
+
+class EmuDistStepper:
+    """Multi-rank (torch.distributed, gloo on CPU) version of EmuStepper: the
+    rank's Partition batch, halo exchange with all_to_all_single between
+    stages, the emulated stage kernel on the owned leaves."""
+
+    def __init__(self, tree, gamma, world, rank, max_run=4, nthr=512):
+        import torch.distributed as dist
+
+        from paper_2107_10987_b200.partition import Partition
+
+        self.dist = dist
+        self.part = Partition(tree, world, rank)
+        self.b = self.part.batch(tree, max_run=max_run)
+        self.gamma = gamma
+        self.nthr = nthr
+        self.run_off = np.ascontiguousarray(self.b.run_off)
+        self.run_leaf = np.ascontiguousarray(self.b.run_leaf)
+
+    def _exchange(self, U):
+        import torch
+
+        from paper_2107_10987_b200.partition import exchange
+
+        p = self.part
+        per = 6 * 512
+        send = np.zeros(max(1, sum(p.send_counts)) * per)
+        recv = np.zeros(max(1, sum(p.recv_counts)) * per)
+
+        def pack(state, idx, out):
+            out[:len(idx) * per] = state.reshape(6, -1, 512)[:, idx].transpose(1, 0, 2).reshape(-1)
+
+        def unpack(inp, state, first):
+            n = sum(p.recv_counts)
+            state.reshape(6, -1, 512)[:, first:first + n] = inp[:n * per].reshape(n, 6, 512).transpose(1, 0, 2)
+
+        pack(U, p.send_local, send)
+        st, rt = torch.from_numpy(send), torch.from_numpy(recv)
+        self.dist.all_to_all_single(rt, st, [c * per for c in p.recv_counts], [c * per for c in p.send_counts])
+        unpack(recv, U, p.nown)
+        _ = exchange  # the product's helper is exercised on the GPU path
+
+    def rk3_step(self, dt):
+        b = self.b
+        U0 = np.ascontiguousarray(b.pack())
+        bufs = [U0, np.empty_like(U0), np.empty_like(U0), np.empty_like(U0)]
+        dtv = np.array([dt])
+        cur = 0
+        for s, (a, bb) in enumerate(SSP_RK3_STAGES):
+            self._exchange(bufs[cur])
+            am = np.zeros(1, dtype=np.uint64)
+            fb = np.zeros(1, dtype=np.uint64)
+            nxt = s + 1
+            d = OmbStageDesc(ucur=ptr(bufs[cur]), u0=ptr(U0), unext=ptr(bufs[nxt]), grav=None,
+                             fstride=b.fstride, info=ptr(b.info), run_off=ptr(self.run_off),
+                             run_leaf=ptr(self.run_leaf), nruns=b.nruns, dt=ptr(dtv), a=a, b=bb,
+                             gamma=self.gamma, gm1=self.gamma - 1.0, eta=1e-3, inv_gamma=1.0 / self.gamma,
+                             omega=0.0, floor_rho=0.0, floor_tau=0.0, floor_vmax=0.0, bc=b.bc, new_mode=1,
+                             override_center=0, contact=0, amax_bits=ptr(am), fallback=ptr(fb))
+            lib().emu_stage(ctypes.byref(d), self.nthr)
+            cur = nxt
+        b.unpack(bufs[cur])

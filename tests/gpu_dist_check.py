@@ -1,0 +1,65 @@
+"""Multi-GPU parity check, run under torchrun (one rank per GPU):
+
+    python -m torch.distributed.run --nproc-per-node N --master-addr 127.0.0.1 tests/gpu_dist_check.py
+
+Each rank advances its leaf partition of the Sedov c1 tree (and of the
+smooth periodic case) with the NCCL halo exchange and compares its leaves
+with the single-process golden state bitwise; dt must equal the golden dt.
+Exit code 0 = parity."""
+
+import os
+import sys
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, HERE)
+sys.path.insert(0, os.path.dirname(HERE))
+
+
+def main():
+    import torch
+    import torch.distributed as dist
+
+    from _cases import EOS, case_tree, state_of
+    from paper_2107_10987_b200 import HydroMode
+    from paper_2107_10987_b200.partition import Partition
+    from paper_2107_10987_b200.stepper import B200HydroStepper
+
+    lr = int(os.environ.get("LOCAL_RANK", 0))
+    torch.cuda.set_device(lr)
+    dist.init_process_group("nccl", device_id=torch.device("cuda", lr))
+    rank, world = dist.get_rank(), dist.get_world_size()
+    bad = 0
+    for name, steps in (("sedov_c1", 3), ("smooth_periodic", 1)):
+        t, g = case_tree(name)
+        part = Partition(t, world, rank)
+        st = B200HydroStepper(t, EOS, HydroMode("new"), partition=part, max_run=2)
+        for s in range(steps):
+            dt = st.cfl_dt(0.4)
+            if dt != float(g["dts"][s]):
+                print(f"rank {rank} {name}: dt {dt!r} != golden {float(g['dts'][s])!r}", flush=True)
+                bad += 1
+            stats = st.rk3_step(dt)
+            if s == 0:
+                b0, b1 = part.bounds[rank], part.bounds[rank + 1]
+                mine = state_of(t)[b0:b1]
+                ref = g["state1"][b0:b1]
+                nb = int(np.count_nonzero(mine[:, :5] != ref[:, :5]))
+                ntau = int(np.count_nonzero(np.abs(mine - ref) > 1e-12 * np.abs(ref)))
+                if nb or ntau:
+                    print(f"rank {rank} {name}: {nb} rho/s/E mismatches, {ntau} beyond 1e-12", flush=True)
+                    bad += 1
+                if stats.amax != float(g["amax"][0]):
+                    print(f"rank {rank} {name}: amax {stats.amax!r} != {float(g['amax'][0])!r}", flush=True)
+                    bad += 1
+    t = torch.tensor([bad], device="cuda")
+    dist.all_reduce(t)
+    if rank == 0:
+        print(f"multi-GPU parity on {world} ranks: {'OK' if int(t.item()) == 0 else 'FAIL'}", flush=True)
+    dist.destroy_process_group()
+    sys.exit(0 if int(t.item()) == 0 else 1)
+
+
+if __name__ == "__main__":
+    main()

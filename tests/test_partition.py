@@ -1,0 +1,84 @@
+"""Leaf partition + halo exchange (the multi-GPU path) on CPU:
+partition invariants, and a world_size-2 gloo run of the emulated stage
+kernel that must reproduce the single-rank golden step bitwise."""
+
+import os
+import socket
+
+import numpy as np
+import pytest
+
+from paper_2107_10987_b200 import mesh
+from paper_2107_10987_b200.batch import OFFS, neighbor_table
+from paper_2107_10987_b200.partition import Partition
+
+
+@pytest.mark.parametrize("bnd", ["reflecting", "periodic"])
+@pytest.mark.parametrize("world", [2, 3, 8])
+def test_partition_invariants(bnd, world):
+    t = mesh.build_uniform_tree(2, 8, boundary=bnd)
+    parts = [Partition(t, world, r) for r in range(world)]
+    G = len(t.leaves())
+    assert sum(p.nown for p in parts) == G
+    for r, p in enumerate(parts):
+        local = set(int(g) for g in p.gids)
+        for g in range(p.bounds[r], p.bounds[r + 1]):
+            for j in p.gnbr[g]:
+                if j >= 0:
+                    assert int(j) in local  # every neighbour is owned or in the halo
+        for s in range(world):
+            assert p.recv_counts[s] == parts[s].send_counts[r]
+            if s != r:
+                # what s sends to r is exactly r's halo block from s, same order
+                blk = p.halo[parts[0].owner[p.halo] == s]
+                assert np.array_equal(blk, parts[s].send[r])
+        b = p.batch(t)
+        assert sorted(b.run_leaf.tolist()) == list(range(p.nown))
+
+
+def test_neighbor_table_fast_path_matches_generic():
+    for bnd in ("reflecting", "periodic", "outflow"):
+        t = mesh.build_uniform_tree(2, 8, boundary=bnd)
+        leaves = t.sorted_leaves()
+        fast = neighbor_table(t, leaves)
+        for i, lf in enumerate(leaves):
+            for q, o in enumerate(OFFS):
+                pos = t.neighbor_ipos(lf, o)
+                want = -1 if pos is None else leaves.index(t.find_leaf_region(lf.level, pos)[0][0])
+                assert fast[i, q] == want
+
+
+def _worker(rank, world, port, out):
+    import torch.distributed as dist
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from _cases import case_tree, state_of
+        from emu import EmuDistStepper
+
+        t, g = case_tree("sedov_c1")
+        st = EmuDistStepper(t, 1.4, world, rank, max_run=2)
+        st.rk3_step(float(g["dts"][0]))
+        mine = state_of(t)[st.part.bounds[rank]:st.part.bounds[rank + 1]]
+        ref = g["state1"][st.part.bounds[rank]:st.part.bounds[rank + 1]]
+        np.save(os.path.join(out, f"r{rank}.npy"), np.array([np.count_nonzero(mine != ref)]))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_two_rank_gloo_step_bitwise(tmp_path):
+    import sys
+
+    import torch.multiprocessing as mp
+
+    here = os.path.dirname(os.path.abspath(__file__))
+    if here not in sys.path:
+        sys.path.insert(0, here)
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    mp.spawn(_worker, args=(2, port, str(tmp_path)), nprocs=2, join=True)
+    for r in range(2):
+        assert int(np.load(tmp_path / f"r{r}.npy")[0]) == 0
