@@ -292,7 +292,7 @@ def gpu_arm(args, rank, world):
         "ms_per_step": ms / K, "higher_is_better": True, "scaling": "weak" if world == 1 else "strong",
         "vs_baseline": None,
         "dtype": "f64", "data": "synthetic (init_sedov Sedov-Taylor, no RNG)",
-        "config": {"workload": f"sedov_uniform_L{level}_n8: {st.batch.L} sub-grids of 8^3 = {cells} cells "
+        "config": {"workload": f"sedov_uniform_L{level}_n8: {st.nglobal} sub-grids of 8^3 = {cells} cells "
                                f"({int(round(cells ** (1 / 3)))}^3), reflecting, cfl 0.4, scheme new",
                    "step": "cfl_dt + 3 fused RK stages, dt on device",
                    "l2": "working set (3 x 6 x cells x 8 B = %.0f MB) > 126 MB L2; no flush" % (3 * 48 * cells / 1e6),

@@ -64,9 +64,12 @@ OMB_HD double dmax(double a, double b) { return fmax(a, b); }
 // ---------------------------------------------------------------------------
 
 // interface value between cells a (=c) and ap1 (=c+d), stencil c-d .. c+2d
+// The clamp bounds use glibc's fmin/fmax tie rule ((x<y)?x:y, (x>y)?x:y) as
+// plain selects: NaN handling cannot matter here because any NaN among the
+// four inputs already makes v7 NaN, which no comparison changes.
 OMB_HD double iface(double am1, double a, double ap1, double ap2) {
   double v7 = (7.0 / 12.0) * (a + ap1) - (1.0 / 12.0) * (am1 + ap2);
-  double mn = dmin(a, ap1), mx = dmax(a, ap1);
+  double mn = a < ap1 ? a : ap1, mx = a > ap1 ? a : ap1;
   if (v7 < mn) v7 = mn;
   if (v7 > mx) v7 = mx;
   return v7;

@@ -52,6 +52,42 @@ OMB_HD void used_range(int l, int& ylo, int& yhi, int& zlo, int& zhi) {
 }
 
 OMB_HD int pos10(int y, int z) { return (y - 2) * 10 + (z - 2); }
+
+// Item order of the 100 lo/hi positions of a plane for one line: positions
+// whose lo or hi feeds a flux come first (a rectangle), the rest -- needed
+// only for the reference's positivity-fallback count, i.e. only rho and p --
+// last, so whole warps take the 2-field path.  shape: 0 = [3,10]^2 (line 0),
+// 1 = y in [2,11] x z in [3,10] (lines 1,3,4), 2 = y in [3,10] x z in [2,11]
+// (lines 2,5,6), 3 = all (diagonals 7..12).
+OMB_HD int line_shape(int l) {
+  if (l == 0) return 0;
+  if (l == 1 || l == 3 || l == 4) return 1;
+  if (l == 2 || l == 5 || l == 6) return 2;
+  return 3;
+}
+OMB_HD int shape_needed(int sh) { return sh == 0 ? 64 : (sh == 3 ? 100 : 80); }
+OMB_HD void shape_pos(int sh, int i, int& y, int& z) {
+  if (sh == 3) { y = 2 + i / 10; z = 2 + i % 10; return; }
+  if (sh == 0) {
+    if (i < 64) { y = 3 + i / 8; z = 3 + i % 8; return; }
+    int j = i - 64;
+    if (j < 10) { y = 2; z = 2 + j; return; }
+    if (j < 20) { y = 11; z = 2 + j - 10; return; }
+    int k = j - 20;
+    y = 3 + k / 2; z = (k & 1) ? 11 : 2;
+    return;
+  }
+  if (sh == 1) {
+    if (i < 80) { y = 2 + i / 8; z = 3 + i % 8; return; }
+    int j = i - 80;
+    y = 2 + j / 2; z = (j & 1) ? 11 : 2;
+    return;
+  }
+  if (i < 80) { y = 3 + i / 10; z = 2 + i % 10; return; }
+  int j = i - 80;
+  if (j < 10) { y = 2; z = 2 + j; return; }
+  y = 11; z = 2 + j - 10;
+}
 OMB_HD int yslot(int y, int z) { return (y - 2) * 8 + (z - 3); }
 OMB_HD int zslot(int y, int z) { return (y - 3) * 9 + (z - 2); }
 OMB_HD int cslot(int a, int b) { return (a - 2) * 9 + (b - 2); }
@@ -215,17 +251,25 @@ struct Stage {
 
   // monotonised lo/hi of 6 fields at (X, y, z) along line l, with contact
   // steepening and the positivity fallback (_core.pyx:61-155 for one cell)
-  OMB_HD void mono6(int l, int X, int y, int z, double* lo, double* hi) {
+  // full = false: only rho and p (fields 0, 4) are reconstructed -- enough
+  // for the fallback count when nothing consumes this cell's lo/hi
+  OMB_HD void mono6(int l, int X, int y, int z, double* lo, double* hi, bool full = true) {
     int dx = ldx(l), dy = ldy(l), dz = ldz(l);
-    int o[5];
+    int c0 = y * M + z, dd = dy * M + dz;
+    int ad[5];
 #pragma unroll
-    for (int k = 0; k < 5; k++) o[k] = (y + (k - 2) * dy) * M + (z + (k - 2) * dz);
+    for (int k = 0; k < 5; k++) ad[k] = (dx ? ring[k] : ring[2]) + c0 + (k - 2) * dd;
     double rr[5] = {0, 0, 0, 0, 0}, pm1 = 0, pp1 = 0;
 #pragma unroll
     for (int v = 0; v < NF; v++) {
+      if (!full && v != 0 && v != 4) {
+        lo[v] = 0.0;
+        hi[v] = 0.0;
+        continue;
+      }
       double s[5];
 #pragma unroll
-      for (int k = 0; k < 5; k++) s[k] = S[(dx ? ring[k] : ring[2]) + v * PL + o[k]];
+      for (int k = 0; k < 5; k++) s[k] = S[ad[k] + v * PL];
       double lv = iface(s[0], s[1], s[2], s[3]);
       double hv = iface(s[1], s[2], s[3], s[4]);
       mono(s[2], lv, hv);
@@ -240,12 +284,12 @@ struct Stage {
     if (lo[0] <= 0.0 || lo[4] <= 0.0) {
       fb += mult(X);
 #pragma unroll
-      for (int v = 0; v < NF; v++) lo[v] = ringp(2, v)[o[2]];
+      for (int v = 0; v < NF; v++) lo[v] = S[ad[2] + v * PL];
     }
     if (hi[0] <= 0.0 || hi[4] <= 0.0) {
       fb += mult(X);
 #pragma unroll
-      for (int v = 0; v < NF; v++) hi[v] = ringp(2, v)[o[2]];
+      for (int v = 0; v < NF; v++) hi[v] = S[ad[2] + v * PL];
     }
   }
 
@@ -270,11 +314,13 @@ struct Stage {
     for (int k = 0; k < 2; k++) {
       int it = tid + k * nthr;
       if (it >= nitems) break;
-      int dl = dl0 + it / NP, pos = it % NP;
+      int dl = dl0 + it / NP, i = it % NP;
       int l = dl_line(dl);
-      int y = 2 + pos / 10, z = 2 + pos % 10;
+      int sh = line_shape(l), y, z;
+      shape_pos(sh, i, y, z);
+      int pos = pos10(y, z);
       double lo[NF], hi[NF];
-      mono6(l, X, y, z, lo, hi);
+      mono6(l, X, y, z, lo, hi, i < shape_needed(sh));
       if (k == 0) {
 #pragma unroll
         for (int v = 0; v < NF; v++) h.h0[v] = hi[v];
@@ -378,9 +424,12 @@ struct Stage {
   OMB_HD void inplane_lines(int tid, int nthr) {
     int nip = A.new_mode ? 4 : 2;
     for (int it = tid; it < nip * NP; it += nthr) {
-      int ip = it / NP, pos = it % NP, l = ip_line(ip);
+      int ip = it / NP, i = it % NP, l = ip_line(ip);
+      int sh = line_shape(l), y, z;
+      shape_pos(sh, i, y, z);
+      int pos = pos10(y, z);
       double lo[NF], hi[NF];
-      mono6(l, X, 2 + pos / 10, 2 + pos % 10, lo, hi);
+      mono6(l, X, y, z, lo, hi, i < shape_needed(sh));
 #pragma unroll
       for (int v = 0; v < NF; v++) {
         S[Smem::LHI + ((ip * 2 + 0) * NF + v) * NP + pos] = lo[v];
