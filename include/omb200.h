@@ -83,6 +83,8 @@ int omb_cfl(const OmbCflDesc *desc, void *stream);
  * unpack such a message into leaf slots first..first+n of a state */
 int omb_pack_leaves(const double *u, long long fstride, const int *idx, int n, double *out, void *stream);
 int omb_unpack_leaves(const double *in, int n, double *u, long long fstride, int first, void *stream);
+/* self-test: counts (into *bad) quotients where the kernels' reciprocal-based division differs from IEEE */
+int omb_selftest_div(unsigned long long seed, long long n, unsigned long long *bad, void *stream);
 /* FP64 DFMA throughput probe (roofline denominator): blocks*256*8*iters DFMAs */
 int omb_fp64_peak(double *scratch, int blocks, int iters, void *stream);
 /* padded (6,14,14,14) conserved block of one leaf as the ghost fill would produce it */

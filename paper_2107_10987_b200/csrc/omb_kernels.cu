@@ -179,8 +179,8 @@ __global__ void k_fluxes(const double* __restrict__ lo, const double* __restrict
           wQ[v] = lo[((long long)l * NF + v) * nc + Q];
         }
         KtState sP, sQ;
-        kt_state(wP, gamma, gm1, sP);
-        kt_state(wQ, gamma, gm1, sQ);
+        kt_state(wP, gamma, gm1, 1.0 / gm1, sP);
+        kt_state(wQ, gamma, gm1, 1.0 / gm1, sQ);
         double fv[NF];
         double sp = kt_axis(sP, sQ, axis, T.flip[rr0 + r] != 0, fv);
         if (sp > amax) amax = sp;
@@ -409,6 +409,28 @@ __global__ void k_unpack(const double* __restrict__ in, int n, double* __restric
   }
 }
 
+// self-test of div_by (Markstein quotient) against the IEEE division on
+// random operands spanning 2^[-60,60] with random signs, 1 in 8 numerators 0
+__global__ void k_selftest_div(unsigned long long seed, long long n, unsigned long long* bad) {
+  unsigned long long s = seed ^ (0x9E3779B97F4A7C15ull * (blockIdx.x * blockDim.x + threadIdx.x + 1));
+  unsigned long long nb = 0;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+    double x[2];
+    for (int j = 0; j < 2; j++) {
+      s ^= s << 13; s ^= s >> 7; s ^= s << 17;
+      unsigned long long m = s & 0xFFFFFFFFFFFFFull;
+      int e = (int)((s >> 52) % 121) - 60;
+      unsigned long long bits = ((unsigned long long)(e + 1023) << 52) | m | ((s >> 63) << 63);
+      x[j] = __longlong_as_double((long long)bits);
+    }
+    if ((s & 7) == 0) x[0] = 0.0;
+    double q = __ddiv_rn(x[0], x[1]);
+    double m = div_by(x[0], x[1], __ddiv_rn(1.0, x[1]));
+    if (__double_as_longlong(q) != __double_as_longlong(m)) nb++;
+  }
+  if (nb) atomicAdd(bad, nb);
+}
+
 // FP64 pipe peak probe (roofline denominator; MEASURED_PEAKS.json has no FP64 entry):
 // 8 independent DFMA chains per thread, 2 flops per DFMA.
 __global__ void k_dfma_peak(double* out, int iters) {
@@ -492,6 +514,7 @@ int omb_stage(const OmbStageDesc* d, void* stream) {
   A.b = d->b;
   A.gamma = d->gamma;
   A.gm1 = d->gm1;
+  A.inv_gm1 = 1.0 / d->gm1;
   A.eta = d->eta;
   A.inv_gamma = d->inv_gamma;
   A.omega = d->omega;
@@ -539,6 +562,12 @@ int omb_unpack_leaves(const double* in, int n, double* U, long long fstride, int
   int blocks = (int)((total + 255) / 256);
   k_unpack<<<blocks < 148 * 16 ? blocks : 148 * 16, 256, 0, (cudaStream_t)stream>>>(in, n, U, fstride, first);
   CK(cudaGetLastError(), "omb_unpack_leaves launch");
+  return 0;
+}
+
+int omb_selftest_div(unsigned long long seed, long long n, unsigned long long* bad, void* stream) {
+  k_selftest_div<<<148 * 8, 256, 0, (cudaStream_t)stream>>>(seed, n, bad);
+  CK(cudaGetLastError(), "omb_selftest_div launch");
   return 0;
 }
 

@@ -55,6 +55,21 @@ OMB_HD double div_nz(double a, double b) {
   return z ? a * q : q;
 }
 
+// IEEE a/b from a precomputed y = RN(1/b) (Markstein): q0 = a*y, then two
+// fma corrections q <- q + (a - b q) y.  q1 is within 1 ulp of a/b, so the
+// second correction returns the correctly rounded quotient (Markstein's
+// theorem; r = a - b q is exact by fma).  Zero, non-finite and extreme-range
+// quotients (where the theorem's no-underflow premise could fail) take the
+// IEEE division instead.  Used where one divisor serves several numerators.
+OMB_HD double div_by(double a, double b, double y) {
+  double q0 = a * y;
+  double q1 = fma(fma(-b, q0, a), y, q0);
+  double q2 = fma(fma(-b, q1, a), y, q1);
+  double m = fabs(q1);
+  if (!(m > 0x1p-1000 && m < 0x1p+1000)) q2 = (a == 0.0) ? a * y : a / b;
+  return q2;
+}
+
 // NaN-faithful helpers: C fmin/fmax semantics (IEEE minNum/maxNum), as libm.
 OMB_HD double dmin(double a, double b) { return fmin(a, b); }
 OMB_HD double dmax(double a, double b) { return fmax(a, b); }
@@ -142,7 +157,7 @@ struct KtState {
   double c;                  // sqrt(gamma p / rho)
 };
 
-OMB_HD void kt_state(const double* w, double gamma, double gm1, KtState& s) {
+OMB_HD void kt_state(const double* w, double gamma, double gm1, double inv_gm1, KtState& s) {
   s.r = w[0];
   s.v[0] = w[1];
   s.v[1] = w[2];
@@ -154,7 +169,7 @@ OMB_HD void kt_state(const double* w, double gamma, double gm1, KtState& s) {
   s.u[1] = s.r * s.v[0];
   s.u[2] = s.r * s.v[1];
   s.u[3] = s.r * s.v[2];
-  s.u[4] = div_nz(s.p, gm1) + kin;
+  s.u[4] = div_by(s.p, gm1, inv_gm1) + kin;
   s.u[5] = w[5];
 }
 
@@ -176,6 +191,7 @@ OMB_HD double kt_axis(const KtState& P, const KtState& Q, int axis, bool flip, d
   double am = dmin(0.0, flip ? dmin(mQ, mP) : dmin(mP, mQ));
   double denom = ap - am;
   double apam = ap * am;
+  double rden = 1.0 / denom;  // one IEEE reciprocal for the six quotients
   double cP = flip ? -am : ap;
   double cQ = flip ? ap : -am;
   double sg = flip ? -apam : apam;
@@ -193,7 +209,7 @@ OMB_HD double kt_axis(const KtState& P, const KtState& Q, int axis, bool flip, d
       fQ = fQ + Q.p * vnQ;
     }
     double num = (cP * fP + cQ * fQ) + sg * (Q.u[v] - P.u[v]);
-    out[v] = ok ? div_nz(num, denom) : (flip ? fQ : fP);
+    out[v] = ok ? div_by(num, denom, rden) : (flip ? fQ : fP);
   }
   return dmax(ap, -am);
 }
@@ -202,7 +218,7 @@ OMB_HD double kt_axis(const KtState& P, const KtState& Q, int axis, bool flip, d
 // F = C + (4 edev + vdev)/36 with edev = (e0+e1)+(e2+e3), e_i = 0.5 acc_i - C
 OMB_HD double pdev_edge(double acc, double c) { return 0.5 * acc - c; }
 OMB_HD double pdev_vert(double acc, double c) { return 0.25 * acc - c; }
-OMB_HD double face_final(double c, double edev, double vdev) { return c + div_nz(4.0 * edev + vdev, 36.0); }
+OMB_HD double face_final(double c, double edev, double vdev) { return c + div_by(4.0 * edev + vdev, 36.0, 1.0 / 36.0); }
 // point accumulators exactly as the Cython loop builds them
 OMB_HD double edge_acc(double f0, double f1) { return (0.0 + f0) + f1; }
 OMB_HD double vert_acc(double f0, double f1, double f2, double f3) { return (0.0 + (f0 + f1)) + (f2 + f3); }

@@ -152,6 +152,7 @@ struct StageArgs {
   const double* dt;     // device scalar
   double a, b;
   double gamma, gm1, eta, inv_gamma, omega;
+  double inv_gm1;       // RN(1/gm1), host-computed
   double floor_rho, floor_tau, floor_vmax;
   int bc;               // 0 outflow, 1 reflecting, 2 periodic
   int new_mode, quad, contact;  // quad = new_mode && !override
@@ -341,8 +342,8 @@ struct Stage {
 #pragma unroll
       for (int v = 0; v < NF; v++) hp[v] = S[Smem::HI + (dl * NF + v) * NP + pp];
       KtState sP, sQ;
-      kt_state(hp, A.gamma, A.gm1, sP);
-      kt_state(lo, A.gamma, A.gm1, sQ);
+      kt_state(hp, A.gamma, A.gm1, A.inv_gm1, sP);
+      kt_state(lo, A.gamma, A.gm1, A.inv_gm1, sQ);
       // axes served by this line: x always; y for lines 3,4; z for 5,6; all for 9..12
       int ax_second = (l == 3 || l == 4) ? 1 : 2;
       int nax = l == 0 ? 1 : (l >= 9 ? 3 : 2);
@@ -442,7 +443,7 @@ struct Stage {
     double w[NF];
 #pragma unroll
     for (int v = 0; v < NF; v++) w[v] = S[Smem::LHI + ((ip * 2 + side) * NF + v) * NP + pos10(y, z)];
-    kt_state(w, A.gamma, A.gm1, s);
+    kt_state(w, A.gamma, A.gm1, A.inv_gm1, s);
   }
 
   // ---- P4: in-plane fluxes (y/z face centres, y/z edge points) -----------

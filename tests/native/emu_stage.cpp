@@ -17,7 +17,7 @@ extern "C" int emu_stage(const OmbStageDesc* d, int nthr) {
   StageArgs A;
   A.ucur = d->ucur; A.u0 = d->u0; A.unext = d->unext; A.grav = d->grav; A.fstride = d->fstride;
   A.info = (const LeafInfo*)d->info; A.run_off = d->run_off; A.run_leaf = d->run_leaf; A.dt = d->dt;
-  A.a = d->a; A.b = d->b; A.gamma = d->gamma; A.gm1 = d->gm1; A.eta = d->eta; A.inv_gamma = d->inv_gamma;
+  A.a = d->a; A.b = d->b; A.gamma = d->gamma; A.gm1 = d->gm1; A.inv_gm1 = 1.0 / d->gm1; A.eta = d->eta; A.inv_gamma = d->inv_gamma;
   A.omega = d->omega; A.floor_rho = d->floor_rho; A.floor_tau = d->floor_tau; A.floor_vmax = d->floor_vmax;
   A.bc = d->bc; A.new_mode = d->new_mode; A.quad = d->new_mode && !d->override_center; A.contact = d->contact;
   A.amax_bits = d->amax_bits; A.fallback = d->fallback;

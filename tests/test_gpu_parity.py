@@ -186,3 +186,19 @@ def test_non_finite_speed_raises():
     st = _stepper(t)
     with pytest.raises(NumericsError, match="non-finite wave speed"):
         st.cfl_dt(0.4)
+
+
+def test_reciprocal_division_is_ieee_exact():
+    """div_by (one reciprocal + two fma corrections, used for the six KT
+    quotients) must equal IEEE division bit for bit: 2^30 random pairs."""
+    import ctypes
+
+    import torch
+
+    from paper_2107_10987_b200 import _lib
+
+    L = _lib.load()
+    bad = torch.zeros(1, dtype=torch.int64, device="cuda")
+    _lib.check(L.omb_selftest_div(12345, 1 << 30, bad.data_ptr(),
+                                  ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)), "selftest")
+    assert int(bad.item()) == 0
