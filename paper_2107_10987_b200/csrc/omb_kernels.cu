@@ -493,12 +493,14 @@ int omb_stage(const OmbStageDesc* d, void* stream) {
     CK(cudaFuncSetAttribute(k_stage<512>, cudaFuncAttributeMaxDynamicSharedMemorySize, Smem::BYTES), "smem attribute");
     CK(cudaFuncSetAttribute(k_stage<384>, cudaFuncAttributeMaxDynamicSharedMemorySize, Smem::BYTES), "smem attribute");
     CK(cudaFuncSetAttribute(k_stage<256>, cudaFuncAttributeMaxDynamicSharedMemorySize, Smem::BYTES), "smem attribute");
+    CK(cudaFuncSetAttribute(k_stage<576>, cudaFuncAttributeMaxDynamicSharedMemorySize, Smem::BYTES), "smem attribute");
+    CK(cudaFuncSetAttribute(k_stage<640>, cudaFuncAttributeMaxDynamicSharedMemorySize, Smem::BYTES), "smem attribute");
     attr_set = true;
   }
   static int nt = [] {
     const char* e = getenv("OMB_STAGE_THREADS");
     int v = e ? atoi(e) : 512;
-    return (v == 256 || v == 384) ? v : 512;
+    return (v == 256 || v == 384 || v == 576 || v == 640) ? v : 512;
   }();
   StageArgs A;
   A.ucur = d->ucur;
@@ -530,6 +532,8 @@ int omb_stage(const OmbStageDesc* d, void* stream) {
   if (d->nruns <= 0) return 0;
   if (nt == 512) k_stage<512><<<d->nruns, 512, Smem::BYTES, (cudaStream_t)stream>>>(A);
   else if (nt == 384) k_stage<384><<<d->nruns, 384, Smem::BYTES, (cudaStream_t)stream>>>(A);
+  else if (nt == 576) k_stage<576><<<d->nruns, 576, Smem::BYTES, (cudaStream_t)stream>>>(A);
+  else if (nt == 640) k_stage<640><<<d->nruns, 640, Smem::BYTES, (cudaStream_t)stream>>>(A);
   else k_stage<256><<<d->nruns, 256, Smem::BYTES, (cudaStream_t)stream>>>(A);
   CK(cudaGetLastError(), "omb_stage launch");
   return 0;
