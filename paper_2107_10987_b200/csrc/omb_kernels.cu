@@ -275,16 +275,16 @@ __global__ void __launch_bounds__(NT, 1) k_stage(StageArgs A) {
       st.set_plane(X);
     }
     __syncthreads();
-    st.template boundary_lines<0>(tid, nthr, h);
-    __syncthreads();
-    st.store_hi(h);
-    if (X >= 3) st.combine_A(tid, nthr);
-    __syncthreads();
-    if (A.new_mode) {
-      st.template boundary_lines<1>(tid, nthr, h);
+    const int ngroups = A.new_mode ? 2 : 1;
+#pragma unroll 1
+    for (int g = 0; g < ngroups; g++) {
+      st.boundary_lines(g, tid, nthr, h);
       __syncthreads();
       st.store_hi(h);
-      if (X >= 3 && A.quad) st.combine_B(tid, nthr);
+      if (X >= 3) {
+        if (g == 0) st.combine_A(tid, nthr);
+        else if (A.quad) st.combine_B(tid, nthr);
+      }
       __syncthreads();
     }
     st.inplane_lines(tid, nthr);

@@ -307,12 +307,7 @@ struct Stage {
   }
 
   // ---- P1: boundary lines (d.x = 1) of group g on plane X ----------------
-  // G = 0: lines 0,3,4,5,6 (1-2 axes); G = 1: body diagonals 9..12 (3 axes).
-  // A compile-time group lets the axis loop unroll so the independent
-  // per-axis reciprocal / quotient chains overlap.
-  template <int G>
-  OMB_HD void boundary_lines(int tid, int nthr, Hold& h) {
-    const int g = G;
+  OMB_HD void boundary_lines(int g, int tid, int nthr, Hold& h) {
     int dl0 = g == 0 ? 0 : 5, ndl = g == 0 ? (A.new_mode ? 5 : 1) : 4;
     int nitems = ndl * NP;
     h.s0 = h.s1 = -1;
@@ -349,15 +344,14 @@ struct Stage {
       KtState sP, sQ;
       kt_state(hp, A.gamma, A.gm1, A.inv_gm1, sP);
       kt_state(lo, A.gamma, A.gm1, A.inv_gm1, sQ);
-      if (G == 1) {
-#pragma unroll
-        for (int ax = 0; ax < 3; ax++) kt_into(sP, sQ, l, ax, S + Smem::RAWB + (chB(l, ax) * NF) * NP + pp, NP);
-      } else {
-        kt_into(sP, sQ, l, 0, S + Smem::RAWA + (chA(l, 0) * NF) * NP + pp, NP);
-        if (l != 0) {
-          int ax2 = (l == 3 || l == 4) ? 1 : 2;
-          kt_into(sP, sQ, l, ax2, S + Smem::RAWA + (chA(l, ax2) * NF) * NP + pp, NP);
-        }
+      // axes served by this line: x always; y for lines 3,4; z for 5,6; all for 9..12
+      int ax_second = (l == 3 || l == 4) ? 1 : 2;
+      int nax = l == 0 ? 1 : (l >= 9 ? 3 : 2);
+#pragma unroll 1
+      for (int q = 0; q < nax; q++) {
+        int ax = q == 0 ? 0 : (l >= 9 ? q : ax_second);
+        double* dst = g == 0 ? S + Smem::RAWA + (chA(l, ax) * NF) * NP + pp : S + Smem::RAWB + (chB(l, ax) * NF) * NP + pp;
+        kt_into(sP, sQ, l, ax, dst, NP);
       }
     }
   }

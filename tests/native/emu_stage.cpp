@@ -39,10 +39,10 @@ extern "C" int emu_stage(const OmbStageDesc* d, int nthr) {
       ALL(s.set_plane(X));
       ALL(if (X + 2 < 8 * R + 6) s.load_plane(X + 2, t, nthr);
           if (X >= 3 && s.interior(X - 2)) { s.set_plane(X - 1); s.update_plane(t, nthr); s.set_plane(X); });
-      ALL(s.template boundary_lines<0>(t, nthr, h[t]));
+      ALL(s.boundary_lines(0, t, nthr, h[t]));
       ALL(s.store_hi(h[t]); if (X >= 3) s.combine_A(t, nthr));
       if (A.new_mode) {
-        ALL(s.template boundary_lines<1>(t, nthr, h[t]));
+        ALL(s.boundary_lines(1, t, nthr, h[t]));
         ALL(s.store_hi(h[t]); if (X >= 3 && A.quad) s.combine_B(t, nthr));
       }
       ALL(s.inplane_lines(t, nthr));
