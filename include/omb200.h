@@ -85,6 +85,10 @@ int omb_pack_leaves(const double *u, long long fstride, const int *idx, int n, d
 int omb_unpack_leaves(const double *in, int n, double *u, long long fstride, int first, void *stream);
 /* self-test: counts (into *bad) quotients where the kernels' reciprocal-based division differs from IEEE */
 int omb_selftest_div(unsigned long long seed, long long n, unsigned long long *bad, void *stream);
+/* host (CPU) packing between per-leaf padded arrays (6, n+6, n+6, n+6) -- SubGrid.u, tree.py:47-61 --
+ * and the [6][L][n^3] device layout; multithreaded, used around H2D/D2H copies */
+int omb_host_pack(const double *const *leaf_u, int L, int n, double *out);
+int omb_host_unpack(const double *in, int L, int n, double *const *leaf_u);
 /* FP64 DFMA throughput probe (roofline denominator): blocks*256*8*iters DFMAs */
 int omb_fp64_peak(double *scratch, int blocks, int iters, void *stream);
 /* padded (6,14,14,14) conserved block of one leaf as the ghost fill would produce it */

@@ -16,7 +16,7 @@ ABI_VERSION = 1
 _lib = None
 
 EXPORTS = ("omb_abi_version", "omb_last_error", "omb_stage_smem_bytes", "omb_primitives", "omb_reconstruct",
-           "omb_fluxes", "omb_stage", "omb_cfl", "omb_gather", "omb_fp64_peak", "omb_pack_leaves", "omb_unpack_leaves", "omb_selftest_div")
+           "omb_fluxes", "omb_stage", "omb_cfl", "omb_gather", "omb_fp64_peak", "omb_pack_leaves", "omb_unpack_leaves", "omb_selftest_div", "omb_host_pack", "omb_host_unpack")
 
 
 def load():
@@ -40,6 +40,8 @@ def load():
     L.omb_pack_leaves.argtypes = [vp, ll, vp, i, vp, vp]
     L.omb_unpack_leaves.argtypes = [vp, i, vp, ll, i, vp]
     L.omb_selftest_div.argtypes = [ctypes.c_ulonglong, ll, vp, vp]
+    L.omb_host_pack.argtypes = [vp, i, i, vp]
+    L.omb_host_unpack.argtypes = [vp, i, i, vp]
     for fn in EXPORTS[3:]:
         getattr(L, fn).restype = i
     if L.omb_abi_version() != ABI_VERSION:

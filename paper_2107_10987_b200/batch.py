@@ -150,14 +150,32 @@ class LeafBatch:
         self.nruns = len(runs)
 
     # -- host <-> packed state --------------------------------------------------
-    def pack(self, out=None):
+    def _leaf_ptrs(self, count):
+        ptrs = np.empty(count, dtype=np.uintp)
+        for i, lf in enumerate(self.leaves[:count]):
+            u = lf.subgrid.u
+            if not (u.flags.c_contiguous and u.dtype == np.float64):
+                return None
+            ptrs[i] = u.__array_interface__["data"][0]
+        return ptrs
+
+    def pack(self, out=None, lib=None):
+        """Interiors of all batch leaves into ``out`` ([6][L][8][8][8])."""
         U = out if out is not None else np.empty((NFIELDS, self.L, 8, 8, 8))
+        ptrs = self._leaf_ptrs(self.L) if lib is not None else None
+        if ptrs is not None and U.flags.c_contiguous:
+            lib.omb_host_pack(ptrs.ctypes.data, self.L, 8, U.ctypes.data)
+            return U
         for i, lf in enumerate(self.leaves):
             U[:, i] = lf.subgrid.interior
         return U
 
-    def unpack(self, U):
+    def unpack(self, U, lib=None):
         """Write the computed leaves back (halo leaves belong to other ranks)."""
+        ptrs = self._leaf_ptrs(self.ncompute) if lib is not None else None
+        if ptrs is not None and U.flags.c_contiguous and self.ncompute == self.L:
+            lib.omb_host_unpack(U.ctypes.data, self.L, 8, ptrs.ctypes.data)
+            return
         for i, lf in enumerate(self.leaves[:self.ncompute]):
             lf.subgrid.interior[:] = U[:, i]
 

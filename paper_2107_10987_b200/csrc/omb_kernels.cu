@@ -7,6 +7,8 @@
 #include <string.h>
 
 #include <mutex>
+#include <thread>
+#include <vector>
 #include <string>
 
 #include "../../include/omb200.h"
@@ -572,6 +574,45 @@ int omb_unpack_leaves(const double* in, int n, double* U, long long fstride, int
 int omb_selftest_div(unsigned long long seed, long long n, unsigned long long* bad, void* stream) {
   k_selftest_div<<<148 * 8, 256, 0, (cudaStream_t)stream>>>(seed, n, bad);
   CK(cudaGetLastError(), "omb_selftest_div launch");
+  return 0;
+}
+
+// host-side packing of the per-leaf padded arrays (the reference's SubGrid.u,
+// (6, m, m, m) C-contiguous) into / out of the [6][L][n^3] device layout;
+// multithreaded memcpy of n-element rows
+static void host_copy(const double* const* leaf_u, int L, int n, double* packed, bool to_packed) {
+  int m = n + 6;
+  long long n3 = (long long)n * n * n;
+  unsigned nt = std::thread::hardware_concurrency();
+  if (nt == 0) nt = 1;
+  if (nt > 16) nt = 16;
+  if ((long long)nt > L) nt = L > 0 ? (unsigned)L : 1u;
+  auto work = [&](int lo, int hi) {
+    for (int i = lo; i < hi; i++) {
+      const double* u = leaf_u[i];
+      for (int v = 0; v < 6; v++)
+        for (int x = 0; x < n; x++)
+          for (int y = 0; y < n; y++) {
+            double* p = packed + ((long long)v * L + i) * n3 + ((long long)x * n + y) * n;
+            double* q = const_cast<double*>(u) + (((long long)v * m + x + 3) * m + y + 3) * m + 3;
+            if (to_packed) memcpy(p, q, sizeof(double) * n);
+            else memcpy(q, p, sizeof(double) * n);
+          }
+    }
+  };
+  std::vector<std::thread> th;
+  for (unsigned t = 1; t < nt; t++) th.emplace_back(work, (int)((long long)L * t / nt), (int)((long long)L * (t + 1) / nt));
+  work(0, (int)((long long)L / nt));
+  for (auto& x : th) x.join();
+}
+
+int omb_host_pack(const double* const* leaf_u, int L, int n, double* out) {
+  host_copy(leaf_u, L, n, out, true);
+  return 0;
+}
+
+int omb_host_unpack(const double* in, int L, int n, double* const* leaf_u) {
+  host_copy((const double* const*)leaf_u, L, n, const_cast<double*>(in), false);
   return 0;
 }
 

@@ -97,14 +97,14 @@ class B200HydroStepper:
         """Copy the host leaves' interiors into the device state."""
         b = self.batch
         host = self._pinned.numpy().reshape(6, b.L, 8, 8, 8)
-        b.pack(out=host)
+        b.pack(out=host, lib=self.lib)
         self._buf[self._state].copy_(self._pinned, non_blocking=True)
 
     def download(self):
         """Copy the device state back into the host leaves."""
         b = self.batch
         self._pinned.copy_(self._buf[self._state])
-        b.unpack(self._pinned.numpy().reshape(6, b.L, 8, 8, 8))
+        b.unpack(self._pinned.numpy().reshape(6, b.L, 8, 8, 8), lib=self.lib)
 
     def state_tensor(self):
         return self._buf[self._state]
