@@ -264,19 +264,28 @@ __global__ void __launch_bounds__(NT, 1) k_stage(StageArgs A) {
   st.fb = 0;
   Hold h;
   const int R = st.R;
+  // prologue: planes 0..3 synchronously, plane 4 staged asynchronously
   for (int X = 0; X < 4; X++) st.load_plane(X, tid, nthr);
+  st.prefetch_plane(4, tid, nthr);
+  async_commit();
+  async_wait_all();
   __syncthreads();
   for (int X = 2; X < 8 * R + 4; X++) {
     st.set_plane(X);
-    // P0 of this step shares a phase with P6 of the previous one: the load
-    // writes the ring slot of plane X-3, the update reads only FX/FYZ
-    if (X + 2 < 8 * R + 6) st.load_plane(X + 2, tid, nthr);
+    // P0 of this step shares a phase with P6 of the previous one (update of
+    // plane X-2): the conversion writes the ring slot of plane X-3, the
+    // update reads FX/FYZ and its staged inputs
+    if (X + 2 < 8 * R + 6) st.convert_plane(X + 2, tid, nthr);
     if (X >= 3 && st.interior(X - 2)) {
       st.set_plane(X - 1);
       st.update_plane(tid, nthr);
       st.set_plane(X);
     }
     __syncthreads();
+    // stage next step's inputs while this step computes (cp.async)
+    if (X + 3 < 8 * R + 6) st.prefetch_plane(X + 3, tid, nthr);
+    if (st.interior(X - 1)) st.prefetch_update(X - 1, tid, nthr);
+    async_commit();
     const int ngroups = A.new_mode ? 2 : 1;
 #pragma unroll 1
     for (int g = 0; g < ngroups; g++) {
@@ -294,6 +303,7 @@ __global__ void __launch_bounds__(NT, 1) k_stage(StageArgs A) {
     if (st.interior(X)) st.inplane_fluxes(tid, nthr);
     __syncthreads();
     if (X >= 3) st.faces_yz(tid, nthr);
+    async_wait_all();
     __syncthreads();
   }
   // P6 of the last plane

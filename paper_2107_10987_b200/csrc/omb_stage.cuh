@@ -129,10 +129,34 @@ struct Smem {
   static constexpr int BV = BZE + NF * NZF;          // [2][6][81]
   static constexpr int FP = BV + 2 * NF * NCOR;      // [2][4][6][72]
   static constexpr int FYZ = FP + 2 * 4 * NF * NYF;  // [2][6][72]
-  static constexpr int TOTAL = FYZ + 2 * NF * NYF;
+  static constexpr int SG0 = FYZ + 2 * NF * NYF;    // [6][196] staged conserved plane (next P0)
+  static constexpr int SG6 = SG0 + NF * PL;          // [16][64] staged cur(6) u0(6) grav(4) (next P6)
+  static constexpr int TOTAL = SG6 + 16 * NFACEX;
   static constexpr int BYTES = TOTAL * 8;
 };
 static_assert(Smem::BYTES <= 232448, "stage shared memory exceeds 227 KB");
+
+// 8-byte global -> shared asynchronous copy (cp.async / LDGSTS on the GPU,
+// an immediate copy in the host emulation), completed by async_wait_all()
+// followed by a barrier.
+OMB_HD void async_copy8(double* dst_smem, const double* src) {
+#ifdef __CUDA_ARCH__
+  unsigned sa = (unsigned)__cvta_generic_to_shared(dst_smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sa), "l"(src) : "memory");
+#else
+  *dst_smem = *src;
+#endif
+}
+OMB_HD void async_commit() {
+#ifdef __CUDA_ARCH__
+  asm volatile("cp.async.commit_group;\n" ::: "memory");
+#endif
+}
+OMB_HD void async_wait_all() {
+#ifdef __CUDA_ARCH__
+  asm volatile("cp.async.wait_all;\n" ::: "memory");
+#endif
+}
 
 struct LeafInfo {
   int nbr[27];    // batch index of the same-level neighbour for each offset, -1 none
@@ -164,10 +188,10 @@ struct StageArgs {
 // mesh/ghosts.py:115-150 fills it for same-level neighbours and physical
 // boundaries: region per axis, off-domain axes remapped (mirror for
 // reflecting walls with the normal momentum negated, clamp for outflow).
-OMB_HD void gather_cell(const double* U, long long fstride, const LeafInfo& LI, int bc, int cx, int cy, int cz,
-                        double* u) {
+OMB_HD long long gather_addr(const LeafInfo& LI, int bc, int cx, int cy, int cz, int& flipmask) {
   int c[3] = {cx, cy, cz};
-  int rd[3], idx[3], flipmask = 0;
+  int rd[3], idx[3];
+  flipmask = 0;
 #pragma unroll
   for (int a = 0; a < 3; a++) {
     int rr = c[a] < 3 ? -1 : (c[a] >= 3 + N ? 1 : 0);
@@ -186,7 +210,13 @@ OMB_HD void gather_cell(const double* U, long long fstride, const LeafInfo& LI, 
     }
   }
   int src = LI.nbr[(rd[0] + 1) * 9 + (rd[1] + 1) * 3 + (rd[2] + 1)];
-  long long base = (long long)src * 512 + (idx[0] * 64 + idx[1] * 8 + idx[2]);
+  return (long long)src * 512 + (idx[0] * 64 + idx[1] * 8 + idx[2]);
+}
+
+OMB_HD void gather_cell(const double* U, long long fstride, const LeafInfo& LI, int bc, int cx, int cy, int cz,
+                        double* u) {
+  int flipmask;
+  long long base = gather_addr(LI, bc, cx, cy, cz, flipmask);
 #pragma unroll
   for (int v = 0; v < NF; v++) u[v] = U[v * fstride + base];
 #pragma unroll
@@ -237,7 +267,7 @@ struct Stage {
     leaf = leaves[r];
   }
 
-  OMB_HD void load_plane(int X, int tid, int nthr) {
+  OMB_HD void load_plane(int X, int tid, int nthr) {  // synchronous (prologue)
     int leaf, lx;
     view_of(X, leaf, lx);
     const LeafInfo& LI = A.info[leaf];
@@ -247,6 +277,57 @@ struct Stage {
       prim_cell(u, A.gamma, A.gm1, A.eta, w);
 #pragma unroll
       for (int v = 0; v < NF; v++) prp(X, v)[it] = w[v];
+    }
+  }
+
+  // issue the asynchronous gather of padded plane Xn into SG0
+  OMB_HD void prefetch_plane(int Xn, int tid, int nthr) {
+    int leaf, lx;
+    view_of(Xn, leaf, lx);
+    const LeafInfo& LI = A.info[leaf];
+    for (int it = tid; it < PL; it += nthr) {
+      int fm;
+      long long base = gather_addr(LI, A.bc, lx, it / M, it % M, fm);
+#pragma unroll
+      for (int v = 0; v < NF; v++) async_copy8(S + Smem::SG0 + v * PL + it, A.ucur + v * A.fstride + base);
+    }
+  }
+
+  // P0: primitives of the staged plane Xn into the ring (flips re-derived)
+  OMB_HD void convert_plane(int Xn, int tid, int nthr) {
+    int leaf, lx;
+    view_of(Xn, leaf, lx);
+    const LeafInfo& LI = A.info[leaf];
+    for (int it = tid; it < PL; it += nthr) {
+      int fm;
+      gather_addr(LI, A.bc, lx, it / M, it % M, fm);
+      double u[NF], w[NF];
+#pragma unroll
+      for (int v = 0; v < NF; v++) u[v] = S[Smem::SG0 + v * PL + it];
+#pragma unroll
+      for (int a = 0; a < 3; a++)
+        if ((fm >> a) & 1) u[1 + a] = -u[1 + a];
+      prim_cell(u, A.gamma, A.gm1, A.eta, w);
+#pragma unroll
+      for (int v = 0; v < NF; v++) prp(Xn, v)[it] = w[v];
+    }
+  }
+
+  // issue the asynchronous loads of cur, u0 (and gravity) of plane Xc's cells into SG6
+  OMB_HD void prefetch_update(int Xc, int tid, int nthr) {
+    int r = (Xc - 3) >> 3, lx = (Xc - 3) & 7;
+    long long base = (long long)leaves[r] * 512 + lx * 64;
+    bool grav = A.grav != nullptr;
+    for (int it = tid; it < NFACEX; it += nthr) {
+      long long cell = base + it;  // (y-3)*8 + (z-3) == it
+#pragma unroll
+      for (int v = 0; v < NF; v++) {
+        async_copy8(S + Smem::SG6 + v * NFACEX + it, A.ucur + v * A.fstride + cell);
+        async_copy8(S + Smem::SG6 + (NF + v) * NFACEX + it, A.u0 + v * A.fstride + cell);
+      }
+      if (grav)
+#pragma unroll
+        for (int k = 0; k < 4; k++) async_copy8(S + Smem::SG6 + (2 * NF + k) * NFACEX + it, A.grav + k * A.fstride + cell);
     }
   }
 
@@ -541,8 +622,8 @@ struct Stage {
       double u[NF], u0[NF], rr[NF], out[NF], g[4] = {0, 0, 0, 0};
 #pragma unroll
       for (int v = 0; v < NF; v++) {
-        u[v] = A.ucur[v * A.fstride + cell];
-        u0[v] = A.u0[v * A.fstride + cell];
+        u[v] = S[Smem::SG6 + v * NFACEX + it];
+        u0[v] = S[Smem::SG6 + (NF + v) * NFACEX + it];
         double dfx = FXhi[v * NFACEX + it] - FXlo[v * NFACEX + it];
         double dfy = S[Smem::FYZ + v * NYF + yslot(y, z)] - S[Smem::FYZ + v * NYF + yslot(y - 1, z)];
         double dfz = S[Smem::FYZ + (NF + v) * NYF + zslot(y, z)] - S[Smem::FYZ + (NF + v) * NYF + zslot(y, z - 1)];
@@ -553,7 +634,7 @@ struct Stage {
       }
       if (P.has_grav)
 #pragma unroll
-        for (int k = 0; k < 4; k++) g[k] = A.grav[k * A.fstride + cell];
+        for (int k = 0; k < 4; k++) g[k] = S[Smem::SG6 + (2 * NF + k) * NFACEX + it];
       double xc = LI.ox + LI.dx * (double)lx;
       double yc = LI.oy + LI.dx * (double)(y - 3);
       update_cell(P, u, u0, rr, xc, yc, g, out);

@@ -35,11 +35,14 @@ extern "C" int emu_stage(const OmbStageDesc* d, int nthr) {
     int R = st[0].R;
 #define ALL(stmt) for (int t = 0; t < nthr; t++) { Stage& s = st[t]; (void)s; stmt; }
     for (int X = 0; X < 4; X++) ALL(s.load_plane(X, t, nthr));
+    ALL(s.prefetch_plane(4, t, nthr));
     for (int X = 2; X < 8 * R + 4; X++) {
       ALL(s.set_plane(X));
-      ALL(if (X + 2 < 8 * R + 6) s.load_plane(X + 2, t, nthr);
+      ALL(if (X + 2 < 8 * R + 6) s.convert_plane(X + 2, t, nthr);
           if (X >= 3 && s.interior(X - 2)) { s.set_plane(X - 1); s.update_plane(t, nthr); s.set_plane(X); });
-      ALL(s.boundary_lines(0, t, nthr, h[t]));
+      ALL(if (X + 3 < 8 * R + 6) s.prefetch_plane(X + 3, t, nthr);
+          if (s.interior(X - 1)) s.prefetch_update(X - 1, t, nthr);
+          s.boundary_lines(0, t, nthr, h[t]));
       ALL(s.store_hi(h[t]); if (X >= 3) s.combine_A(t, nthr));
       if (A.new_mode) {
         ALL(s.boundary_lines(1, t, nthr, h[t]));
