@@ -272,37 +272,37 @@ __global__ void __launch_bounds__(NT, 1) k_stage(StageArgs A) {
   __syncthreads();
   for (int X = 2; X < 8 * R + 4; X++) {
     st.set_plane(X);
-    // P0 of this step shares a phase with P6 of the previous one (update of
-    // plane X-2): the conversion writes the ring slot of plane X-3, the
-    // update reads FX/FYZ and its staged inputs
-    if (X + 2 < 8 * R + 6) st.convert_plane(X + 2, tid, nthr);
-    if (X >= 3 && st.interior(X - 2)) {
-      st.set_plane(X - 1);
-      st.update_plane(tid, nthr);
-      st.set_plane(X);
-    }
+    if (X + 2 < 8 * R + 6) st.convert_plane(X + 2, tid, nthr);  // P0
     __syncthreads();
-    // stage next step's inputs while this step computes (cp.async)
-    if (X + 3 < 8 * R + 6) st.prefetch_plane(X + 3, tid, nthr);
-    if (st.interior(X - 1)) st.prefetch_update(X - 1, tid, nthr);
+    if (X + 3 < 8 * R + 6) st.prefetch_plane(X + 3, tid, nthr);  // stage next P0 (cp.async)
     async_commit();
     const int ngroups = A.new_mode ? 2 : 1;
 #pragma unroll 1
     for (int g = 0; g < ngroups; g++) {
-      st.boundary_lines(g, tid, nthr, h);
+      st.boundary_lines(g, tid, nthr, h);  // P1
       __syncthreads();
       st.store_hi(h);
-      if (X >= 3) {
+      if (X >= 3) {  // P2
         if (g == 0) st.combine_A(tid, nthr);
         else if (A.quad) st.combine_B(tid, nthr);
       }
       __syncthreads();
     }
-    st.inplane_lines(tid, nthr);
+    st.inplane_lines(tid, nthr);  // P3
     __syncthreads();
+    // P4 (in-plane fluxes, <= 306 items) shares a phase with P6 = the update
+    // of plane X-2 (64 items; its x fluxes sit in the 3-slot FX ring, its
+    // y/z fluxes in FYZ until this step's P5, its inputs staged in SG6)
     if (st.interior(X)) st.inplane_fluxes(tid, nthr);
+    if (X >= 3 && st.interior(X - 2)) {
+      st.set_plane(X - 1);
+      st.update_plane_offset(tid, nthr, NYF + NZF + 2 * NCOR);
+      st.set_plane(X);
+    }
     __syncthreads();
-    if (X >= 3) st.faces_yz(tid, nthr);
+    if (st.interior(X - 1)) st.prefetch_update(X - 1, tid, nthr);  // stage next P6
+    async_commit();
+    if (X >= 3) st.faces_yz(tid, nthr);  // P5
     async_wait_all();
     __syncthreads();
   }

@@ -122,9 +122,9 @@ struct Smem {
   static constexpr int RAW_END_IP = IPR + 2 * 2 * NF * NCOR;
   static constexpr int RAW_END_B = RAW + 12 * NF * NP;
   static constexpr int RAW_SIZE = (RAW_END_IP > RAW_END_B ? RAW_END_IP : RAW_END_B) - RAW;
-  static constexpr int XPART = RAW + RAW_SIZE;       // [2][6][64] (C, edev)
-  static constexpr int FX = XPART + 2 * NF * NFACEX; // [2 ring][6][64]
-  static constexpr int BYE = FX + 2 * NF * NFACEX;   // [6][72]
+  static constexpr int EDEV = RAW + RAW_SIZE;        // [6][64] x-face edge deviation sums
+  static constexpr int FX = EDEV + NF * NFACEX;      // [3 ring][6][64] x-face fluxes (centre, then final)
+  static constexpr int BYE = FX + 3 * NF * NFACEX;   // [6][72]
   static constexpr int BZE = BYE + NF * NYF;         // [6][72]
   static constexpr int BV = BZE + NF * NZF;          // [2][6][81]
   static constexpr int FP = BV + 2 * NF * NCOR;      // [2][4][6][72]
@@ -457,7 +457,7 @@ struct Stage {
 
   // ---- P2A: x-face centre + edges, boundary edge points for y/z faces -----
   OMB_HD void combine_A(int tid, int nthr) {
-    double* FXc = S + Smem::FX + (X & 1) * NF * NFACEX;
+    double* FXc = S + Smem::FX + (X % 3) * NF * NFACEX;
     int nx = NF * NFACEX;
     int ntot = A.quad ? nx + NF * (NYF + NZF) : nx;
     for (int it = tid; it < ntot; it += nthr) {
@@ -470,8 +470,8 @@ struct Stage {
         double e2 = edge_acc(rawA(3, 0, v, y - 1, z), rawA(4, 0, v, y, z));
         double e3 = edge_acc(rawA(3, 0, v, y, z), rawA(4, 0, v, y + 1, z));
         double edev = (pdev_edge(e0, C) + pdev_edge(e1, C)) + (pdev_edge(e2, C) + pdev_edge(e3, C));
-        S[Smem::XPART + v * NFACEX + f] = C;
-        S[Smem::XPART + (NF + v) * NFACEX + f] = edev;
+        FXc[v * NFACEX + f] = C;
+        S[Smem::EDEV + v * NFACEX + f] = edev;
       } else if (it < nx + NF * NYF) {
         int j = it - nx, v = j / NYF, s = j % NYF, y = 2 + s / 8, z = 3 + s % 8;
         S[Smem::BYE + v * NYF + s] = edge_acc(rawA(3, 1, v, y, z), rawA(4, 1, v, y + 1, z));
@@ -484,14 +484,14 @@ struct Stage {
 
   // ---- P2B: x-face vertices -> final x flux; vertex points for y/z -------
   OMB_HD void combine_B(int tid, int nthr) {
-    double* FXc = S + Smem::FX + (X & 1) * NF * NFACEX;
+    double* FXc = S + Smem::FX + (X % 3) * NF * NFACEX;
     int nx = NF * NFACEX;
     int ntot = nx + 2 * NF * NCOR;
     for (int it = tid; it < ntot; it += nthr) {
       if (it < nx) {
         int v = it / NFACEX, f = it % NFACEX, y = 3 + f / 8, z = 3 + f % 8;
-        double C = S[Smem::XPART + v * NFACEX + f];
-        double edev = S[Smem::XPART + (NF + v) * NFACEX + f];
+        double C = FXc[v * NFACEX + f];
+        double edev = S[Smem::EDEV + v * NFACEX + f];
         double vdev = (pdev_vert(vertex(0, v, y - 1, z - 1), C) + pdev_vert(vertex(0, v, y - 1, z), C)) +
                       (pdev_vert(vertex(0, v, y, z - 1), C) + pdev_vert(vertex(0, v, y, z), C));
         FXc[v * NFACEX + f] = face_final(C, edev, vdev);
@@ -603,13 +603,20 @@ struct Stage {
   }
 
   // ---- P6: update the cells of plane X-1 ---------------------------------
+  // run the update on threads [off, off+64) when the block is large enough,
+  // so it overlaps a phase that only occupies the first `off` threads
+  OMB_HD void update_plane_offset(int tid, int nthr, int off) {
+    int base = nthr >= off + NFACEX ? off : 0;
+    update_plane(tid - base, nthr);
+  }
+
   OMB_HD void update_plane(int tid, int nthr) {
     int Xc = X - 1;
     int r = (Xc - 3) >> 3, lx = (Xc - 3) & 7;
     int leaf = leaves[r];
     const LeafInfo& LI = A.info[leaf];
-    const double* FXlo = S + Smem::FX + ((Xc) & 1) * NF * NFACEX;
-    const double* FXhi = S + Smem::FX + (X & 1) * NF * NFACEX;
+    const double* FXlo = S + Smem::FX + (Xc % 3) * NF * NFACEX;
+    const double* FXhi = S + Smem::FX + (X % 3) * NF * NFACEX;
     UpdateParams P;
     P.dt = *A.dt; P.a = A.a; P.b = A.b;
     P.gamma = A.gamma; P.eta = A.eta; P.inv_gamma = A.inv_gamma; P.omega = A.omega;
@@ -617,6 +624,7 @@ struct Stage {
     P.has_grav = A.grav != nullptr;
     P.has_src = (A.omega != 0.0) || P.has_grav;
     for (int it = tid; it < NFACEX; it += nthr) {
+      if (it < 0) continue;
       int y = 3 + it / 8, z = 3 + it % 8;
       long long cell = (long long)leaf * 512 + lx * 64 + (y - 3) * 8 + (z - 3);
       double u[NF], u0[NF], rr[NF], out[NF], g[4] = {0, 0, 0, 0};

@@ -38,10 +38,8 @@ extern "C" int emu_stage(const OmbStageDesc* d, int nthr) {
     ALL(s.prefetch_plane(4, t, nthr));
     for (int X = 2; X < 8 * R + 4; X++) {
       ALL(s.set_plane(X));
-      ALL(if (X + 2 < 8 * R + 6) s.convert_plane(X + 2, t, nthr);
-          if (X >= 3 && s.interior(X - 2)) { s.set_plane(X - 1); s.update_plane(t, nthr); s.set_plane(X); });
+      ALL(if (X + 2 < 8 * R + 6) s.convert_plane(X + 2, t, nthr));
       ALL(if (X + 3 < 8 * R + 6) s.prefetch_plane(X + 3, t, nthr);
-          if (s.interior(X - 1)) s.prefetch_update(X - 1, t, nthr);
           s.boundary_lines(0, t, nthr, h[t]));
       ALL(s.store_hi(h[t]); if (X >= 3) s.combine_A(t, nthr));
       if (A.new_mode) {
@@ -49,8 +47,10 @@ extern "C" int emu_stage(const OmbStageDesc* d, int nthr) {
         ALL(s.store_hi(h[t]); if (X >= 3 && A.quad) s.combine_B(t, nthr));
       }
       ALL(s.inplane_lines(t, nthr));
-      ALL(if (s.interior(X)) s.inplane_fluxes(t, nthr));
-      ALL(if (X >= 3) s.faces_yz(t, nthr));
+      ALL(if (s.interior(X)) s.inplane_fluxes(t, nthr);
+          if (X >= 3 && s.interior(X - 2)) { s.set_plane(X - 1); s.update_plane_offset(t, nthr, NYF + NZF + 2 * NCOR); s.set_plane(X); });
+      ALL(if (s.interior(X - 1)) s.prefetch_update(X - 1, t, nthr);
+          if (X >= 3) s.faces_yz(t, nthr));
     }
     ALL(s.set_plane(8 * R + 3); s.update_plane(t, nthr));
     double m = 0.0;
