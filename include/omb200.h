@@ -23,7 +23,7 @@
 extern "C" {
 #endif
 
-#define OMB_ABI_VERSION 1
+#define OMB_ABI_VERSION 2
 
 /* per-leaf topology / geometry record (device array, one per leaf) */
 typedef struct {
@@ -31,7 +31,12 @@ typedef struct {
     int offmask;   /* bit 2a: the -a face is a physical wall; bit 2a+1: the +a face */
     double ox, oy, oz;  /* first interior cell centre (SubGrid.origin) */
     double dx, inv_dx;  /* cell width and the host-computed 1.0/dx */
+    int flags;     /* bit 0: export face fluxes to flux[slot]; bit 1: update deferred to omb_reflux_update */
+    int slot;      /* flux export slot (OMB_FLUX_SLOT doubles: FX (6,9,8,8), FY (6,8,9,8), FZ (6,8,8,9)) */
 } OmbLeafInfo;
+
+#define OMB_FLUX_SLOT (3 * 6 * 9 * 8 * 8)
+#define OMB_AMR_TASK_INTS 16
 
 /* one RK3 stage over all runs of the batch (state layout [6][fstride], leaf-major 8^3 blocks, z fastest) */
 typedef struct {
@@ -52,7 +57,28 @@ typedef struct {
     int new_mode, override_center, contact;
     unsigned long long *amax_bits;  /* device: running max of the signal speed (bits of a non-negative double) */
     unsigned long long *fallback;   /* device: running positivity-fallback count */
+    double *flux;         /* face-flux export slots (AMR coarse/fine faces), may be NULL if no leaf exports */
 } OmbStageDesc;
+
+/* AMR ghost regions: each task fills, in the interior of a VIRTUAL leaf (batch index >= number of real
+ * leaves), the cells the stage kernel's gather reads for one coarse/fine neighbour region of a real leaf:
+ * minmod prolongation of the coarse leaf (task[0] = 0) or 8-cell restriction of the fine children (1).
+ * int task[16]: role, rd[3], virtual leaf, coarse: src, m0[3], m1[3], foff[3] | fine: child[8] */
+typedef struct {
+    double *u;            /* state [6][fstride] (real + virtual leaves) */
+    long long fstride;
+    const int *tasks;     /* [ntasks][16] */
+    int ntasks;
+} OmbAmrDesc;
+
+/* reflux + deferred update of coarse leaves on coarse/fine faces */
+typedef struct {
+    OmbStageDesc stage;   /* same arguments as the stage just run */
+    const int *leaf;      /* [nleaves] batch index of each reflux leaf */
+    const int *off;       /* [nleaves+1] CSR offsets into tasks */
+    const int *tasks;     /* [.][6]: axis, side, fine child's flux slot, k_t1, k_t2, unused */
+    int nleaves;
+} OmbRefluxDesc;
 
 typedef struct {
     const double *u;      /* state [6][fstride] */
@@ -77,6 +103,10 @@ int omb_reconstruct(const double *prim, int m, int new_mode, int contact_on, dou
 int omb_fluxes(const double *lo, const double *hi, int n, double gamma, int new_mode, int override_center,
                double *fx, double *fy, double *fz, unsigned long long *amax_bits, void *stream);
 int omb_stage(const OmbStageDesc *desc, void *stream);
+/* coarse/fine ghost regions (ghosts.py:62-112, transfer.py:13-64) before a stage */
+int omb_amr_ghosts(const OmbAmrDesc *desc, void *stream);
+/* reflux (step.py:206-241) + update (step.py:243-288) of the deferred coarse leaves after a stage */
+int omb_reflux_update(const OmbRefluxDesc *desc, void *stream);
 int omb_cfl(const OmbCflDesc *desc, void *stream);
 /* multi-GPU halo exchange (replaces the cross-rank part of fill_leaf_ghosts, ghosts.py:115-150):
  * pack whole leaves idx[0..n) of a [6][fstride] state into a leaf-major [n][6][512] message, and
@@ -87,8 +117,8 @@ int omb_unpack_leaves(const double *in, int n, double *u, long long fstride, int
 int omb_selftest_div(unsigned long long seed, long long n, unsigned long long *bad, void *stream);
 /* host (CPU) packing between per-leaf padded arrays (6, n+6, n+6, n+6) -- SubGrid.u, tree.py:47-61 --
  * and the [6][L][n^3] device layout; multithreaded, used around H2D/D2H copies */
-int omb_host_pack(const double *const *leaf_u, int L, int n, double *out);
-int omb_host_unpack(const double *in, int L, int n, double *const *leaf_u);
+int omb_host_pack(const double *const *leaf_u, int L, int n, long long fstride, double *out);
+int omb_host_unpack(const double *in, int L, int n, long long fstride, double *const *leaf_u);
 /* FP64 DFMA throughput probe (roofline denominator): blocks*256*8*iters DFMAs */
 int omb_fp64_peak(double *scratch, int blocks, int iters, void *stream);
 /* padded (6,14,14,14) conserved block of one leaf as the ghost fill would produce it */

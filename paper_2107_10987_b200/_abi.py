@@ -13,8 +13,11 @@ c_ip = ctypes.POINTER(ctypes.c_int)
 c_u64p = ctypes.POINTER(ctypes.c_uint64)
 
 LEAF_INFO_DTYPE = np.dtype([("nbr", "<i4", (27,)), ("offmask", "<i4"), ("ox", "<f8"), ("oy", "<f8"),
-                            ("oz", "<f8"), ("dx", "<f8"), ("inv_dx", "<f8")], align=True)
-assert LEAF_INFO_DTYPE.itemsize == 152
+                            ("oz", "<f8"), ("dx", "<f8"), ("inv_dx", "<f8"), ("flags", "<i4"), ("slot", "<i4")],
+                           align=True)
+assert LEAF_INFO_DTYPE.itemsize == 160
+AMR_TASK_INTS = 16
+FLUX_SLOT_DOUBLES = 3 * 6 * 9 * 8 * 8  # FX, FY, FZ of one 8^3 leaf (reference flux layouts)
 
 
 class OmbStageDesc(ctypes.Structure):
@@ -28,6 +31,20 @@ class OmbStageDesc(ctypes.Structure):
         ("floor_rho", ctypes.c_double), ("floor_tau", ctypes.c_double), ("floor_vmax", ctypes.c_double),
         ("bc", ctypes.c_int), ("new_mode", ctypes.c_int), ("override_center", ctypes.c_int),
         ("contact", ctypes.c_int), ("amax_bits", ctypes.c_void_p), ("fallback", ctypes.c_void_p),
+        ("flux", ctypes.c_void_p),
+    ]
+
+
+class OmbAmrDesc(ctypes.Structure):
+    _fields_ = [
+        ("u", ctypes.c_void_p), ("fstride", ctypes.c_longlong), ("tasks", ctypes.c_void_p), ("ntasks", ctypes.c_int),
+    ]
+
+
+class OmbRefluxDesc(ctypes.Structure):
+    _fields_ = [
+        ("stage", OmbStageDesc), ("leaf", ctypes.c_void_p), ("off", ctypes.c_void_p), ("tasks", ctypes.c_void_p),
+        ("nleaves", ctypes.c_int),
     ]
 
 

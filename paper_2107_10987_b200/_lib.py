@@ -7,16 +7,17 @@ entry point raises NativeError.  The product never imports the oracle.
 import ctypes
 import os
 
-from ._abi import OmbCflDesc, OmbStageDesc
+from ._abi import OmbAmrDesc, OmbCflDesc, OmbRefluxDesc, OmbStageDesc
 from .errors import NativeError
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 SO_PATH = os.path.join(_HERE, "libomb200.so")
-ABI_VERSION = 1
+ABI_VERSION = 2
 _lib = None
 
 EXPORTS = ("omb_abi_version", "omb_last_error", "omb_stage_smem_bytes", "omb_primitives", "omb_reconstruct",
-           "omb_fluxes", "omb_stage", "omb_cfl", "omb_gather", "omb_fp64_peak", "omb_pack_leaves", "omb_unpack_leaves", "omb_selftest_div", "omb_host_pack", "omb_host_unpack")
+           "omb_fluxes", "omb_stage", "omb_cfl", "omb_gather", "omb_fp64_peak", "omb_pack_leaves", "omb_unpack_leaves", "omb_selftest_div", "omb_host_pack", "omb_host_unpack", "omb_amr_ghosts",
+           "omb_reflux_update")
 
 
 def load():
@@ -40,8 +41,10 @@ def load():
     L.omb_pack_leaves.argtypes = [vp, ll, vp, i, vp, vp]
     L.omb_unpack_leaves.argtypes = [vp, i, vp, ll, i, vp]
     L.omb_selftest_div.argtypes = [ctypes.c_ulonglong, ll, vp, vp]
-    L.omb_host_pack.argtypes = [vp, i, i, vp]
-    L.omb_host_unpack.argtypes = [vp, i, i, vp]
+    L.omb_host_pack.argtypes = [vp, i, i, ll, vp]
+    L.omb_host_unpack.argtypes = [vp, i, i, ll, vp]
+    L.omb_amr_ghosts.argtypes = [ctypes.POINTER(OmbAmrDesc), vp]
+    L.omb_reflux_update.argtypes = [ctypes.POINTER(OmbRefluxDesc), vp]
     for fn in EXPORTS[3:]:
         getattr(L, fn).restype = i
     if L.omb_abi_version() != ABI_VERSION:

@@ -17,7 +17,7 @@ keep >= a few waves of CTAs on 148 SMs.
 
 import numpy as np
 
-from ._abi import BC_CODES, LEAF_INFO_DTYPE
+from ._abi import AMR_TASK_INTS, BC_CODES, LEAF_INFO_DTYPE
 from .geometry import NFIELDS
 
 OFFS = [(i, j, k) for i in (-1, 0, 1) for j in (-1, 0, 1) for k in (-1, 0, 1)]
@@ -27,7 +27,10 @@ class UnsupportedTree(NotImplementedError):
     pass
 
 
-def neighbor_table(tree, leaves):
+AMR = -2  # neighbor_table code: region covered by a coarser or finer leaf
+
+
+def neighbor_table(tree, leaves, allow_amr=False):
     """(len(leaves), 27) global indices (into `leaves`) of the same-level
     neighbour at each offset (OFFS order; centre = self), -1 where the
     offset leaves the domain (non-periodic).  Uses Octree.neighbor_ipos /
@@ -63,7 +66,10 @@ def neighbor_table(tree, leaves):
                 continue
             cover = tree.find_leaf_region(lf.level, pos)
             if cover[0][1] != "same":
-                raise UnsupportedTree("coarse/fine neighbours (AMR) are not handled by the fused kernel yet")
+                if not allow_amr:
+                    raise UnsupportedTree("coarse/fine neighbours need the AMR path (single GPU)")
+                out[i, q] = AMR
+                continue
             j = index.get(cover[0][0].path)
             if j is None:
                 raise UnsupportedTree("neighbour outside the leaf set")
@@ -89,9 +95,10 @@ class LeafBatch:
         self.L = len(self.leaves)
         self.ncompute = self.L if ncompute is None else ncompute
         if gnbr is None:
-            gnbr = neighbor_table(tree, self.leaves)
+            gnbr = neighbor_table(tree, self.leaves, allow_amr=(ncompute is None))
             gids = np.arange(self.L)
         local = {int(g): i for i, g in enumerate(gids)}
+        self.amr = bool(np.any(gnbr == AMR))
         self.info = np.zeros(self.L, dtype=LEAF_INFO_DTYPE)
         self.dx = np.empty(self.L)
         for i, lf in enumerate(self.leaves):
@@ -108,15 +115,116 @@ class LeafBatch:
             rec["offmask"] = off
             if i < self.ncompute:
                 row = gnbr[int(gids[i])]
-                rec["nbr"] = [local[int(g)] if g >= 0 else -1 for g in row]
+                rec["nbr"] = [local[int(g)] if g >= 0 else g for g in row]
             else:
                 rec["nbr"] = -1
             rec["ox"], rec["oy"], rec["oz"] = (float(x) for x in sg.origin)
             rec["dx"] = sg.dx
             rec["inv_dx"] = 1.0 / sg.dx
             self.dx[i] = sg.dx
-        self.fstride = self.L * 512
+        self.nvirtual = 0
+        self.amr_tasks = np.zeros((0, AMR_TASK_INTS), dtype=np.int32)
+        self.flux_slots = 0
+        self.reflux_off = np.zeros(1, dtype=np.int32)
+        self.reflux_leaf = np.zeros(0, dtype=np.int32)
+        self.reflux_tasks = np.zeros((0, 6), dtype=np.int32)
+        self.solo = np.zeros(self.L, dtype=bool)
+        if self.amr:
+            self._build_amr()
+        self.fstride = (self.L + self.nvirtual) * 512
         self._build_runs(max_run)
+
+    # -- AMR: virtual neighbour leaves, flux export, reflux --------------------
+    def _build_amr(self):
+        """Coarse/fine neighbour regions become VIRTUAL leaves (indices L..):
+        before each stage omb_amr_ghosts fills, in a virtual leaf's interior,
+        exactly the cells the stage kernel's gather reads for that region,
+        with the reference's prolongation / restriction (mesh/ghosts.py:62-112,
+        mesh/transfer.py:13-64).  Leaves on a coarse/fine face export their
+        face fluxes; coarse ones defer their update to omb_reflux_update,
+        which first applies the reflux substitution (hydro/step.py:206-241)."""
+        tree, n, L = self.tree, self.n, self.L
+        index = {lf.path: i for i, lf in enumerate(self.leaves)}
+        tasks = []
+        g = 3
+        for i, lf in enumerate(self.leaves[:self.ncompute]):
+            nbr = self.info[i]["nbr"]
+            for q, o in enumerate(OFFS):
+                if nbr[q] != AMR:
+                    continue
+                pos = tree.neighbor_ipos(lf, o)
+                cover = tree.find_leaf_region(lf.level, pos)
+                role = cover[0][1]
+                t = np.zeros(AMR_TASK_INTS, dtype=np.int32)
+                t[1:4] = o
+                t[4] = L + len(tasks)
+                if role == "coarse":
+                    t[0] = 0
+                    t[5] = index[cover[0][0].path]
+                    for a in range(3):
+                        c = o[a]
+                        fr = (0, g) if c == 1 else ((n - g, n) if c == -1 else (0, n))
+                        octa = int(pos[a]) & 1
+                        c0 = octa * (n // 2) + fr[0] // 2
+                        c1 = octa * (n // 2) + (fr[1] - 1) // 2 + 1
+                        m0, m1 = max(c0 - 1, 0), min(c1 + 1, n)
+                        t[6 + a], t[9 + a], t[12 + a] = m0, m1, fr[0] + octa * n - 2 * m0
+                else:
+                    t[0] = 1
+                    for k, (child, _) in enumerate(cover):
+                        t[5 + k] = index[child.path]
+                tasks.append(t)
+                nbr[q] = t[4]
+            self.info[i]["nbr"] = nbr
+            if len(tasks) and any(nbr[q] >= L for q in range(27)):
+                self.solo[i] = True
+        self.nvirtual = len(tasks)
+        self.amr_tasks = np.array(tasks, dtype=np.int32).reshape(-1, AMR_TASK_INTS)
+        # reflux relations across faces (the reference's _reflux loop order)
+        faces = [(ax, side) for ax in range(3) for side in (-1, 1)]
+        slot = {}
+        rtasks = {}
+
+        def get_slot(j):
+            if j not in slot:
+                slot[j] = len(slot)
+            return slot[j]
+
+        for i, lf in enumerate(self.leaves[:self.ncompute]):
+            for ax, side in faces:
+                off = [0, 0, 0]
+                off[ax] = side
+                pos = tree.neighbor_ipos(lf, off)
+                if pos is None:
+                    continue
+                cover = tree.find_leaf_region(lf.level, pos)
+                if cover[0][1] != "fine":
+                    continue
+                t1, t2 = [x for x in range(3) if x != ax]
+                for child, _ in cover:
+                    k = [int(child.ipos[x]) & 1 for x in range(3)]
+                    if k[ax] != (0 if side > 0 else 1):
+                        continue
+                    rtasks.setdefault(i, []).append((ax, side, index[child.path], k[t1], k[t2]))
+        for i in sorted(rtasks):
+            get_slot(i)
+            for (_, _, j, _, _) in rtasks[i]:
+                get_slot(j)
+        self.flux_slots = len(slot)
+        for j, sl in slot.items():
+            self.info[j]["flags"] |= 1  # export face fluxes
+            self.info[j]["slot"] = sl
+            self.solo[j] = True
+        self.reflux_leaf = np.array(sorted(rtasks), dtype=np.int32)
+        off = [0]
+        rows = []
+        for i in self.reflux_leaf:
+            self.info[i]["flags"] |= 2  # update deferred to the reflux kernel
+            for (ax, side, j, k1, k2) in rtasks[int(i)]:
+                rows.append((ax, side, slot[j], k1, k2, 0))
+            off.append(len(rows))
+        self.reflux_off = np.array(off, dtype=np.int32)
+        self.reflux_tasks = np.array(rows, dtype=np.int32).reshape(-1, 6)
 
     def _build_runs(self, max_run):
         xp = OFFS.index((1, 0, 0))
@@ -125,13 +233,14 @@ class LeafBatch:
         for i, lf in enumerate(self.leaves[:self.ncompute]):
             prev = self.info[i]["nbr"][xm]
             # a run starts where there is no computed same-level -x neighbour inside the domain
-            if prev >= 0 and prev < self.ncompute and lf.ipos[0] > 0:
+            if prev >= 0 and prev < self.ncompute and lf.ipos[0] > 0 and not self.solo[i] and not self.solo[prev]:
                 continue
             chain = [i]
-            while True:
+            while not self.solo[i]:
                 cur = chain[-1]
                 nxt = self.info[cur]["nbr"][xp]
-                if nxt < 0 or nxt >= self.ncompute or self.leaves[cur].ipos[0] + 1 >= 2 ** self.leaves[cur].level:
+                if nxt < 0 or nxt >= self.ncompute or self.solo[nxt] or \
+                        self.leaves[cur].ipos[0] + 1 >= 2 ** self.leaves[cur].level:
                     break
                 chain.append(int(nxt))
             # balanced split into pieces of <= max_run
@@ -160,11 +269,12 @@ class LeafBatch:
         return ptrs
 
     def pack(self, out=None, lib=None):
-        """Interiors of all batch leaves into ``out`` ([6][L][8][8][8])."""
-        U = out if out is not None else np.empty((NFIELDS, self.L, 8, 8, 8))
+        """Interiors of all batch leaves into ``out`` ([6][L+nvirtual][8][8][8]);
+        virtual (AMR ghost) leaves are left as they are."""
+        U = out if out is not None else np.zeros((NFIELDS, self.L + self.nvirtual, 8, 8, 8))
         ptrs = self._leaf_ptrs(self.L) if lib is not None else None
         if ptrs is not None and U.flags.c_contiguous:
-            lib.omb_host_pack(ptrs.ctypes.data, self.L, 8, U.ctypes.data)
+            lib.omb_host_pack(ptrs.ctypes.data, self.L, 8, self.fstride, U.ctypes.data)
             return U
         for i, lf in enumerate(self.leaves):
             U[:, i] = lf.subgrid.interior
@@ -174,13 +284,13 @@ class LeafBatch:
         """Write the computed leaves back (halo leaves belong to other ranks)."""
         ptrs = self._leaf_ptrs(self.ncompute) if lib is not None else None
         if ptrs is not None and U.flags.c_contiguous and self.ncompute == self.L:
-            lib.omb_host_unpack(U.ctypes.data, self.L, 8, ptrs.ctypes.data)
+            lib.omb_host_unpack(U.ctypes.data, self.L, 8, self.fstride, ptrs.ctypes.data)
             return
         for i, lf in enumerate(self.leaves[:self.ncompute]):
             lf.subgrid.interior[:] = U[:, i]
 
     def pack_gravity(self, fields):
-        G = np.empty((4, self.L, 8, 8, 8))
+        G = np.zeros((4, self.L + self.nvirtual, 8, 8, 8))
         for i, lf in enumerate(self.leaves):
             f = fields[lf.path]
             for k, name in enumerate(("gx", "gy", "gz", "dphi_dt")):

@@ -397,6 +397,40 @@ __global__ void k_gather(const double* U, long long fstride, const LeafInfo* inf
   }
 }
 
+// AMR ghost regions: one thread per (task, block cell), 6 fields
+__global__ void k_amr_ghosts(double* U, long long fstride, const int* __restrict__ tasks, int ntasks) {
+  int task = blockIdx.x;
+  if (task >= ntasks) return;
+  const int* t = tasks + task * 16;
+  int tl[16];
+#pragma unroll
+  for (int i = 0; i < 16; i++) tl[i] = t[i];
+  int ncell = amr_block_cells(tl);
+  for (int i = threadIdx.x; i < ncell; i += blockDim.x) {
+    int b[3], vcell;
+    amr_decode(tl, i, b, vcell);
+    double out[NF];
+#pragma unroll
+    for (int v = 0; v < NF; v++) out[v] = amr_cell(U, fstride, tl, v, b);
+#pragma unroll
+    for (int v = 0; v < NF; v++) U[v * fstride + (long long)tl[4] * 512 + vcell] = out[v];
+  }
+}
+
+// reflux (step.py:206-241) + update (step.py:243-288) of one deferred coarse leaf per CTA
+__global__ void k_reflux_update(StageArgs A, const int* __restrict__ rleaf, const int* __restrict__ roff,
+                                const int* __restrict__ rtasks) {
+  extern __shared__ double F[];  // FLUX_SLOT doubles: this leaf's FX | FY | FZ
+  int leaf = rleaf[blockIdx.x];
+  const double* src = A.flux + (long long)A.info[leaf].slot * FLUX_SLOT;
+  for (int i = threadIdx.x; i < FLUX_SLOT; i += blockDim.x) F[i] = src[i];
+  __syncthreads();
+  // substitutions touch disjoint face blocks: no ordering among them
+  for (int q = roff[blockIdx.x]; q < roff[blockIdx.x + 1]; q++) reflux_apply(F, A.flux, rtasks + q * 6, threadIdx.x, blockDim.x);
+  __syncthreads();
+  update_leaf(A, leaf, F, threadIdx.x, blockDim.x);
+}
+
 // halo exchange packing: whole 8^3 leaves, field-major state <-> leaf-major message
 __global__ void k_pack(const double* __restrict__ U, long long fstride, const int* __restrict__ idx, int n,
                        double* __restrict__ out) {
@@ -497,23 +531,7 @@ int omb_fluxes(const double* lo, const double* hi, int n, double gamma, int new_
   return 0;
 }
 
-int omb_stage(const OmbStageDesc* d, void* stream) {
-  if (int rc = lib_init()) return rc;
-  if (d->ucur == d->unext) return set_err("omb_stage: unext must not alias ucur");
-  static bool attr_set = false;
-  if (!attr_set) {
-    CK(cudaFuncSetAttribute(k_stage<512>, cudaFuncAttributeMaxDynamicSharedMemorySize, Smem::BYTES), "smem attribute");
-    CK(cudaFuncSetAttribute(k_stage<384>, cudaFuncAttributeMaxDynamicSharedMemorySize, Smem::BYTES), "smem attribute");
-    CK(cudaFuncSetAttribute(k_stage<256>, cudaFuncAttributeMaxDynamicSharedMemorySize, Smem::BYTES), "smem attribute");
-    CK(cudaFuncSetAttribute(k_stage<576>, cudaFuncAttributeMaxDynamicSharedMemorySize, Smem::BYTES), "smem attribute");
-    CK(cudaFuncSetAttribute(k_stage<640>, cudaFuncAttributeMaxDynamicSharedMemorySize, Smem::BYTES), "smem attribute");
-    attr_set = true;
-  }
-  static int nt = [] {
-    const char* e = getenv("OMB_STAGE_THREADS");
-    int v = e ? atoi(e) : 512;
-    return (v == 256 || v == 384 || v == 576 || v == 640) ? v : 512;
-  }();
+static StageArgs stage_args(const OmbStageDesc* d) {
   StageArgs A;
   A.ucur = d->ucur;
   A.u0 = d->u0;
@@ -541,6 +559,51 @@ int omb_stage(const OmbStageDesc* d, void* stream) {
   A.contact = d->contact;
   A.amax_bits = d->amax_bits;
   A.fallback = d->fallback;
+  A.flux = d->flux;
+  return A;
+}
+
+int omb_amr_ghosts(const OmbAmrDesc* d, void* stream) {
+  if (int rc = lib_init()) return rc;
+  if (d->ntasks <= 0) return 0;
+  k_amr_ghosts<<<d->ntasks, 192, 0, (cudaStream_t)stream>>>(d->u, d->fstride, d->tasks, d->ntasks);
+  CK(cudaGetLastError(), "omb_amr_ghosts launch");
+  return 0;
+}
+
+int omb_reflux_update(const OmbRefluxDesc* d, void* stream) {
+  if (int rc = lib_init()) return rc;
+  if (d->nleaves <= 0) return 0;
+  static bool attr = false;
+  if (!attr) {
+    CK(cudaFuncSetAttribute(k_reflux_update, cudaFuncAttributeMaxDynamicSharedMemorySize, FLUX_SLOT * 8),
+       "reflux smem attribute");
+    attr = true;
+  }
+  StageArgs A = stage_args(&d->stage);
+  k_reflux_update<<<d->nleaves, 256, FLUX_SLOT * 8, (cudaStream_t)stream>>>(A, d->leaf, d->off, d->tasks);
+  CK(cudaGetLastError(), "omb_reflux_update launch");
+  return 0;
+}
+
+int omb_stage(const OmbStageDesc* d, void* stream) {
+  if (int rc = lib_init()) return rc;
+  if (d->ucur == d->unext) return set_err("omb_stage: unext must not alias ucur");
+  static bool attr_set = false;
+  if (!attr_set) {
+    CK(cudaFuncSetAttribute(k_stage<512>, cudaFuncAttributeMaxDynamicSharedMemorySize, Smem::BYTES), "smem attribute");
+    CK(cudaFuncSetAttribute(k_stage<384>, cudaFuncAttributeMaxDynamicSharedMemorySize, Smem::BYTES), "smem attribute");
+    CK(cudaFuncSetAttribute(k_stage<256>, cudaFuncAttributeMaxDynamicSharedMemorySize, Smem::BYTES), "smem attribute");
+    CK(cudaFuncSetAttribute(k_stage<576>, cudaFuncAttributeMaxDynamicSharedMemorySize, Smem::BYTES), "smem attribute");
+    CK(cudaFuncSetAttribute(k_stage<640>, cudaFuncAttributeMaxDynamicSharedMemorySize, Smem::BYTES), "smem attribute");
+    attr_set = true;
+  }
+  static int nt = [] {
+    const char* e = getenv("OMB_STAGE_THREADS");
+    int v = e ? atoi(e) : 512;
+    return (v == 256 || v == 384 || v == 576 || v == 640) ? v : 512;
+  }();
+  StageArgs A = stage_args(d);
   if (d->nruns <= 0) return 0;
   if (nt == 512) k_stage<512><<<d->nruns, 512, Smem::BYTES, (cudaStream_t)stream>>>(A);
   else if (nt == 384) k_stage<384><<<d->nruns, 384, Smem::BYTES, (cudaStream_t)stream>>>(A);
@@ -590,7 +653,7 @@ int omb_selftest_div(unsigned long long seed, long long n, unsigned long long* b
 // host-side packing of the per-leaf padded arrays (the reference's SubGrid.u,
 // (6, m, m, m) C-contiguous) into / out of the [6][L][n^3] device layout;
 // multithreaded memcpy of n-element rows
-static void host_copy(const double* const* leaf_u, int L, int n, double* packed, bool to_packed) {
+static void host_copy(const double* const* leaf_u, int L, int n, long long fstride, double* packed, bool to_packed) {
   int m = n + 6;
   long long n3 = (long long)n * n * n;
   unsigned nt = std::thread::hardware_concurrency();
@@ -603,7 +666,7 @@ static void host_copy(const double* const* leaf_u, int L, int n, double* packed,
       for (int v = 0; v < 6; v++)
         for (int x = 0; x < n; x++)
           for (int y = 0; y < n; y++) {
-            double* p = packed + ((long long)v * L + i) * n3 + ((long long)x * n + y) * n;
+            double* p = packed + (long long)v * fstride + (long long)i * n3 + ((long long)x * n + y) * n;
             double* q = const_cast<double*>(u) + (((long long)v * m + x + 3) * m + y + 3) * m + 3;
             if (to_packed) memcpy(p, q, sizeof(double) * n);
             else memcpy(q, p, sizeof(double) * n);
@@ -616,13 +679,13 @@ static void host_copy(const double* const* leaf_u, int L, int n, double* packed,
   for (auto& x : th) x.join();
 }
 
-int omb_host_pack(const double* const* leaf_u, int L, int n, double* out) {
-  host_copy(leaf_u, L, n, out, true);
+int omb_host_pack(const double* const* leaf_u, int L, int n, long long fstride, double* out) {
+  host_copy(leaf_u, L, n, fstride, out, true);
   return 0;
 }
 
-int omb_host_unpack(const double* in, int L, int n, double* const* leaf_u) {
-  host_copy((const double* const*)leaf_u, L, n, const_cast<double*>(in), false);
+int omb_host_unpack(const double* in, int L, int n, long long fstride, double* const* leaf_u) {
+  host_copy((const double* const*)leaf_u, L, n, fstride, const_cast<double*>(in), false);
   return 0;
 }
 

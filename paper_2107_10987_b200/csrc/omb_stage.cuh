@@ -159,10 +159,14 @@ OMB_HD void async_wait_all() {
 }
 
 struct LeafInfo {
-  int nbr[27];    // batch index of the same-level neighbour for each offset, -1 none
+  int nbr[27];    // batch index of the same-level (or virtual AMR) neighbour per offset, -1 none
   int offmask;    // bit 2a: -a side is a physical wall, bit 2a+1: +a side
   double ox, oy, oz, dx, inv_dx;
+  int flags;      // bit 0: export face fluxes to flux[slot]; bit 1: update deferred (reflux)
+  int slot;
 };
+constexpr int FLUX_SLOT = 3 * NF * 9 * 8 * 8;  // FX (6,9,8,8) | FY (6,8,9,8) | FZ (6,8,8,9)
+constexpr int FXO = 0, FYO = NF * 9 * 64, FZO = 2 * NF * 9 * 64;
 
 struct StageArgs {
   const double* ucur;   // [6][L][512] stage input (halo source)
@@ -182,6 +186,7 @@ struct StageArgs {
   int new_mode, quad, contact;  // quad = new_mode && !override
   unsigned long long* amax_bits;  // per-stage accumulators
   unsigned long long* fallback;
+  double* flux;                   // face-flux export slots (AMR), or null
 };
 
 // conserved state of padded cell c (local coords in [0,14)^3) of a leaf, as
@@ -249,6 +254,13 @@ struct Stage {
     for (int k = 0; k < 5; k++) ring[k] = Smem::PR + (((x + 3 + k) % 5) * NF) * PL;  // (x-2+k) mod 5
   }
   OMB_HD const double* ringp(int k, int v) const { return S + ring[k] + v * PL; }
+
+  // flux export slot of this run's leaf (exporting leaves always run alone)
+  OMB_HD double* export_slot() const {
+    if (R != 1 || A.flux == nullptr) return nullptr;
+    const LeafInfo& LI = A.info[leaves[0]];
+    return (LI.flags & 1) ? A.flux + (long long)LI.slot * FLUX_SLOT : nullptr;
+  }
 
   OMB_HD int mult(int X) const {  // how many leaves of the run count plane X in [2,12)
     int c = 0;
@@ -464,7 +476,11 @@ struct Stage {
       if (it < nx) {
         int v = it / NFACEX, f = it % NFACEX, y = 3 + f / 8, z = 3 + f % 8;
         double C = rawA(0, 0, v, y, z);
-        if (!A.quad) { FXc[v * NFACEX + f] = C; continue; }
+        if (!A.quad) {
+          FXc[v * NFACEX + f] = C;
+          if (double* ex = export_slot()) ex[FXO + (v * 9 + (X - 3)) * 64 + f] = C;
+          continue;
+        }
         double e0 = edge_acc(rawA(5, 0, v, y, z - 1), rawA(6, 0, v, y, z));
         double e1 = edge_acc(rawA(5, 0, v, y, z), rawA(6, 0, v, y, z + 1));
         double e2 = edge_acc(rawA(3, 0, v, y - 1, z), rawA(4, 0, v, y, z));
@@ -494,7 +510,9 @@ struct Stage {
         double edev = S[Smem::EDEV + v * NFACEX + f];
         double vdev = (pdev_vert(vertex(0, v, y - 1, z - 1), C) + pdev_vert(vertex(0, v, y - 1, z), C)) +
                       (pdev_vert(vertex(0, v, y, z - 1), C) + pdev_vert(vertex(0, v, y, z), C));
-        FXc[v * NFACEX + f] = face_final(C, edev, vdev);
+        double Fv = face_final(C, edev, vdev);
+        FXc[v * NFACEX + f] = Fv;
+        if (double* ex = export_slot()) ex[FXO + (v * 9 + (X - 3)) * 64 + f] = Fv;
       } else {
         int j = it - nx, ax = j / (NF * NCOR), rem = j % (NF * NCOR), v = rem / NCOR, c = rem % NCOR;
         S[Smem::BV + (ax * NF + v) * NCOR + c] = vertex(1 + ax, v, 2 + c / 9, 2 + c % 9);
@@ -587,6 +605,11 @@ struct Stage {
           F = face_final(C, S01 + (pd2 + pd3), T01 + (pv2 + pv3));
         }
         S[Smem::FYZ + (zf * NF + v) * NYF + s] = F;
+        if (double* ex = export_slot()) {
+          int xi = X - 1 - 3;  // cell plane being finalised
+          if (!zf) ex[FYO + ((v * 8 + xi) * 9 + (y - 2)) * 8 + (z - 3)] = F;
+          else ex[FZO + ((v * 8 + xi) * 8 + (y - 3)) * 9 + (z - 2)] = F;
+        }
       }
       if (start) {
         double C = S[(zf ? Smem::IPCZ : Smem::IPCY) + v * NYF + s];
@@ -615,6 +638,7 @@ struct Stage {
     int r = (Xc - 3) >> 3, lx = (Xc - 3) & 7;
     int leaf = leaves[r];
     const LeafInfo& LI = A.info[leaf];
+    if (LI.flags & 2) return;  // coarse leaf on a coarse/fine face: omb_reflux_update does it
     const double* FXlo = S + Smem::FX + (Xc % 3) * NF * NFACEX;
     const double* FXhi = S + Smem::FX + (X % 3) * NF * NFACEX;
     UpdateParams P;
@@ -651,5 +675,145 @@ struct Stage {
     }
   }
 };
+
+// ---------------------------------------------------------------------------
+// AMR ghost regions (mesh/ghosts.py:62-112, mesh/transfer.py:13-64)
+// ---------------------------------------------------------------------------
+// minmod of the forward / backward differences (transfer.py:13-35); b is the
+// coarse row inside the clipped sub-block [0, nb): edge cells see the
+// linear-extrapolation pad, so their slope is one-sided
+OMB_HD double amr_minmod(double a, double b) {
+  double pick = fabs(a) < fabs(b) ? a : b;
+  return a * b > 0.0 ? pick : 0.0;
+}
+OMB_HD double amr_slope(double bm, double b0, double bp, int j, int nb) {
+  if (nb == 1) return 0.0;
+  double fwd, bwd;
+  if (j == 0) {
+    bwd = b0 - (2.0 * b0 - bp);  // padded lo = 2*b[0] - b[1]
+    fwd = bp - b0;
+  } else if (j == nb - 1) {
+    fwd = (2.0 * b0 - bm) - b0;  // padded hi = 2*b[nb-1] - b[nb-2]
+    bwd = b0 - bm;
+  } else {
+    fwd = bp - b0;
+    bwd = b0 - bm;
+  }
+  return amr_minmod(fwd, bwd);
+}
+
+// value (field v) of block cell (b0,b1,b2) of AMR task t, reading interiors of U
+OMB_HD double amr_cell(const double* U, long long fstride, const int* t, int v, const int* b) {
+  const double* Uv = U + v * fstride;
+  if (t[0] == 0) {  // coarse neighbour: prolong the clipped coarse sub-block
+    const double* C = Uv + (long long)t[5] * 512;
+    int j[3], p[3], nb[3], cg[3];
+#pragma unroll
+    for (int a = 0; a < 3; a++) {
+      int fi = t[12 + a] + b[a];  // index in the prolonged sub-block
+      j[a] = fi >> 1;
+      p[a] = fi & 1;
+      nb[a] = t[9 + a] - t[6 + a];
+      cg[a] = t[6 + a] + j[a];
+    }
+    auto at = [&](int x, int y, int z) { return C[x * 64 + y * 8 + z]; };
+    double c0 = at(cg[0], cg[1], cg[2]);
+    double sx = amr_slope(j[0] > 0 ? at(cg[0] - 1, cg[1], cg[2]) : 0.0, c0,
+                          j[0] < nb[0] - 1 ? at(cg[0] + 1, cg[1], cg[2]) : 0.0, j[0], nb[0]);
+    double sy = amr_slope(j[1] > 0 ? at(cg[0], cg[1] - 1, cg[2]) : 0.0, c0,
+                          j[1] < nb[1] - 1 ? at(cg[0], cg[1] + 1, cg[2]) : 0.0, j[1], nb[1]);
+    double sz = amr_slope(j[2] > 0 ? at(cg[0], cg[1], cg[2] - 1) : 0.0, c0,
+                          j[2] < nb[2] - 1 ? at(cg[0], cg[1], cg[2] + 1) : 0.0, j[2], nb[2]);
+    return ((c0 + sx * (p[0] ? 0.25 : -0.25)) + sy * (p[1] ? 0.25 : -0.25)) + sz * (p[2] ? 0.25 : -0.25);
+  }
+  // fine neighbours: restriction of the covering child's 2x2x2 cells
+  int c[3], k[3], f[3];
+#pragma unroll
+  for (int a = 0; a < 3; a++) {
+    c[a] = b[a] + (t[1 + a] == -1 ? N - 3 : 0);  // coarse cell within the region's pos block
+    k[a] = c[a] >= N / 2 ? 1 : 0;
+    f[a] = 2 * c[a] - k[a] * N;
+  }
+  const double* F = Uv + (long long)t[5 + k[0] + 2 * k[1] + 4 * k[2]] * 512;
+  auto at = [&](int x, int y, int z) { return F[(f[0] + x) * 64 + (f[1] + y) * 8 + (f[2] + z)]; };
+  return 0.125 * (((at(0, 0, 0) + at(1, 0, 0)) + (at(0, 1, 0) + at(1, 1, 0))) +
+                  ((at(0, 0, 1) + at(1, 0, 1)) + (at(0, 1, 1) + at(1, 1, 1))));
+}
+
+// reflux substitution of one task into this leaf's flux set F (step.py:222-241):
+// the coarse face block gets 0.25*((f00+f10)+(f01+f11)) of the fine child's face fluxes
+OMB_HD int flux_index(int ax, int v, int fi, int s1, int s2) {
+  if (ax == 0) return FXO + ((v * 9 + fi) * 8 + s1) * 8 + s2;
+  if (ax == 1) return FYO + ((v * 8 + s1) * 9 + fi) * 8 + s2;
+  return FZO + ((v * 8 + s1) * 8 + s2) * 9 + fi;
+}
+OMB_HD void reflux_apply(double* F, const double* flux, const int* rt, int tid, int nthr) {
+  int ax = rt[0], side = rt[1], k1 = rt[3], k2 = rt[4];
+  const double* fine = flux + (long long)rt[2] * FLUX_SLOT;
+  int cface = side > 0 ? N : 0, fface = side > 0 ? 0 : N;
+  for (int i = tid; i < NF * 16; i += nthr) {
+    int v = i / 16, a = (i / 4) % 4, b = i % 4;
+    double f00 = fine[flux_index(ax, v, fface, 2 * a, 2 * b)], f10 = fine[flux_index(ax, v, fface, 2 * a + 1, 2 * b)];
+    double f01 = fine[flux_index(ax, v, fface, 2 * a, 2 * b + 1)];
+    double f11 = fine[flux_index(ax, v, fface, 2 * a + 1, 2 * b + 1)];
+    F[flux_index(ax, v, cface, k1 * 4 + a, k2 * 4 + b)] = 0.25 * ((f00 + f10) + (f01 + f11));
+  }
+}
+
+// update of all 512 cells of `leaf` from its (refluxed) flux set F (step.py:243-288)
+OMB_HD void update_leaf(const StageArgs& A, int leaf, const double* F, int tid, int nthr) {
+  const LeafInfo& LI = A.info[leaf];
+  UpdateParams P;
+  P.dt = *A.dt; P.a = A.a; P.b = A.b;
+  P.gamma = A.gamma; P.eta = A.eta; P.inv_gamma = A.inv_gamma; P.omega = A.omega;
+  P.floor_rho = A.floor_rho; P.floor_tau = A.floor_tau; P.floor_vmax = A.floor_vmax;
+  P.has_grav = A.grav != nullptr;
+  P.has_src = (A.omega != 0.0) || P.has_grav;
+  for (int c = tid; c < 512; c += nthr) {
+    int x = c / 64, y = (c / 8) % 8, z = c % 8;
+    long long cell = (long long)leaf * 512 + c;
+    double u[NF], u0[NF], rr[NF], out[NF], g[4] = {0, 0, 0, 0};
+#pragma unroll
+    for (int v = 0; v < NF; v++) {
+      u[v] = A.ucur[v * A.fstride + cell];
+      u0[v] = A.u0[v * A.fstride + cell];
+      double dfx = F[flux_index(0, v, x + 1, y, z)] - F[flux_index(0, v, x, y, z)];
+      double dfy = F[flux_index(1, v, y + 1, x, z)] - F[flux_index(1, v, y, x, z)];
+      double dfz = F[flux_index(2, v, z + 1, x, y)] - F[flux_index(2, v, z, x, y)];
+      double tt = 0.0 - dfx * LI.inv_dx;
+      tt = tt - dfy * LI.inv_dx;
+      tt = tt - dfz * LI.inv_dx;
+      rr[v] = tt;
+    }
+    if (P.has_grav)
+#pragma unroll
+      for (int q = 0; q < 4; q++) g[q] = A.grav[q * A.fstride + cell];
+    double xc = LI.ox + LI.dx * (double)x;
+    double yc = LI.oy + LI.dx * (double)y;
+    update_cell(P, u, u0, rr, xc, yc, g, out);
+#pragma unroll
+    for (int v = 0; v < NF; v++) A.unext[v * A.fstride + cell] = out[v];
+  }
+}
+
+// block cell count / decode and placement inside the virtual leaf
+OMB_HD int amr_block_cells(const int* t) {
+  int c = 1;
+#pragma unroll
+  for (int a = 0; a < 3; a++) c *= t[1 + a] ? 3 : N;
+  return c;
+}
+OMB_HD void amr_decode(const int* t, int i, int* b, int& vcell) {
+  int d[3];
+#pragma unroll
+  for (int a = 0; a < 3; a++) d[a] = t[1 + a] ? 3 : N;
+  b[2] = i % d[2];
+  b[1] = (i / d[2]) % d[1];
+  b[0] = i / (d[2] * d[1]);
+  int v[3];
+#pragma unroll
+  for (int a = 0; a < 3; a++) v[a] = b[a] + (t[1 + a] == -1 ? N - 3 : 0);
+  vcell = v[0] * 64 + v[1] * 8 + v[2];
+}
 
 }  // namespace omb

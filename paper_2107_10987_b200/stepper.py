@@ -27,7 +27,7 @@ import ctypes
 import numpy as np
 
 from . import _lib
-from ._abi import OmbCflDesc, OmbStageDesc
+from ._abi import FLUX_SLOT_DOUBLES, OmbAmrDesc, OmbCflDesc, OmbRefluxDesc, OmbStageDesc
 from .batch import LeafBatch
 from .device import ptr, require_cuda, stream_handle, torch
 from .errors import NumericsError
@@ -80,7 +80,16 @@ class B200HydroStepper:
         self._cfl_bad = T.empty(b.L, dtype=T.int32, device=dev)
         self._cfl_out = T.empty(2, dtype=T.float64, device=dev)
         self._cfl_badleaf = T.empty(1, dtype=T.int32, device=dev)
-        self._pinned = T.empty(n, dtype=T.float64).pin_memory()
+        self._pinned = T.zeros(n, dtype=T.float64).pin_memory()
+        # AMR (coarse/fine neighbours): virtual-leaf ghost tasks, flux export slots, reflux lists
+        if partition is not None and b.amr:
+            raise NotImplementedError("AMR trees run on a single GPU for now")
+        self._amr_tasks = T.from_numpy(b.amr_tasks.reshape(-1).copy()).to(dev) if b.nvirtual else None
+        self._flux = T.empty(max(1, b.flux_slots) * FLUX_SLOT_DOUBLES, dtype=T.float64, device=dev) \
+            if b.flux_slots else None
+        self._rleaf = T.from_numpy(b.reflux_leaf.copy()).to(dev) if len(b.reflux_leaf) else None
+        self._roff = T.from_numpy(b.reflux_off.copy()).to(dev) if len(b.reflux_leaf) else None
+        self._rtasks = T.from_numpy(b.reflux_tasks.reshape(-1).copy()).to(dev) if len(b.reflux_leaf) else None
         self._grav = None
         self._fresh = False  # device state was just uploaded from the host by cfl_dt
         self.dx_min = float(min(lf.subgrid.dx for lf in tree.leaves()))
@@ -96,7 +105,7 @@ class B200HydroStepper:
     def upload(self):
         """Copy the host leaves' interiors into the device state."""
         b = self.batch
-        host = self._pinned.numpy().reshape(6, b.L, 8, 8, 8)
+        host = self._pinned.numpy().reshape(6, b.L + b.nvirtual, 8, 8, 8)
         b.pack(out=host, lib=self.lib)
         self._buf[self._state].copy_(self._pinned, non_blocking=True)
 
@@ -104,7 +113,7 @@ class B200HydroStepper:
         """Copy the device state back into the host leaves."""
         b = self.batch
         self._pinned.copy_(self._buf[self._state])
-        b.unpack(self._pinned.numpy().reshape(6, b.L, 8, 8, 8), lib=self.lib)
+        b.unpack(self._pinned.numpy().reshape(6, b.L + b.nvirtual, 8, 8, 8), lib=self.lib)
 
     def state_tensor(self):
         return self._buf[self._state]
@@ -177,7 +186,7 @@ class B200HydroStepper:
             floor_rho=float(fl.rho), floor_tau=float(fl.tau), floor_vmax=float(fl.vmax), bc=b.bc,
             new_mode=int(self.mode.is_new), override_center=int(self.mode.quadrature_override),
             contact=int(self.mode.contact_detection), amax_bits=acc.data_ptr() + 8 * s,
-            fallback=acc.data_ptr() + 8 * (3 + s))
+            fallback=acc.data_ptr() + 8 * (3 + s), flux=ptr(self._flux))
 
     def launch_step(self, dt=None, stream=None, events=None):
         """Enqueue the three stages (no host sync) and advance the device state.
@@ -195,12 +204,21 @@ class B200HydroStepper:
                 self._grav = torch.from_numpy(self.batch.pack_gravity(fields).reshape(-1)).to(self.dev)
             nxt = others[s]
             self._exchange(cur, stream)
+            sh = stream_handle(stream)
+            if self._amr_tasks is not None:
+                ad = OmbAmrDesc(u=ptr(self._buf[cur]), fstride=self.batch.fstride, tasks=ptr(self._amr_tasks),
+                                ntasks=self.batch.nvirtual)
+                _lib.check(self.lib.omb_amr_ghosts(ctypes.byref(ad), sh), "omb_amr_ghosts")
             d = self._stage_desc(cur, nxt, s, a, bw)
             if events is not None:
                 events[s][0].record()
-            _lib.check(self.lib.omb_stage(ctypes.byref(d), stream_handle(stream)), "omb_stage")
+            _lib.check(self.lib.omb_stage(ctypes.byref(d), sh), "omb_stage")
             if events is not None:
                 events[s][1].record()
+            if self._rleaf is not None:
+                rd = OmbRefluxDesc(stage=d, leaf=ptr(self._rleaf), off=ptr(self._roff), tasks=ptr(self._rtasks),
+                                   nleaves=len(self.batch.reflux_leaf))
+                _lib.check(self.lib.omb_reflux_update(ctypes.byref(rd), sh), "omb_reflux_update")
             outs.append(nxt)
             cur = nxt
         start = self._state

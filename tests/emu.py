@@ -8,7 +8,7 @@ import subprocess
 
 import numpy as np
 
-from paper_2107_10987_b200._abi import OmbStageDesc
+from paper_2107_10987_b200._abi import FLUX_SLOT_DOUBLES, OmbAmrDesc, OmbRefluxDesc, OmbStageDesc
 from paper_2107_10987_b200.batch import LeafBatch
 from paper_2107_10987_b200.hydro import SSP_RK3_STAGES
 
@@ -32,6 +32,8 @@ def lib():
         _lib.emu_stage.argtypes = [ctypes.POINTER(OmbStageDesc), ctypes.c_int]
         _lib.emu_gather.argtypes = [ctypes.c_void_p, ctypes.c_longlong, ctypes.c_void_p, ctypes.c_int, ctypes.c_int,
                                     ctypes.c_void_p]
+        _lib.emu_amr_ghosts.argtypes = [ctypes.POINTER(OmbAmrDesc)]
+        _lib.emu_reflux_update.argtypes = [ctypes.POINTER(OmbRefluxDesc)]
     return _lib
 
 
@@ -60,11 +62,18 @@ class EmuStepper:
         dtv = np.array([dt])
         G = None if self.grav is None else np.ascontiguousarray(b.pack_gravity(self.grav))
         self.amax, self.fallback = 0.0, 0
+        flux = np.zeros(max(1, b.flux_slots) * FLUX_SLOT_DOUBLES)
+        tasks = np.ascontiguousarray(b.amr_tasks.reshape(-1))
+        rleaf, roff = np.ascontiguousarray(b.reflux_leaf), np.ascontiguousarray(b.reflux_off)
+        rtasks = np.ascontiguousarray(b.reflux_tasks.reshape(-1))
         cur = 0
         for s, (a, bb) in enumerate(SSP_RK3_STAGES):
             am = np.zeros(1, dtype=np.uint64)
             fb = np.zeros(1, dtype=np.uint64)
             nxt = s + 1
+            if b.nvirtual:
+                lib().emu_amr_ghosts(ctypes.byref(OmbAmrDesc(u=ptr(bufs[cur]), fstride=b.fstride, tasks=ptr(tasks),
+                                                              ntasks=b.nvirtual)))
             d = OmbStageDesc(ucur=ptr(bufs[cur]), u0=ptr(U0), unext=ptr(bufs[nxt]), grav=ptr(G),
                              fstride=b.fstride, info=ptr(b.info), run_off=ptr(self.run_off),
                              run_leaf=ptr(self.run_leaf), nruns=b.nruns, dt=ptr(dtv), a=a, b=bb,
@@ -72,8 +81,11 @@ class EmuStepper:
                              omega=self.omega, floor_rho=self.floors[0], floor_tau=self.floors[1],
                              floor_vmax=self.floors[2], bc=b.bc, new_mode=self.flags[0],
                              override_center=self.flags[1], contact=self.flags[2], amax_bits=ptr(am),
-                             fallback=ptr(fb))
+                             fallback=ptr(fb), flux=ptr(flux))
             lib().emu_stage(ctypes.byref(d), self.nthr)
+            if len(rleaf):
+                lib().emu_reflux_update(ctypes.byref(OmbRefluxDesc(stage=d, leaf=ptr(rleaf), off=ptr(roff),
+                                                                   tasks=ptr(rtasks), nleaves=len(rleaf))))
             self.amax = max(self.amax, float(am.view(np.float64)[0]))
             self.fallback += int(fb[0])
             cur = nxt

@@ -20,7 +20,7 @@ extern "C" int emu_stage(const OmbStageDesc* d, int nthr) {
   A.a = d->a; A.b = d->b; A.gamma = d->gamma; A.gm1 = d->gm1; A.inv_gm1 = 1.0 / d->gm1; A.eta = d->eta; A.inv_gamma = d->inv_gamma;
   A.omega = d->omega; A.floor_rho = d->floor_rho; A.floor_tau = d->floor_tau; A.floor_vmax = d->floor_vmax;
   A.bc = d->bc; A.new_mode = d->new_mode; A.quad = d->new_mode && !d->override_center; A.contact = d->contact;
-  A.amax_bits = d->amax_bits; A.fallback = d->fallback;
+  A.amax_bits = d->amax_bits; A.fallback = d->fallback; A.flux = d->flux;
   std::vector<double> S(Smem::TOTAL);
   for (int run = 0; run < d->nruns; run++) {
     std::fill(S.begin(), S.end(), NAN);  // catch reads of never-written shared memory
@@ -78,4 +78,37 @@ extern "C" int emu_gather(const double* U, long long fstride, const OmbLeafInfo*
 
 extern "C" double emu_speed(const double* u6, double gamma, double gm1, double eta) {
   return speed_cell(u6, gamma, gm1, eta);
+}
+
+extern "C" int emu_amr_ghosts(const OmbAmrDesc* d) {
+  for (int task = 0; task < d->ntasks; task++) {
+    const int* t = d->tasks + task * 16;
+    int nc = amr_block_cells(t);
+    for (int i = 0; i < nc; i++) {
+      int b[3], vcell;
+      amr_decode(t, i, b, vcell);
+      double out[NF];
+      for (int v = 0; v < NF; v++) out[v] = amr_cell(d->u, d->fstride, t, v, b);
+      for (int v = 0; v < NF; v++) d->u[v * d->fstride + (long long)t[4] * 512 + vcell] = out[v];
+    }
+  }
+  return 0;
+}
+
+extern "C" int emu_reflux_update(const OmbRefluxDesc* r) {
+  const OmbStageDesc* d = &r->stage;
+  StageArgs A;
+  A.ucur = d->ucur; A.u0 = d->u0; A.unext = d->unext; A.grav = d->grav; A.fstride = d->fstride;
+  A.info = (const LeafInfo*)d->info; A.dt = d->dt; A.a = d->a; A.b = d->b; A.gamma = d->gamma; A.gm1 = d->gm1;
+  A.inv_gm1 = 1.0 / d->gm1; A.eta = d->eta; A.inv_gamma = d->inv_gamma; A.omega = d->omega;
+  A.floor_rho = d->floor_rho; A.floor_tau = d->floor_tau; A.floor_vmax = d->floor_vmax; A.flux = d->flux;
+  std::vector<double> F(FLUX_SLOT);
+  for (int i = 0; i < r->nleaves; i++) {
+    int leaf = r->leaf[i];
+    const double* src = A.flux + (long long)A.info[leaf].slot * FLUX_SLOT;
+    for (int j = 0; j < FLUX_SLOT; j++) F[j] = src[j];
+    for (int q = r->off[i]; q < r->off[i + 1]; q++) reflux_apply(F.data(), A.flux, r->tasks + q * 6, 0, 1);
+    update_leaf(A, leaf, F.data(), 0, 1);
+  }
+  return 0;
 }

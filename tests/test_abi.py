@@ -25,7 +25,7 @@ def test_header_symbols_exported():
     for n in names:
         assert hasattr(L, n), n
     assert set(names) == set(_lib.EXPORTS)
-    assert L.omb_abi_version() == 1
+    assert L.omb_abi_version() == _lib.ABI_VERSION
     assert L.omb_stage_smem_bytes() <= 232448
 
 
@@ -33,11 +33,13 @@ def test_struct_layouts_match_header(tmp_path):
     """ctypes mirrors vs the C compiler's view of include/omb200.h (size + every field offset)."""
     import subprocess
 
-    from paper_2107_10987_b200._abi import LEAF_INFO_DTYPE, OmbCflDesc, OmbStageDesc
+    from paper_2107_10987_b200._abi import (LEAF_INFO_DTYPE, OmbAmrDesc, OmbCflDesc, OmbRefluxDesc,
+                                             OmbStageDesc)
 
     lines = ['#include <stdio.h>', '#include <stddef.h>', f'#include "{ROOT}/include/omb200.h"', "int main(void){"]
     checks = []
-    for cls, cname in ((OmbStageDesc, "OmbStageDesc"), (OmbCflDesc, "OmbCflDesc")):
+    for cls, cname in ((OmbStageDesc, "OmbStageDesc"), (OmbCflDesc, "OmbCflDesc"), (OmbAmrDesc, "OmbAmrDesc"),
+                       (OmbRefluxDesc, "OmbRefluxDesc")):
         lines.append(f'printf("%zu\\n", sizeof({cname}));')
         checks.append(ctypes.sizeof(cls))
         for fname, _ in cls._fields_:

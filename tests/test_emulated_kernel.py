@@ -66,3 +66,45 @@ def test_emulated_gather_matches_ghost_golden():
             out = np.empty((6, 14, 14, 14))
             lib().emu_gather(U.ctypes.data, b.fstride, b.info.ctypes.data, i, b.bc, out.ctypes.data)
             assert bitwise_mismatch(out, g[bnd][i]) == 0, (bnd, i)
+
+
+def test_emulated_amr_reflux_two_steps():
+    """Coarse/fine ghosts (virtual leaves) + flux export + reflux, vs the reference (2 steps)."""
+    import hashlib
+
+    t, g = case_tree("amr_reflux")
+    em = EmuStepper(t, 1.4, max_run=2)
+    assert em.b.nvirtual > 0 and len(em.b.reflux_leaf) > 0
+    for s in range(2):
+        em.rk3_step(float(g["dts"][s]))
+        if s == 0:
+            assert bitwise_mismatch(state_of(t), g["state1"]) == 0
+        assert em.amax == float(g["amax"][s])
+    assert hashlib.sha256(np.ascontiguousarray(state_of(t)).tobytes()).hexdigest() == str(g["final_sha"])
+
+
+def test_emulated_amr_ghost_regions():
+    """Gathered padded blocks (incl. prolonged / restricted regions) equal the reference ghost fill."""
+    import ctypes
+    import json
+
+    from paper_2107_10987_b200 import mesh
+    from paper_2107_10987_b200._abi import OmbAmrDesc
+    from paper_2107_10987_b200.batch import LeafBatch
+
+    g = golden("ghosts")
+    t = mesh.build_uniform_tree(1, 8, boundary="reflecting")
+    t.split(t.leaf_at(1, (0, 0, 0)))
+    t.reindex()
+    assert [json.loads(p) for p in g["amr_paths"]] == [list(lf.path) for lf in t.sorted_leaves()]
+    for lf, u in zip(t.sorted_leaves(), g["amr"]):
+        lf.subgrid.interior[:] = u[:, 3:11, 3:11, 3:11]
+    b = LeafBatch(t)
+    U = np.ascontiguousarray(b.pack())
+    tasks = np.ascontiguousarray(b.amr_tasks.reshape(-1))
+    lib().emu_amr_ghosts(ctypes.byref(OmbAmrDesc(u=U.ctypes.data, fstride=b.fstride, tasks=tasks.ctypes.data,
+                                                  ntasks=b.nvirtual)))
+    for i in range(b.L):
+        out = np.empty((6, 14, 14, 14))
+        lib().emu_gather(U.ctypes.data, b.fstride, b.info.ctypes.data, i, b.bc, out.ctypes.data)
+        assert bitwise_mismatch(out, g["amr"][i]) == 0, i
