@@ -52,15 +52,37 @@ def parse():
     p.add_argument("--e2e-steps", type=int, default=8)
     p.add_argument("--cpu-leaves", type=int, default=512)
     p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--config", default=None, choices=["c2", "c3", "c4"],
+                   help="c2: uniform 128^3 (N=1 default); c3: uniform 256^3 (N>1 default); c4: AMR Sedov, levels 3-6")
     return p.parse_args()
 
 
 def sedov_tree(level):
     from paper_2107_10987_b200 import EosConfig, SedovConfig, build_uniform_tree, init_sedov
 
+    if level == "c4":
+        from paper_2107_10987_b200.problems import amr_sedov_tree
+
+        return amr_sedov_tree()
     t = build_uniform_tree(level, 8, boundary="reflecting")
     init_sedov(SedovConfig(), t, EosConfig(gamma=1.4))
     return t
+
+
+def resolve_level(args, world):
+    if args.config == "c4":
+        return "c4"
+    if args.config == "c3":
+        return 5
+    if args.config == "c2":
+        return 4
+    return args.level if args.level is not None else (4 if world == 1 else 5)
+
+
+def workload_name(level, nleaves):
+    if level == "c4":
+        return f"sedov_amr_L3-6_n8 (config c4): {nleaves} sub-grids of 8^3 on levels 3-6 (SURVEY.md 8d construction)"
+    return f"sedov_uniform_L{level}_n8"
 
 
 def peaks():
@@ -141,7 +163,7 @@ def cpu_run(level, nleaves, steps, warmup):
 def reference_arm(args, rank, world):
     if rank != 0:
         return
-    level = args.level if args.level is not None else (4 if world == 1 else 5)
+    level = resolve_level(args, world)
     # size the per-step sample so the whole run stays within ~3 minutes
     probe_v, nthr, _, _ = cpu_run(level, 8, 1, 0)
     budget = 150.0 / max(1, args.steps + args.warmup)
@@ -150,8 +172,7 @@ def reference_arm(args, rank, world):
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": per * 1e3, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic (init_sedov, no RNG)",
-            "config": {"workload": f"sedov_uniform_L{level}_n8 ({8 ** level} sub-grids of 8^3, "
-                                   f"{8 ** level * 512} cells), reflecting, cfl 0.4; CPU sample per step"},
+            "config": {"workload": f"{workload_name(level, None)}, reflecting, cfl 0.4; CPU sample per step"},
             "cpu_baseline": {"value": v, "unit": UNIT, "cores": nthr, "kind": "port", "sample": sample},
             "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
@@ -194,7 +215,7 @@ def gpu_arm(args, rank, world):
         import torch.distributed as dist
 
     # N=1: config c2 (128^3, level 4); N>1: config c3 (256^3, level 5) partitioned by leaf
-    level = args.level if args.level is not None else (4 if world == 1 else 5)
+    level = resolve_level(args, world)
     tree = sedov_tree(level)
     eos = EosConfig(gamma=1.4)
     part = None
@@ -292,8 +313,8 @@ def gpu_arm(args, rank, world):
         "ms_per_step": ms / K, "higher_is_better": True, "scaling": "weak" if world == 1 else "strong",
         "vs_baseline": None,
         "dtype": "f64", "data": "synthetic (init_sedov Sedov-Taylor, no RNG)",
-        "config": {"workload": f"sedov_uniform_L{level}_n8: {st.nglobal} sub-grids of 8^3 = {cells} cells "
-                               f"({int(round(cells ** (1 / 3)))}^3), reflecting, cfl 0.4, scheme new",
+        "config": {"workload": f"{workload_name(level, st.nglobal)}: {st.nglobal} sub-grids of 8^3 = {cells} cells, "
+                               "reflecting, cfl 0.4, scheme new",
                    "step": "cfl_dt + 3 fused RK stages, dt on device",
                    "l2": "working set (3 x 6 x cells x 8 B = %.0f MB) > 126 MB L2; no flush" % (3 * 48 * cells / 1e6),
                    "runs": st.batch.nruns, "max_run": args.max_run, "parallelism": f"leaf-partitioned x{world}",

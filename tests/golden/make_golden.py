@@ -233,7 +233,27 @@ def ghost_cases():
     save("ghosts", **out)
 
 
+def amr_sedov_case():
+    """Reduced config c4: Sedov on a geometrically refined octree (SURVEY.md §8(d) construction)."""
+    from octomini.mesh import refine_by_criterion
+
+    radii = {2: 0.6, 3: 0.35}
+    t = build_uniform_tree(2, 8, boundary="reflecting")
+
+    def crit(leaf):
+        sg = leaf.subgrid
+        lo = sg.origin - 0.5 * sg.dx
+        hi = lo + sg.dx * sg.n
+        nearest = np.clip(0.0, lo, hi)
+        return float(np.sqrt(np.sum(nearest * nearest))) <= radii.get(leaf.level, -1.0)
+
+    refine_by_criterion(t, crit, 4)
+    init_sedov(SedovConfig(), t, EOS)
+    step_case("amr_sedov_small", t, steps=1)
+
+
 def main():
+    amr_sedov_case()
     kernel_cases()
     ghost_cases()
     # Sedov benchmark config c1 (32^3 = 64 leaves of 8^3, reflecting), 10 steps

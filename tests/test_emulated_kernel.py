@@ -108,3 +108,12 @@ def test_emulated_amr_ghost_regions():
         out = np.empty((6, 14, 14, 14))
         lib().emu_gather(U.ctypes.data, b.fstride, b.info.ctypes.data, i, b.bc, out.ctypes.data)
         assert bitwise_mismatch(out, g["amr"][i]) == 0, i
+
+
+def test_emulated_amr_sedov_small():
+    """Reduced config c4 (Sedov on a 3-level refined octree) vs the reference, one step."""
+    t, g = case_tree("amr_sedov_small")
+    em = EmuStepper(t, 1.4)
+    em.rk3_step(float(g["dts"][0]))
+    assert bitwise_mismatch(state_of(t), g["state1"]) == 0
+    assert em.amax == float(g["amax"][0])

@@ -87,7 +87,7 @@ def _check_state(t, g, key="state1"):
     assert rel_close(got, ref, 1e-12) == 0
 
 
-@pytest.mark.parametrize("name", ["smooth_periodic", "smooth_reflecting", "sedov_c1"])
+@pytest.mark.parametrize("name", ["smooth_periodic", "smooth_reflecting", "sedov_c1", "amr_sedov_small"])
 @pytest.mark.parametrize("max_run", [1, 4])
 def test_step_parity(name, max_run):
     t, g = case_tree(name)

@@ -78,7 +78,8 @@ def test_ghost_fill(bnd):
     assert bitwise_mismatch(got, g[bnd]) == 0
 
 
-@pytest.mark.parametrize("name", ["smooth_periodic", "smooth_reflecting", "smooth_old", "amr_reflux"])
+@pytest.mark.parametrize("name", ["smooth_periodic", "smooth_reflecting", "smooth_old", "amr_reflux",
+                                  "amr_sedov_small"])
 def test_step_cases_bitwise(name):
     t, g = case_tree(name)
     st = OracleStepper(t, 1.4, new_mode=(name != "smooth_old"))
