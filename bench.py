@@ -141,6 +141,26 @@ def cpu_run(level, nleaves, steps, warmup):
 
     tree = sedov_tree(level)
     leaves = tree.sorted_leaves()[:nleaves]
+    # the reference's reflux reads the fine face-neighbours' fluxes: close the sample under that relation
+    chosen = {lf.path for lf in leaves}
+    grew = True
+    while grew:
+        grew = False
+        for lf in list(leaves):
+            for ax in range(3):
+                for side in (-1, 1):
+                    off = [0, 0, 0]
+                    off[ax] = side
+                    pos = tree.neighbor_ipos(lf, off)
+                    if pos is None:
+                        continue
+                    cover = tree.find_leaf_region(lf.level, pos)
+                    if cover[0][1] == "fine":
+                        for child, _ in cover:
+                            if child.path not in chosen:
+                                chosen.add(child.path)
+                                leaves.append(child)
+                                grew = True
     nthr = os.cpu_count() or 1
     st = OracleStepper(tree, 1.4, nthreads=nthr)
     oracle.lib()
