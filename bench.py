@@ -52,8 +52,9 @@ def parse():
     p.add_argument("--e2e-steps", type=int, default=8)
     p.add_argument("--cpu-leaves", type=int, default=512)
     p.add_argument("--no-cpu-baseline", action="store_true")
-    p.add_argument("--config", default=None, choices=["c2", "c3", "c4"],
-                   help="c2: uniform 128^3 (N=1 default); c3: uniform 256^3 (N>1 default); c4: AMR Sedov, levels 3-6")
+    p.add_argument("--config", default=None, choices=["c2", "c3", "c4", "c5"],
+                   help="c2: uniform 128^3 (N=1 default); c3: uniform 256^3 (N>1 default); c4: AMR Sedov, "
+                        "levels 3-6; c5: rotating polytrope stand-in, fixed gravity, 128^3")
     return p.parse_args()
 
 
@@ -70,8 +71,8 @@ def sedov_tree(level):
 
 
 def resolve_level(args, world):
-    if args.config == "c4":
-        return "c4"
+    if args.config in ("c4", "c5"):
+        return args.config
     if args.config == "c3":
         return 5
     if args.config == "c2":
@@ -80,6 +81,9 @@ def resolve_level(args, world):
 
 
 def workload_name(level, nleaves):
+    if level == "c5":
+        return ("star_uniform_L4_n8 (config c5 stand-in: closed-form n=1 polytrope, rotating frame, fixed "
+                "self-gravity, rho floor 1e-4, outflow, gamma 5/3)")
     if level == "c4":
         return f"sedov_amr_L3-6_n8 (config c4): {nleaves} sub-grids of 8^3 on levels 3-6 (SURVEY.md 8d construction)"
     return f"sedov_uniform_L{level}_n8"
@@ -139,7 +143,16 @@ def cpu_run(level, nleaves, steps, warmup):
     import oracle
     from oracle.step import OracleStepper
 
-    tree = sedov_tree(level)
+    kw = {}
+    gamma = 1.4
+    if level == "c5":
+        from paper_2107_10987_b200.problems import synthetic_star
+
+        tree, eos, grav, om, fl = synthetic_star(level=4)
+        kw = dict(omega=om, gravity=grav, floors=(fl.rho, fl.tau, fl.vmax))
+        gamma = eos.gamma
+    else:
+        tree = sedov_tree(level)
     leaves = tree.sorted_leaves()[:nleaves]
     # the reference's reflux reads the fine face-neighbours' fluxes: close the sample under that relation
     chosen = {lf.path for lf in leaves}
@@ -162,7 +175,7 @@ def cpu_run(level, nleaves, steps, warmup):
                                 leaves.append(child)
                                 grew = True
     nthr = os.cpu_count() or 1
-    st = OracleStepper(tree, 1.4, nthreads=nthr)
+    st = OracleStepper(tree, gamma, nthreads=nthr, **kw)
     oracle.lib()
     times = []
     for k in range(warmup + steps):
@@ -236,14 +249,22 @@ def gpu_arm(args, rank, world):
 
     # N=1: config c2 (128^3, level 4); N>1: config c3 (256^3, level 5) partitioned by leaf
     level = resolve_level(args, world)
-    tree = sedov_tree(level)
-    eos = EosConfig(gamma=1.4)
+    extra = {}
+    if level == "c5":
+        from paper_2107_10987_b200.problems import synthetic_star
+
+        tree, eos, grav, om, fl = synthetic_star(level=4)
+        extra = dict(gravity=grav, omega=om, floors=fl)
+    else:
+        tree = sedov_tree(level)
+        eos = EosConfig(gamma=1.4)
     part = None
     if world > 1:
         from paper_2107_10987_b200.partition import Partition
 
         part = Partition(tree, world, rank)
-    st = B200HydroStepper(tree, eos, HydroMode("new"), host_sync=False, max_run=args.max_run, partition=part)
+    st = B200HydroStepper(tree, eos, HydroMode("new"), host_sync=False, max_run=args.max_run, partition=part,
+                          **extra)
     lib = _lib.load()
     cells = st.nglobal * 512  # whole job
     local_cells = st.batch.ncompute * 512
@@ -293,9 +314,15 @@ def gpu_arm(args, rank, world):
     # end-to-end through the public drop-in API (host state of record, H2D + D2H every step)
     e2e = None
     if args.e2e_steps > 0:
-        t2 = sedov_tree(level)
+        extra2 = {}
+        if level == "c5":
+            t2, _, g2, om2, fl2 = synthetic_star(level=4)
+            extra2 = dict(gravity=g2, omega=om2, floors=fl2)
+        else:
+            t2 = sedov_tree(level)
         p2 = Partition(t2, world, rank) if world > 1 else None
-        st2 = B200HydroStepper(t2, eos, HydroMode("new"), host_sync=True, max_run=args.max_run, partition=p2)
+        st2 = B200HydroStepper(t2, eos, HydroMode("new"), host_sync=True, max_run=args.max_run, partition=p2,
+                               **extra2)
         for _ in range(2):
             st2.rk3_step(st2.cfl_dt(0.4))
         torch.cuda.synchronize()

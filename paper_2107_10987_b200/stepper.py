@@ -200,8 +200,12 @@ class B200HydroStepper:
         others = [i for i in range(4) if i != self._state]
         for s, (a, bw) in enumerate(SSP_RK3_STAGES):
             if self.gravity is not None:
+                # the reference re-solves gravity every stage (step.py:111-113); a solver that
+                # returns the same field object again (fixed gravity) is uploaded only once
                 fields = self.gravity.solve(self.tree, need_derivative=True)
-                self._grav = torch.from_numpy(self.batch.pack_gravity(fields).reshape(-1)).to(self.dev)
+                if fields is not getattr(self, "_grav_src", None):
+                    self._grav = torch.from_numpy(self.batch.pack_gravity(fields).reshape(-1)).to(self.dev)
+                    self._grav_src = fields
             nxt = others[s]
             self._exchange(cur, stream)
             sh = stream_handle(stream)

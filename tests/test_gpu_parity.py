@@ -222,3 +222,24 @@ def test_amr_reflux_two_steps_gpu():
         # tau may differ by an ulp through CUDA's pow; everything else must be bitwise
         assert rel_close(got, g["final"], 1e-12) == 0
         assert bitwise_mismatch(got[:, :5], g["final"][:, :5]) == 0
+
+
+def test_synthetic_star_matches_oracle():
+    """Config c5 stand-in (rotating frame + fixed gravity + floors, outflow): GPU vs the CPU oracle, 2 steps."""
+    from oracle.step import OracleStepper
+    from paper_2107_10987_b200 import HydroMode
+    from paper_2107_10987_b200.problems import synthetic_star
+    from paper_2107_10987_b200.stepper import B200HydroStepper
+
+    tg, eos, grav, om, fl = synthetic_star(level=2)
+    tc, _, gravc, _, _ = synthetic_star(level=2)
+    gpu = B200HydroStepper(tg, eos, HydroMode("new"), gravity=grav, omega=om, floors=fl)
+    ref = OracleStepper(tc, eos.gamma, omega=om, gravity=gravc, floors=(fl.rho, fl.tau, fl.vmax))
+    for _ in range(2):
+        dt = gpu.cfl_dt(0.4)
+        assert dt == ref.cfl_dt(0.4)
+        gpu.rk3_step(dt)
+        ref.rk3_step(dt)
+    a, b = state_of(tg), state_of(tc)
+    assert bitwise_mismatch(a[:, :5], b[:, :5]) == 0
+    assert rel_close(a, b, 1e-12) == 0
