@@ -70,21 +70,6 @@ OMB_HD double div_by(double a, double b, double y) {
   return q2;
 }
 
-// div_by without its rare-case branch: zero numerators are handled by a
-// select (a/b == a*(1/b) for a == 0); `rare` is raised when the premise of
-// the theorem may fail (extreme or non-finite quotient) and the caller then
-// redoes ALL its quotients with the IEEE division -- one uniform branch per
-// group instead of one per quotient.
-OMB_HD double div_by_nobranch(double a, double b, double y, bool& rare) {
-  double q0 = a * y;
-  double q1 = fma(fma(-b, q0, a), y, q0);
-  double q2 = fma(fma(-b, q1, a), y, q1);
-  double m = fabs(q1);
-  bool z = (a == 0.0);
-  rare |= !z && !(m > 0x1p-1000 && m < 0x1p+1000);
-  return z ? a * y : q2;
-}
-
 // NaN-faithful helpers: C fmin/fmax semantics (IEEE minNum/maxNum), as libm.
 OMB_HD double dmin(double a, double b) { return fmin(a, b); }
 OMB_HD double dmax(double a, double b) { return fmax(a, b); }
@@ -110,22 +95,24 @@ OMB_HD double iface(double am1, double a, double ap1, double ap2) {
 // multiply by RN(1/6) and the exact IEEE division is taken only when the
 // comparison margin is within a guard band of 8 ulp -- the branch outcomes
 // (hence the outputs) are identical to the reference's.
-// Branch-free except for the rare exact-division fallback: both outcomes are
-// computed and selected (the extremum test's result is the same as the
-// reference's early branch).
 OMB_HD void mono(double a, double& lv, double& hv) {
-  bool ext = (hv - a) * (a - lv) <= 0.0;
+  if ((hv - a) * (a - lv) <= 0.0) {
+    lv = a;
+    hv = a;
+    return;
+  }
   double diff = hv - lv;
   double mid = a - 0.5 * (lv + hv);
   double dm = diff * mid;
   double d2 = diff * diff;
   double q = d2 * (1.0 / 6.0);
   double band = 0x1p-49 * fabs(q) + 0x1p-1000;
-  if (!ext && (!(fabs(dm - q) > band) || !(fabs(dm + q) > band))) q = d2 / 6.0;
-  double nlv = (dm > q) ? 3.0 * a - 2.0 * hv : lv;
-  double nhv = (-q > dm) ? 3.0 * a - 2.0 * nlv : hv;
-  lv = ext ? a : nlv;
-  hv = ext ? a : nhv;
+  if (!(fabs(dm - q) > band) || !(fabs(dm + q) > band)) q = d2 / 6.0;
+  double nlv = lv, nhv = hv;
+  if (dm > q) nlv = 3.0 * a - 2.0 * hv;
+  if (-q > dm) nhv = 3.0 * a - 2.0 * nlv;
+  lv = nlv;
+  hv = nhv;
 }
 
 // _core.pyx:159-173
@@ -205,7 +192,6 @@ OMB_HD double kt_axis(const KtState& P, const KtState& Q, int axis, bool flip, d
   double denom = ap - am;
   double apam = ap * am;
   double rden = 1.0 / denom;  // one IEEE reciprocal for the six quotients
-  bool rare = false;
   double cP = flip ? -am : ap;
   double cQ = flip ? ap : -am;
   double sg = flip ? -apam : apam;
@@ -223,23 +209,7 @@ OMB_HD double kt_axis(const KtState& P, const KtState& Q, int axis, bool flip, d
       fQ = fQ + Q.p * vnQ;
     }
     double num = (cP * fP + cQ * fQ) + sg * (Q.u[v] - P.u[v]);
-    out[v] = ok ? div_by_nobranch(num, denom, rden, rare) : (flip ? fQ : fP);
-  }
-  if (rare && ok) {  // extreme / non-finite quotients: redo with the IEEE division
-#pragma unroll
-    for (int v = 0; v < NF; v++) {
-      double fP = P.u[v] * vnP, fQ = Q.u[v] * vnQ;
-      if (v == 1 || v == 2 || v == 3) {
-        bool nrm = (v == 1 + axis);
-        fP = nrm ? fP + P.p : fP;
-        fQ = nrm ? fQ + Q.p : fQ;
-      }
-      if (v == 4) {
-        fP = fP + P.p * vnP;
-        fQ = fQ + Q.p * vnQ;
-      }
-      out[v] = ((cP * fP + cQ * fQ) + sg * (Q.u[v] - P.u[v])) / denom;
-    }
+    out[v] = ok ? div_by(num, denom, rden) : (flip ? fQ : fP);
   }
   return dmax(ap, -am);
 }
