@@ -385,6 +385,8 @@ def gpu_arm(args, rank, world):
 
 
 def main():
+    # NCCL writes its version/debug lines to stdout; keep stdout for the single JSON line
+    os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
     args = parse()
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))

@@ -11,7 +11,7 @@ from ._abi import OmbAmrDesc, OmbCflDesc, OmbRefluxDesc, OmbStageDesc
 from .errors import NativeError
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-SO_PATH = os.path.join(_HERE, "libomb200.so")
+SO_PATH = os.environ.get("OMB_LIB_PATH") or os.path.join(_HERE, "libomb200.so")  # override: A/B experiments
 ABI_VERSION = 2
 _lib = None
 

@@ -95,6 +95,22 @@ OMB_HD double iface(double am1, double a, double ap1, double ap2) {
 // multiply by RN(1/6) and the exact IEEE division is taken only when the
 // comparison margin is within a guard band of 8 ulp -- the branch outcomes
 // (hence the outputs) are identical to the reference's.
+#if defined(OMB_MONO_BF)
+OMB_HD void mono(double a, double& lv, double& hv) {  // experimental branch-free variant
+  bool ext = (hv - a) * (a - lv) <= 0.0;
+  double diff = hv - lv;
+  double mid = a - 0.5 * (lv + hv);
+  double dm = diff * mid;
+  double d2 = diff * diff;
+  double q = d2 * (1.0 / 6.0);
+  double band = 0x1p-49 * fabs(q) + 0x1p-1000;
+  if (!ext && (!(fabs(dm - q) > band) || !(fabs(dm + q) > band))) q = d2 / 6.0;
+  double nlv = (dm > q) ? 3.0 * a - 2.0 * hv : lv;
+  double nhv = (-q > dm) ? 3.0 * a - 2.0 * nlv : hv;
+  lv = ext ? a : nlv;
+  hv = ext ? a : nhv;
+}
+#else
 OMB_HD void mono(double a, double& lv, double& hv) {
   if ((hv - a) * (a - lv) <= 0.0) {
     lv = a;
@@ -114,6 +130,7 @@ OMB_HD void mono(double a, double& lv, double& hv) {
   lv = nlv;
   hv = nhv;
 }
+#endif
 
 // _core.pyx:159-173
 OMB_HD double mc_slope(double am1, double a, double ap1) {
