@@ -119,6 +119,11 @@ int omb_selftest_div(unsigned long long seed, long long n, unsigned long long *b
  * and the [6][L][n^3] device layout; multithreaded, used around H2D/D2H copies */
 int omb_host_pack(const double *const *leaf_u, int L, int n, long long fstride, double *out);
 int omb_host_unpack(const double *in, int L, int n, long long fstride, double *const *leaf_u);
+/* device-side diagnostics / IO: per-leaf field sums for conservation_totals
+ * (problems/diagnostics.py:9-30; fixed summation order), and the checkpoint payload order
+ * (mesh/checkpoint.py:34-55: per leaf, 6 fields, x fastest) */
+int omb_leaf_sums(const double *u, long long fstride, int L, double *out, void *stream);
+int omb_disk_order(const double *u, long long fstride, int L, double *out, void *stream);
 /* FP64 DFMA throughput probe (roofline denominator): blocks*256*8*iters DFMAs */
 int omb_fp64_peak(double *scratch, int blocks, int iters, void *stream);
 /* padded (6,14,14,14) conserved block of one leaf as the ghost fill would produce it */

@@ -431,6 +431,34 @@ __global__ void k_reflux_update(StageArgs A, const int* __restrict__ rleaf, cons
   update_leaf(A, leaf, F, threadIdx.x, blockDim.x);
 }
 
+// per-leaf field sums in a fixed order (x-major rows of 8, pairwise inside a
+// row, rows accumulated in order) -- device side of conservation_totals
+__global__ void k_leaf_sums(const double* __restrict__ U, long long fstride, int L, double* __restrict__ out) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= L * NF) return;
+  int leaf = i / NF, v = i % NF;
+  const double* p = U + v * fstride + (long long)leaf * 512;
+  double acc = 0.0;
+  for (int r = 0; r < 64; r++) {
+    const double* a = p + r * 8;
+    acc += ((a[0] + a[1]) + (a[2] + a[3])) + ((a[4] + a[5]) + (a[6] + a[7]));
+  }
+  out[leaf * NF + v] = acc;
+}
+
+// checkpoint payload order (mesh/checkpoint.py:53-54): per leaf, fields, cells x-fastest
+__global__ void k_disk_order(const double* __restrict__ U, long long fstride, int L, double* __restrict__ out) {
+  long long total = (long long)L * NF * 512;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total; i += (long long)gridDim.x * blockDim.x) {
+    int c = (int)(i & 511);
+    long long lv = i >> 9;
+    int v = (int)(lv % NF);
+    long long leaf = lv / NF;
+    int z = c >> 6, y = (c >> 3) & 7, x = c & 7;  // on disk x varies fastest
+    out[i] = U[v * fstride + leaf * 512 + x * 64 + y * 8 + z];
+  }
+}
+
 // halo exchange packing: whole 8^3 leaves, field-major state <-> leaf-major message
 __global__ void k_pack(const double* __restrict__ U, long long fstride, const int* __restrict__ idx, int n,
                        double* __restrict__ out) {
@@ -623,6 +651,22 @@ int omb_cfl(const OmbCflDesc* d, void* stream) {
   k_cfl_reduce<<<1, 1024, 0, (cudaStream_t)stream>>>(d->nleaves, d->ratio, d->bad, d->cfl, d->out, d->bad_leaf,
                                                      d->dt_dev);
   CK(cudaGetLastError(), "omb_cfl reduce launch");
+  return 0;
+}
+
+int omb_leaf_sums(const double* U, long long fstride, int L, double* out, void* stream) {
+  if (L <= 0) return 0;
+  k_leaf_sums<<<(L * NF + 127) / 128, 128, 0, (cudaStream_t)stream>>>(U, fstride, L, out);
+  CK(cudaGetLastError(), "omb_leaf_sums launch");
+  return 0;
+}
+
+int omb_disk_order(const double* U, long long fstride, int L, double* out, void* stream) {
+  if (L <= 0) return 0;
+  long long total = (long long)L * NF * 512;
+  int blocks = (int)((total + 255) / 256);
+  k_disk_order<<<blocks < 148 * 16 ? blocks : 148 * 16, 256, 0, (cudaStream_t)stream>>>(U, fstride, L, out);
+  CK(cudaGetLastError(), "omb_disk_order launch");
   return 0;
 }
 

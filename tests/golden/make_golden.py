@@ -252,7 +252,20 @@ def amr_sedov_case():
     step_case("amr_sedov_small", t, steps=1)
 
 
+def checkpoint_case():
+    """A reference-written OMCK v1 checkpoint (mesh/checkpoint.py:34-55) of an AMR tree."""
+    from octomini.mesh import checkpoint
+
+    t = build_uniform_tree(1, 8, boundary="periodic")
+    t.split(t.leaf_at(1, (0, 0, 0)))
+    t.reindex()
+    random_smooth(t, seed=5)
+    checkpoint.write(t, os.path.join(HERE, "amr_reflux_init.omck"), time=0.25, step=7, extra={"gamma": 1.4})
+    print("wrote amr_reflux_init.omck")
+
+
 def main():
+    checkpoint_case()
     amr_sedov_case()
     kernel_cases()
     ghost_cases()
