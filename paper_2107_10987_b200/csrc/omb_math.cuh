@@ -15,11 +15,14 @@
 #pragma once
 #include <math.h>
 #include <stdint.h>
+#include <string.h>
 
 #ifdef __CUDACC__
 #define OMB_HD __host__ __device__ __forceinline__
+#define OMB_HD_NOINLINE __host__ __device__ __noinline__
 #else
 #define OMB_HD inline
+#define OMB_HD_NOINLINE inline
 #endif
 
 namespace omb {
@@ -27,22 +30,14 @@ namespace omb {
 constexpr int NF = 6;
 constexpr int NLINES = 13;
 
-// geometry.py:24-41 -- line directions
-OMB_HD int ldx(int l) { return (l == 0 || (l >= 3 && l <= 6) || l >= 9) ? 1 : 0; }
-OMB_HD int ldy(int l) {
-  switch (l) {
-    case 1: case 3: case 7: case 8: case 9: case 10: return 1;
-    case 4: case 11: case 12: return -1;
-    default: return 0;
-  }
-}
-OMB_HD int ldz(int l) {
-  switch (l) {
-    case 2: case 5: case 7: case 9: case 11: return 1;
-    case 6: case 8: case 10: case 12: return -1;
-    default: return 0;
-  }
-}
+// geometry.py:24-41 -- line directions, packed 2 bits per line (component+1)
+// so the lookups are branch-free shifts of a constant
+constexpr unsigned LDX_BITS = 0x2A96A96u;  // lines 0..12: 1,0,0,1,1,1,1,0,0,1,1,1,1
+constexpr unsigned LDY_BITS = 0x2A9499u;   // 0,1,0,1,-1,0,0,1,1,1,1,-1,-1
+constexpr unsigned LDZ_BITS = 0x888965u;   // 0,0,1,0,0,1,-1,1,-1,1,-1,1,-1
+OMB_HD int ldx(int l) { return (int)((LDX_BITS >> (2 * l)) & 3u) - 1; }
+OMB_HD int ldy(int l) { return (int)((LDY_BITS >> (2 * l)) & 3u) - 1; }
+OMB_HD int ldz(int l) { return (int)((LDZ_BITS >> (2 * l)) & 3u) - 1; }
 
 // IEEE a/b that never takes CUDA's division slow path for a zero numerator
 // (CUDA routes 0/b through a called subroutine; zero momenta and zero
@@ -68,6 +63,29 @@ OMB_HD double div_by(double a, double b, double y) {
   double m = fabs(q1);
   if (!(m > 0x1p-1000 && m < 0x1p+1000)) q2 = (a == 0.0) ? a * y : a / b;
   return q2;
+}
+
+// div_by without its rare-case branch: zero numerators go through a select
+// (a/b == a*(1/b) for a == 0); `rare` is raised -- by an integer test of the
+// exponent of q1 -- when the theorem's no-underflow/overflow premise may fail
+// (or the quotient is not finite); the caller then redoes its quotients with
+// the IEEE division.  One branch per group of quotients instead of one each.
+OMB_HD unsigned dbl_exp(double x) {
+#ifdef __CUDA_ARCH__
+  return (unsigned)(__double_as_longlong(x) >> 52) & 0x7ffu;
+#else
+  unsigned long long b;
+  memcpy(&b, &x, 8);
+  return (unsigned)(b >> 52) & 0x7ffu;
+#endif
+}
+OMB_HD double div_by_nobranch(double a, double b, double y, bool& rare) {
+  double q0 = a * y;
+  double q1 = fma(fma(-b, q0, a), y, q0);
+  double q2 = fma(fma(-b, q1, a), y, q1);
+  bool z = (a == 0.0);
+  rare |= !z && (dbl_exp(q1) - 24u > 2000u);  // |q1| outside [2^-999, 2^1001) or inf/NaN
+  return z ? a * y : q2;
 }
 
 // NaN-faithful helpers: C fmin/fmax semantics (IEEE minNum/maxNum), as libm.
@@ -190,6 +208,25 @@ OMB_HD void kt_state(const double* w, double gamma, double gm1, double inv_gm1, 
   s.u[5] = w[5];
 }
 
+// IEEE-division fallback of kt_axis (never inlined: it is almost never run)
+OMB_HD_NOINLINE void kt_quotients_ieee(const KtState& P, const KtState& Q, int axis, double vnP, double vnQ,
+                                       double cP, double cQ, double sg, double denom, double* out) {
+#pragma unroll
+  for (int v = 0; v < NF; v++) {
+    double fP = P.u[v] * vnP, fQ = Q.u[v] * vnQ;
+    if (v == 1 || v == 2 || v == 3) {
+      bool nrm = (v == 1 + axis);
+      fP = nrm ? fP + P.p : fP;
+      fQ = nrm ? fQ + Q.p : fQ;
+    }
+    if (v == 4) {
+      fP = fP + P.p * vnP;
+      fQ = fQ + Q.p * vnQ;
+    }
+    out[v] = ((cP * fP + cQ * fQ) + sg * (Q.u[v] - P.u[v])) / denom;
+  }
+}
+
 // Flux through an `axis` face across the interface P -> Q (P = cell the
 // `hi` state belongs to, Q = P + line direction, whose `lo` state is used).
 // When the line runs against the face normal (`flip`) the reference swaps
@@ -213,6 +250,7 @@ OMB_HD double kt_axis(const KtState& P, const KtState& Q, int axis, bool flip, d
   double cQ = flip ? ap : -am;
   double sg = flip ? -apam : apam;
   bool ok = denom > 0.0;
+  bool rare = false;
 #pragma unroll
   for (int v = 0; v < NF; v++) {
     double fP = P.u[v] * vnP, fQ = Q.u[v] * vnQ;
@@ -226,8 +264,9 @@ OMB_HD double kt_axis(const KtState& P, const KtState& Q, int axis, bool flip, d
       fQ = fQ + Q.p * vnQ;
     }
     double num = (cP * fP + cQ * fQ) + sg * (Q.u[v] - P.u[v]);
-    out[v] = ok ? div_by(num, denom, rden) : (flip ? fQ : fP);
+    out[v] = ok ? div_by_nobranch(num, denom, rden, rare) : (flip ? fQ : fP);
   }
+  if (ok && rare) kt_quotients_ieee(P, Q, axis, vnP, vnQ, cP, cQ, sg, denom, out);
   return dmax(ap, -am);
 }
 

@@ -14,7 +14,7 @@ from paper_2107_10987_b200.hydro import SSP_RK3_STAGES
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
-SO = os.path.join(HERE, "native", "_build", "libomb_emu.so")
+SO = os.environ.get("OMB_EMU_SO") or os.path.join(HERE, "native", "_build", "libomb_emu.so")
 _lib = None
 
 
