@@ -250,7 +250,6 @@ OMB_HD double kt_axis(const KtState& P, const KtState& Q, int axis, bool flip, d
   double cQ = flip ? ap : -am;
   double sg = flip ? -apam : apam;
   bool ok = denom > 0.0;
-  bool rare = false;
 #pragma unroll
   for (int v = 0; v < NF; v++) {
     double fP = P.u[v] * vnP, fQ = Q.u[v] * vnQ;
@@ -264,9 +263,8 @@ OMB_HD double kt_axis(const KtState& P, const KtState& Q, int axis, bool flip, d
       fQ = fQ + Q.p * vnQ;
     }
     double num = (cP * fP + cQ * fQ) + sg * (Q.u[v] - P.u[v]);
-    out[v] = ok ? div_by_nobranch(num, denom, rden, rare) : (flip ? fQ : fP);
+    out[v] = ok ? div_by(num, denom, rden) : (flip ? fQ : fP);
   }
-  if (ok && rare) kt_quotients_ieee(P, Q, axis, vnP, vnQ, cP, cQ, sg, denom, out);
   return dmax(ap, -am);
 }
 
