@@ -364,9 +364,16 @@ struct Stage {
       double s[5];
 #pragma unroll
       for (int k = 0; k < 5; k++) s[k] = S[ad[k] + v * PL];
-      double lv = iface(s[0], s[1], s[2], s[3]);
-      double hv = iface(s[1], s[2], s[3], s[4]);
-      mono(s[2], lv, hv);
+      double lv, hv;
+      if (s[0] == s[2] && s[1] == s[2] && s[3] == s[2] && s[4] == s[2]) {
+        // flat stencil: both interface values are clamped to a and the
+        // extremum test then sets lo = hi = a (_core.pyx:80-97) -- exactly
+        lv = hv = s[2];
+      } else {
+        lv = iface(s[0], s[1], s[2], s[3]);
+        hv = iface(s[1], s[2], s[3], s[4]);
+        mono(s[2], lv, hv);
+      }
       lo[v] = lv;
       hi[v] = hv;
       if (v == 0)
