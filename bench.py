@@ -259,9 +259,9 @@ def gpu_arm(args, rank, world):
         tree = sedov_tree(level)
         eos = EosConfig(gamma=1.4)
     part = None
-    if world > 1:
-        from paper_2107_10987_b200.partition import Partition
+    from paper_2107_10987_b200.partition import Partition
 
+    if world > 1:
         part = Partition(tree, world, rank)
     st = B200HydroStepper(tree, eos, HydroMode("new"), host_sync=False, max_run=args.max_run, partition=part,
                           **extra)
@@ -342,6 +342,37 @@ def gpu_arm(args, rank, world):
                "h2d_bytes_per_step": nbytes, "d2h_bytes_per_step": nbytes + 2 * 8 + 4 + 6 * 8,
                "steps": args.e2e_steps, "api": "B200HydroStepper.cfl_dt + rk3_step (host_sync=True)"}
 
+    # the same step on a NON-FLAT state (every cell off the limiter's flat shortcut), same tree
+    nontrivial = None
+    if level in (4, 5) and args.e2e_steps >= 0:
+        from paper_2107_10987_b200.problems import smooth_state
+
+        t3 = smooth_state(sedov_tree(level))
+        p3 = Partition(t3, world, rank) if world > 1 else None
+        st3 = B200HydroStepper(t3, eos, HydroMode("new"), host_sync=False, max_run=args.max_run, partition=p3)
+        for _ in range(2):
+            st3._cfl_launch(0.4)
+            st3.launch_step(None)
+        K3 = max(3, min(10, K))
+        if dist is not None:
+            dist.barrier()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(K3):
+            st3._cfl_launch(0.4)
+            st3.launch_step(None)
+        e1.record()
+        torch.cuda.synchronize()
+        ms3 = e0.elapsed_time(e1)
+        if dist is not None:
+            t = torch.tensor([ms3], dtype=torch.float64, device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ms3 = float(t.item())
+        nontrivial = {"value": cells * K3 / (ms3 / 1e3), "unit": UNIT, "ms_per_step": ms3 / K3, "steps": K3,
+                      "state": "smooth sinusoidal field of the reference tests (test_hydro_step.py:37-49) on the "
+                               "same tree: no flat cells"}
+
     if rank != 0:
         return
     value = cells * K / (ms / 1e3)
@@ -375,6 +406,7 @@ def gpu_arm(args, rank, world):
                              "algorithmic_bytes_per_launch": BYTES_PER_CELL_STAGE * local_cells}},
         "clocks": clocks,
         "e2e": e2e,
+        "nontrivial_state": nontrivial,
         "gpu_launches": K * (5 + (6 if world > 1 else 0)),
         "cfl_abort_in_timed_steps": aborted,
     }
