@@ -227,21 +227,6 @@ OMB_HD_NOINLINE void kt_quotients_ieee(const KtState& P, const KtState& Q, int a
   }
 }
 
-// bitwise equality of two primitive 6-vectors (identical bits => identical
-// KtState, so the second state computation can be skipped)
-OMB_HD bool same_bits6(const double* a, const double* b) {
-  bool same = true;
-#pragma unroll
-  for (int v = 0; v < NF; v++) {
-#ifdef __CUDA_ARCH__
-    same = same && (__double_as_longlong(a[v]) == __double_as_longlong(b[v]));
-#else
-    same = same && (memcmp(&a[v], &b[v], 8) == 0);
-#endif
-  }
-  return same;
-}
-
 // Flux through an `axis` face across the interface P -> Q (P = cell the
 // `hi` state belongs to, Q = P + line direction, whose `lo` state is used).
 // When the line runs against the face normal (`flip`) the reference swaps

@@ -443,8 +443,7 @@ struct Stage {
       for (int v = 0; v < NF; v++) hp[v] = S[Smem::HI + (dl * NF + v) * NP + pp];
       KtState sP, sQ;
       kt_state(hp, A.gamma, A.gm1, A.inv_gm1, sP);
-      if (same_bits6(hp, lo)) sQ = sP;  // flat interface: identical state
-      else kt_state(lo, A.gamma, A.gm1, A.inv_gm1, sQ);
+      kt_state(lo, A.gamma, A.gm1, A.inv_gm1, sQ);
       // axes served by this line: x always; y for lines 3,4; z for 5,6; all for 9..12
       int ax_second = (l == 3 || l == 4) ? 1 : 2;
       int nax = l == 0 ? 1 : (l >= 9 ? 3 : 2);
@@ -575,15 +574,8 @@ struct Stage {
         ax0 = 1; nax = 2; dst = S + Smem::IPR + ((li * 2) * NF) * NCOR + c; stride = NCOR;
       }
       KtState sP, sQ;
-      double wP[NF], wQ[NF];
-#pragma unroll
-      for (int v = 0; v < NF; v++) {
-        wP[v] = S[Smem::LHI + ((ip * 2 + 1) * NF + v) * NP + pos10(py, pz)];
-        wQ[v] = S[Smem::LHI + ((ip * 2 + 0) * NF + v) * NP + pos10(qy, qz)];
-      }
-      kt_state(wP, A.gamma, A.gm1, A.inv_gm1, sP);
-      if (same_bits6(wP, wQ)) sQ = sP;
-      else kt_state(wQ, A.gamma, A.gm1, A.inv_gm1, sQ);
+      lhi_state(ip, 1, py, pz, sP);
+      lhi_state(ip, 0, qy, qz, sQ);
 #pragma unroll 1
       for (int k = 0; k < nax; k++) kt_into(sP, sQ, l, ax0 + k, dst + k * NF * NCOR, stride);
     }
