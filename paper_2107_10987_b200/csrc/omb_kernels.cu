@@ -264,11 +264,14 @@ __global__ void __launch_bounds__(NT, 1) k_stage(StageArgs A) {
   st.fb = 0;
   Hold h;
   const int R = st.R;
-  // prologue: planes 0..3 synchronously, plane 4 staged asynchronously
-  for (int X = 0; X < 4; X++) st.load_plane(X, tid, nthr);
+  // prologue: planes 0..3 staged in the (still unused) RAW union and plane 4
+  // in SG0, all loads in flight at once; then planes 0..3 converted
+  for (int X = 0; X < 4; X++) st.prefetch_plane(X, tid, nthr, Smem::RAW + X * NF * PL);
   st.prefetch_plane(4, tid, nthr);
   async_commit();
   async_wait_all();
+  __syncthreads();
+  for (int X = 0; X < 4; X++) st.convert_plane(X, tid, nthr, Smem::RAW + X * NF * PL);
   __syncthreads();
   for (int X = 2; X < 8 * R + 4; X++) {
     st.set_plane(X);

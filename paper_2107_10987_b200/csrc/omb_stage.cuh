@@ -135,6 +135,7 @@ struct Smem {
   static constexpr int BYTES = TOTAL * 8;
 };
 static_assert(Smem::BYTES <= 232448, "stage shared memory exceeds 227 KB");
+static_assert(Smem::RAW_SIZE >= 4 * NF * PL, "prologue staging of planes 0..3 uses the RAW union");
 
 // 8-byte global -> shared asynchronous copy (cp.async / LDGSTS on the GPU,
 // an immediate copy in the host emulation), completed by async_wait_all()
@@ -292,8 +293,8 @@ struct Stage {
     }
   }
 
-  // issue the asynchronous gather of padded plane Xn into SG0
-  OMB_HD void prefetch_plane(int Xn, int tid, int nthr) {
+  // issue the asynchronous gather of padded plane Xn into SG0 (or `stage`)
+  OMB_HD void prefetch_plane(int Xn, int tid, int nthr, int stage = Smem::SG0) {
     int leaf, lx;
     view_of(Xn, leaf, lx);
     const LeafInfo& LI = A.info[leaf];
@@ -301,12 +302,12 @@ struct Stage {
       int fm;
       long long base = gather_addr(LI, A.bc, lx, it / M, it % M, fm);
 #pragma unroll
-      for (int v = 0; v < NF; v++) async_copy8(S + Smem::SG0 + v * PL + it, A.ucur + v * A.fstride + base);
+      for (int v = 0; v < NF; v++) async_copy8(S + stage + v * PL + it, A.ucur + v * A.fstride + base);
     }
   }
 
   // P0: primitives of the staged plane Xn into the ring (flips re-derived)
-  OMB_HD void convert_plane(int Xn, int tid, int nthr) {
+  OMB_HD void convert_plane(int Xn, int tid, int nthr, int stage = Smem::SG0) {
     int leaf, lx;
     view_of(Xn, leaf, lx);
     const LeafInfo& LI = A.info[leaf];
@@ -315,7 +316,7 @@ struct Stage {
       gather_addr(LI, A.bc, lx, it / M, it % M, fm);
       double u[NF], w[NF];
 #pragma unroll
-      for (int v = 0; v < NF; v++) u[v] = S[Smem::SG0 + v * PL + it];
+      for (int v = 0; v < NF; v++) u[v] = S[stage + v * PL + it];
 #pragma unroll
       for (int a = 0; a < 3; a++)
         if ((fm >> a) & 1) u[1 + a] = -u[1 + a];

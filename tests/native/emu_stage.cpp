@@ -34,8 +34,9 @@ extern "C" int emu_stage(const OmbStageDesc* d, int nthr) {
     }
     int R = st[0].R;
 #define ALL(stmt) for (int t = 0; t < nthr; t++) { Stage& s = st[t]; (void)s; stmt; }
-    for (int X = 0; X < 4; X++) ALL(s.load_plane(X, t, nthr));
+    for (int X = 0; X < 4; X++) ALL(s.prefetch_plane(X, t, nthr, Smem::RAW + X * NF * PL));
     ALL(s.prefetch_plane(4, t, nthr));
+    for (int X = 0; X < 4; X++) ALL(s.convert_plane(X, t, nthr, Smem::RAW + X * NF * PL));
     for (int X = 2; X < 8 * R + 4; X++) {
       ALL(s.set_plane(X));
       ALL(if (X + 2 < 8 * R + 6) s.convert_plane(X + 2, t, nthr));
