@@ -220,7 +220,7 @@ __global__ void k_fluxes(const double* __restrict__ lo, const double* __restrict
 // ---------------------------------------------------------------------------
 // fused stage: one CTA per run
 // ---------------------------------------------------------------------------
-constexpr int STAGE_THREADS = 512;  // max threads of any k_stage variant
+constexpr int STAGE_THREADS = 512;
 
 __device__ __forceinline__ void block_reduce(double amax, long long fb, unsigned long long* amax_bits,
                                              unsigned long long* fallback) {
@@ -622,25 +622,14 @@ int omb_stage(const OmbStageDesc* d, void* stream) {
   if (d->ucur == d->unext) return set_err("omb_stage: unext must not alias ucur");
   static bool attr_set = false;
   if (!attr_set) {
-    CK(cudaFuncSetAttribute(k_stage<512>, cudaFuncAttributeMaxDynamicSharedMemorySize, Smem::BYTES), "smem attribute");
-    CK(cudaFuncSetAttribute(k_stage<384>, cudaFuncAttributeMaxDynamicSharedMemorySize, Smem::BYTES), "smem attribute");
-    CK(cudaFuncSetAttribute(k_stage<256>, cudaFuncAttributeMaxDynamicSharedMemorySize, Smem::BYTES), "smem attribute");
-    CK(cudaFuncSetAttribute(k_stage<576>, cudaFuncAttributeMaxDynamicSharedMemorySize, Smem::BYTES), "smem attribute");
-    CK(cudaFuncSetAttribute(k_stage<640>, cudaFuncAttributeMaxDynamicSharedMemorySize, Smem::BYTES), "smem attribute");
+    // 512 threads x 128 registers fills the register file; 256/384/576/640 were measured slower
+    CK(cudaFuncSetAttribute(k_stage<STAGE_THREADS>, cudaFuncAttributeMaxDynamicSharedMemorySize, Smem::BYTES),
+       "smem attribute");
     attr_set = true;
   }
-  static int nt = [] {
-    const char* e = getenv("OMB_STAGE_THREADS");
-    int v = e ? atoi(e) : 512;
-    return (v == 256 || v == 384 || v == 576 || v == 640) ? v : 512;
-  }();
   StageArgs A = stage_args(d);
   if (d->nruns <= 0) return 0;
-  if (nt == 512) k_stage<512><<<d->nruns, 512, Smem::BYTES, (cudaStream_t)stream>>>(A);
-  else if (nt == 384) k_stage<384><<<d->nruns, 384, Smem::BYTES, (cudaStream_t)stream>>>(A);
-  else if (nt == 576) k_stage<576><<<d->nruns, 576, Smem::BYTES, (cudaStream_t)stream>>>(A);
-  else if (nt == 640) k_stage<640><<<d->nruns, 640, Smem::BYTES, (cudaStream_t)stream>>>(A);
-  else k_stage<256><<<d->nruns, 256, Smem::BYTES, (cudaStream_t)stream>>>(A);
+  k_stage<STAGE_THREADS><<<d->nruns, STAGE_THREADS, Smem::BYTES, (cudaStream_t)stream>>>(A);
   CK(cudaGetLastError(), "omb_stage launch");
   return 0;
 }

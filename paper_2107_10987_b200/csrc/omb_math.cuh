@@ -19,10 +19,8 @@
 
 #ifdef __CUDACC__
 #define OMB_HD __host__ __device__ __forceinline__
-#define OMB_HD_NOINLINE __host__ __device__ __noinline__
 #else
 #define OMB_HD inline
-#define OMB_HD_NOINLINE inline
 #endif
 
 namespace omb {
@@ -65,29 +63,6 @@ OMB_HD double div_by(double a, double b, double y) {
   return q2;
 }
 
-// div_by without its rare-case branch: zero numerators go through a select
-// (a/b == a*(1/b) for a == 0); `rare` is raised -- by an integer test of the
-// exponent of q1 -- when the theorem's no-underflow/overflow premise may fail
-// (or the quotient is not finite); the caller then redoes its quotients with
-// the IEEE division.  One branch per group of quotients instead of one each.
-OMB_HD unsigned dbl_exp(double x) {
-#ifdef __CUDA_ARCH__
-  return (unsigned)(__double_as_longlong(x) >> 52) & 0x7ffu;
-#else
-  unsigned long long b;
-  memcpy(&b, &x, 8);
-  return (unsigned)(b >> 52) & 0x7ffu;
-#endif
-}
-OMB_HD double div_by_nobranch(double a, double b, double y, bool& rare) {
-  double q0 = a * y;
-  double q1 = fma(fma(-b, q0, a), y, q0);
-  double q2 = fma(fma(-b, q1, a), y, q1);
-  bool z = (a == 0.0);
-  rare |= !z && (dbl_exp(q1) - 24u > 2000u);  // |q1| outside [2^-999, 2^1001) or inf/NaN
-  return z ? a * y : q2;
-}
-
 // NaN-faithful helpers: C fmin/fmax semantics (IEEE minNum/maxNum), as libm.
 OMB_HD double dmin(double a, double b) { return fmin(a, b); }
 OMB_HD double dmax(double a, double b) { return fmax(a, b); }
@@ -113,22 +88,6 @@ OMB_HD double iface(double am1, double a, double ap1, double ap2) {
 // multiply by RN(1/6) and the exact IEEE division is taken only when the
 // comparison margin is within a guard band of 8 ulp -- the branch outcomes
 // (hence the outputs) are identical to the reference's.
-#if defined(OMB_MONO_BF)
-OMB_HD void mono(double a, double& lv, double& hv) {  // experimental branch-free variant
-  bool ext = (hv - a) * (a - lv) <= 0.0;
-  double diff = hv - lv;
-  double mid = a - 0.5 * (lv + hv);
-  double dm = diff * mid;
-  double d2 = diff * diff;
-  double q = d2 * (1.0 / 6.0);
-  double band = 0x1p-49 * fabs(q) + 0x1p-1000;
-  if (!ext && (!(fabs(dm - q) > band) || !(fabs(dm + q) > band))) q = d2 / 6.0;
-  double nlv = (dm > q) ? 3.0 * a - 2.0 * hv : lv;
-  double nhv = (-q > dm) ? 3.0 * a - 2.0 * nlv : hv;
-  lv = ext ? a : nlv;
-  hv = ext ? a : nhv;
-}
-#else
 OMB_HD void mono(double a, double& lv, double& hv) {
   if ((hv - a) * (a - lv) <= 0.0) {
     lv = a;
@@ -148,7 +107,6 @@ OMB_HD void mono(double a, double& lv, double& hv) {
   lv = nlv;
   hv = nhv;
 }
-#endif
 
 // _core.pyx:159-173
 OMB_HD double mc_slope(double am1, double a, double ap1) {
@@ -206,25 +164,6 @@ OMB_HD void kt_state(const double* w, double gamma, double gm1, double inv_gm1, 
   s.u[3] = s.r * s.v[2];
   s.u[4] = div_by(s.p, gm1, inv_gm1) + kin;
   s.u[5] = w[5];
-}
-
-// IEEE-division fallback of kt_axis (never inlined: it is almost never run)
-OMB_HD_NOINLINE void kt_quotients_ieee(const KtState& P, const KtState& Q, int axis, double vnP, double vnQ,
-                                       double cP, double cQ, double sg, double denom, double* out) {
-#pragma unroll
-  for (int v = 0; v < NF; v++) {
-    double fP = P.u[v] * vnP, fQ = Q.u[v] * vnQ;
-    if (v == 1 || v == 2 || v == 3) {
-      bool nrm = (v == 1 + axis);
-      fP = nrm ? fP + P.p : fP;
-      fQ = nrm ? fQ + Q.p : fQ;
-    }
-    if (v == 4) {
-      fP = fP + P.p * vnP;
-      fQ = fQ + Q.p * vnQ;
-    }
-    out[v] = ((cP * fP + cQ * fQ) + sg * (Q.u[v] - P.u[v])) / denom;
-  }
 }
 
 // Flux through an `axis` face across the interface P -> Q (P = cell the
