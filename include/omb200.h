@@ -119,6 +119,10 @@ int omb_selftest_div(unsigned long long seed, long long n, unsigned long long *b
  * and the [6][L][n^3] device layout; multithreaded, used around H2D/D2H copies */
 int omb_host_pack(const double *const *leaf_u, int L, int n, long long fstride, double *out);
 int omb_host_unpack(const double *in, int L, int n, long long fstride, double *const *leaf_u);
+/* multi-GPU AMR: gather rows idx[0..n) of length `row` into a contiguous message / scatter them back
+ * (the exported face-flux slots the reflux of step.py:206-241 reads across ranks) */
+int omb_gather_rows(const double *src, long long row, const int *idx, int n, double *out, void *stream);
+int omb_scatter_rows(const double *in, long long row, const int *idx, int n, double *dst, void *stream);
 /* device-side diagnostics / IO: per-leaf field sums for conservation_totals
  * (problems/diagnostics.py:9-30; fixed summation order), and the checkpoint payload order
  * (mesh/checkpoint.py:34-55: per leaf, 6 fields, x fastest) */

@@ -17,7 +17,8 @@ _lib = None
 
 EXPORTS = ("omb_abi_version", "omb_last_error", "omb_stage_smem_bytes", "omb_primitives", "omb_reconstruct",
            "omb_fluxes", "omb_stage", "omb_cfl", "omb_gather", "omb_fp64_peak", "omb_pack_leaves", "omb_unpack_leaves", "omb_selftest_div", "omb_host_pack", "omb_host_unpack", "omb_amr_ghosts",
-           "omb_reflux_update", "omb_leaf_sums", "omb_disk_order")
+           "omb_reflux_update", "omb_leaf_sums", "omb_disk_order",
+           "omb_gather_rows", "omb_scatter_rows")
 
 
 def load():
@@ -46,6 +47,8 @@ def load():
     L.omb_amr_ghosts.argtypes = [ctypes.POINTER(OmbAmrDesc), vp]
     L.omb_leaf_sums.argtypes = [vp, ll, i, vp, vp]
     L.omb_disk_order.argtypes = [vp, ll, i, vp, vp]
+    L.omb_gather_rows.argtypes = [vp, ll, vp, i, vp, vp]
+    L.omb_scatter_rows.argtypes = [vp, ll, vp, i, vp, vp]
     L.omb_reflux_update.argtypes = [ctypes.POINTER(OmbRefluxDesc), vp]
     for fn in EXPORTS[3:]:
         getattr(L, fn).restype = i

@@ -83,7 +83,7 @@ class LeafBatch:
     only provide ghost data.  ``gnbr`` optionally supplies the neighbour
     table in global indices with ``gids`` the global index of each leaf."""
 
-    def __init__(self, tree, max_run=4, leaves=None, ncompute=None, gnbr=None, gids=None):
+    def __init__(self, tree, max_run=4, leaves=None, ncompute=None, gnbr=None, gids=None, extra_exporters=()):
         self.tree = tree
         self.n = tree.n
         if self.n != 8:
@@ -95,7 +95,7 @@ class LeafBatch:
         self.L = len(self.leaves)
         self.ncompute = self.L if ncompute is None else ncompute
         if gnbr is None:
-            gnbr = neighbor_table(tree, self.leaves, allow_amr=(ncompute is None))
+            gnbr = neighbor_table(tree, self.leaves, allow_amr=True)
             gids = np.arange(self.L)
         local = {int(g): i for i, g in enumerate(gids)}
         self.amr = bool(np.any(gnbr == AMR))
@@ -129,13 +129,14 @@ class LeafBatch:
         self.reflux_leaf = np.zeros(0, dtype=np.int32)
         self.reflux_tasks = np.zeros((0, 6), dtype=np.int32)
         self.solo = np.zeros(self.L, dtype=bool)
+        self.slot_of = {}
         if self.amr:
-            self._build_amr()
+            self._build_amr(extra_exporters)
         self.fstride = (self.L + self.nvirtual) * 512
         self._build_runs(max_run)
 
     # -- AMR: virtual neighbour leaves, flux export, reflux --------------------
-    def _build_amr(self):
+    def _build_amr(self, extra_exporters=()):
         """Coarse/fine neighbour regions become VIRTUAL leaves (indices L..):
         before each stage omb_amr_ghosts fills, in a virtual leaf's interior,
         exactly the cells the stage kernel's gather reads for that region,
@@ -210,9 +211,12 @@ class LeafBatch:
             get_slot(i)
             for (_, _, j, _, _) in rtasks[i]:
                 get_slot(j)
+        for j in extra_exporters:  # owned fine leaves whose fluxes other ranks' reflux reads
+            get_slot(int(j))
         self.flux_slots = len(slot)
+        self.slot_of = dict(slot)
         for j, sl in slot.items():
-            self.info[j]["flags"] |= 1  # export face fluxes
+            self.info[j]["flags"] |= 1  # export face fluxes (halo leaves: received instead)
             self.info[j]["slot"] = sl
             self.solo[j] = True
         self.reflux_leaf = np.array(sorted(rtasks), dtype=np.int32)

@@ -508,6 +508,17 @@ __global__ void k_selftest_div(unsigned long long seed, long long n, unsigned lo
   if (nb) atomicAdd(bad, nb);
 }
 
+// row gather / scatter (multi-GPU AMR: exchange of exported flux slots)
+__global__ void k_rows(const double* __restrict__ src, long long row, const int* __restrict__ idx, int n,
+                       double* __restrict__ dst, int scatter) {
+  long long total = (long long)n * row;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total; i += (long long)gridDim.x * blockDim.x) {
+    long long k = i / row, c = i % row;
+    if (scatter) dst[(long long)idx[k] * row + c] = src[i];
+    else dst[i] = src[(long long)idx[k] * row + c];
+  }
+}
+
 // FP64 pipe peak probe (roofline denominator; MEASURED_PEAKS.json has no FP64 entry):
 // 8 independent DFMA chains per thread, 2 flops per DFMA.
 __global__ void k_dfma_peak(double* out, int iters) {
@@ -659,6 +670,24 @@ int omb_disk_order(const double* U, long long fstride, int L, double* out, void*
   int blocks = (int)((total + 255) / 256);
   k_disk_order<<<blocks < 148 * 16 ? blocks : 148 * 16, 256, 0, (cudaStream_t)stream>>>(U, fstride, L, out);
   CK(cudaGetLastError(), "omb_disk_order launch");
+  return 0;
+}
+
+int omb_gather_rows(const double* src, long long row, const int* idx, int n, double* out, void* stream) {
+  if (n <= 0) return 0;
+  long long total = (long long)n * row;
+  int blocks = (int)((total + 255) / 256);
+  k_rows<<<blocks < 148 * 16 ? blocks : 148 * 16, 256, 0, (cudaStream_t)stream>>>(src, row, idx, n, out, 0);
+  CK(cudaGetLastError(), "omb_gather_rows launch");
+  return 0;
+}
+
+int omb_scatter_rows(const double* in, long long row, const int* idx, int n, double* dst, void* stream) {
+  if (n <= 0) return 0;
+  long long total = (long long)n * row;
+  int blocks = (int)((total + 255) / 256);
+  k_rows<<<blocks < 148 * 16 ? blocks : 148 * 16, 256, 0, (cudaStream_t)stream>>>(in, row, idx, n, dst, 1);
+  CK(cudaGetLastError(), "omb_scatter_rows launch");
   return 0;
 }
 

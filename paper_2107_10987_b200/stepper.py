@@ -82,8 +82,6 @@ class B200HydroStepper:
         self._cfl_badleaf = T.empty(1, dtype=T.int32, device=dev)
         self._pinned = T.zeros(n, dtype=T.float64).pin_memory()
         # AMR (coarse/fine neighbours): virtual-leaf ghost tasks, flux export slots, reflux lists
-        if partition is not None and b.amr:
-            raise NotImplementedError("AMR trees run on a single GPU for now")
         self._amr_tasks = T.from_numpy(b.amr_tasks.reshape(-1).copy()).to(dev) if b.nvirtual else None
         self._flux = T.empty(max(1, b.flux_slots) * FLUX_SLOT_DOUBLES, dtype=T.float64, device=dev) \
             if b.flux_slots else None
@@ -99,6 +97,13 @@ class B200HydroStepper:
             self._sendbuf = T.empty(max(1, sum(partition.send_counts)) * 3072, dtype=T.float64, device=dev)
             self._recvbuf = T.empty(max(1, sum(partition.recv_counts)) * 3072, dtype=T.float64, device=dev)
             self._gids = partition.gids
+            if partition.amr and (sum(partition.flux_send_counts) or sum(partition.flux_recv_counts)):
+                self._fsend = T.from_numpy(partition.flux_send_slots.copy()).to(dev)
+                self._frecv = T.from_numpy(partition.flux_recv_slots.copy()).to(dev)
+                self._fsendbuf = T.empty(max(1, sum(partition.flux_send_counts)) * FLUX_SLOT_DOUBLES,
+                                         dtype=T.float64, device=dev)
+                self._frecvbuf = T.empty(max(1, sum(partition.flux_recv_counts)) * FLUX_SLOT_DOUBLES,
+                                         dtype=T.float64, device=dev)
         self.upload()
 
     # -- host <-> device -------------------------------------------------------------
@@ -138,6 +143,22 @@ class B200HydroStepper:
         p = self.part
         exchange(self.dist, self.group, self._buf[buf_index], self._send_idx, p.send_counts, p.recv_counts, p.nown,
                  pack, unpack, self._sendbuf, self._recvbuf)
+
+    def _exchange_fluxes(self, stream=None):
+        """Second exchange of AMR multi-GPU runs: exported face fluxes of fine leaves
+        whose coarse face-neighbour lives on another rank (reflux, step.py:206-241)."""
+        p = self.part
+        sh = stream_handle(stream)
+        row = FLUX_SLOT_DOUBLES
+        ns, nr = sum(p.flux_send_counts), sum(p.flux_recv_counts)
+        if ns:
+            _lib.check(self.lib.omb_gather_rows(ptr(self._flux), row, ptr(self._fsend), ns, ptr(self._fsendbuf), sh),
+                       "omb_gather_rows")
+        self.dist.all_to_all_single(self._frecvbuf[:nr * row], self._fsendbuf[:ns * row], [c * row for c in p.flux_recv_counts],
+                                    [c * row for c in p.flux_send_counts], group=self.group)
+        if nr:
+            _lib.check(self.lib.omb_scatter_rows(ptr(self._frecvbuf), row, ptr(self._frecv), nr, ptr(self._flux), sh),
+                       "omb_scatter_rows")
 
     # -- timestep ---------------------------------------------------------------------
     def _cfl_launch(self, cfl, stream=None):
@@ -219,6 +240,8 @@ class B200HydroStepper:
             _lib.check(self.lib.omb_stage(ctypes.byref(d), sh), "omb_stage")
             if events is not None:
                 events[s][1].record()
+            if getattr(self, "_fsend", None) is not None:
+                self._exchange_fluxes(stream)
             if self._rleaf is not None:
                 rd = OmbRefluxDesc(stage=d, leaf=ptr(self._rleaf), off=ptr(self._roff), tasks=ptr(self._rtasks),
                                    nleaves=len(self.batch.reflux_leaf))

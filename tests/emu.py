@@ -133,14 +133,36 @@ class EmuDistStepper:
         unpack(recv, U, p.nown)
         _ = exchange  # the product's helper is exercised on the GPU path
 
+    def _exchange_fluxes(self, flux):
+        import torch
+
+        p = self.part
+        row = FLUX_SLOT_DOUBLES
+        ns, nr = sum(p.flux_send_counts), sum(p.flux_recv_counts)
+        send = np.zeros(max(1, ns) * row)
+        recv = np.zeros(max(1, nr) * row)
+        fl = flux.reshape(-1, row)
+        send[:ns * row] = fl[p.flux_send_slots].reshape(-1)
+        self.dist.all_to_all_single(torch.from_numpy(recv[:nr * row]), torch.from_numpy(send[:ns * row]),
+                                    [c * row for c in p.flux_recv_counts], [c * row for c in p.flux_send_counts])
+        fl[p.flux_recv_slots] = recv[:nr * row].reshape(nr, row)
+
     def rk3_step(self, dt):
         b = self.b
         U0 = np.ascontiguousarray(b.pack())
         bufs = [U0, np.empty_like(U0), np.empty_like(U0), np.empty_like(U0)]
         dtv = np.array([dt])
+        flux = np.zeros(max(1, b.flux_slots) * FLUX_SLOT_DOUBLES)
+        tasks = np.ascontiguousarray(b.amr_tasks.reshape(-1))
+        rleaf, roff = np.ascontiguousarray(b.reflux_leaf), np.ascontiguousarray(b.reflux_off)
+        rtasks = np.ascontiguousarray(b.reflux_tasks.reshape(-1))
+        self.amax = 0.0
         cur = 0
         for s, (a, bb) in enumerate(SSP_RK3_STAGES):
             self._exchange(bufs[cur])
+            if b.nvirtual:
+                lib().emu_amr_ghosts(ctypes.byref(OmbAmrDesc(u=ptr(bufs[cur]), fstride=b.fstride, tasks=ptr(tasks),
+                                                              ntasks=b.nvirtual)))
             am = np.zeros(1, dtype=np.uint64)
             fb = np.zeros(1, dtype=np.uint64)
             nxt = s + 1
@@ -149,7 +171,13 @@ class EmuDistStepper:
                              run_leaf=ptr(self.run_leaf), nruns=b.nruns, dt=ptr(dtv), a=a, b=bb,
                              gamma=self.gamma, gm1=self.gamma - 1.0, eta=1e-3, inv_gamma=1.0 / self.gamma,
                              omega=0.0, floor_rho=0.0, floor_tau=0.0, floor_vmax=0.0, bc=b.bc, new_mode=1,
-                             override_center=0, contact=0, amax_bits=ptr(am), fallback=ptr(fb))
+                             override_center=0, contact=0, amax_bits=ptr(am), fallback=ptr(fb), flux=ptr(flux))
             lib().emu_stage(ctypes.byref(d), self.nthr)
+            if self.part.amr:
+                self._exchange_fluxes(flux)
+            if len(rleaf):
+                lib().emu_reflux_update(ctypes.byref(OmbRefluxDesc(stage=d, leaf=ptr(rleaf), off=ptr(roff),
+                                                                   tasks=ptr(rtasks), nleaves=len(rleaf))))
+            self.amax = max(self.amax, float(am.view(np.float64)[0]))
             cur = nxt
         b.unpack(bufs[cur])

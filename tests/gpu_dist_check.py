@@ -3,7 +3,8 @@
     python -m torch.distributed.run --nproc-per-node N --master-addr 127.0.0.1 tests/gpu_dist_check.py
 
 Each rank advances its leaf partition of the Sedov c1 tree (and of the
-smooth periodic case) with the NCCL halo exchange and compares its leaves
+smooth periodic case and two AMR trees, whose coarse/fine ghost sources and
+reflux face fluxes cross ranks) with the NCCL halo + flux-slot exchanges and compares its leaves
 with the single-process golden state bitwise; dt must equal the golden dt.
 Exit code 0 = parity."""
 
@@ -31,7 +32,7 @@ def main():
     dist.init_process_group("nccl", device_id=torch.device("cuda", lr))
     rank, world = dist.get_rank(), dist.get_world_size()
     bad = 0
-    for name, steps in (("sedov_c1", 3), ("smooth_periodic", 1)):
+    for name, steps in (("sedov_c1", 3), ("smooth_periodic", 1), ("amr_reflux", 2), ("amr_sedov_small", 1)):
         t, g = case_tree(name)
         part = Partition(t, world, rank)
         st = B200HydroStepper(t, EOS, HydroMode("new"), partition=part, max_run=2)

@@ -48,7 +48,7 @@ def test_neighbor_table_fast_path_matches_generic():
                 assert fast[i, q] == want
 
 
-def _worker(rank, world, port, out):
+def _worker(rank, world, port, out, case="sedov_c1"):
     import torch.distributed as dist
 
     os.environ["MASTER_ADDR"] = "127.0.0.1"
@@ -58,7 +58,7 @@ def _worker(rank, world, port, out):
         from _cases import case_tree, state_of
         from emu import EmuDistStepper
 
-        t, g = case_tree("sedov_c1")
+        t, g = case_tree(case)
         st = EmuDistStepper(t, 1.4, world, rank, max_run=2)
         st.rk3_step(float(g["dts"][0]))
         mine = state_of(t)[st.part.bounds[rank]:st.part.bounds[rank + 1]]
@@ -68,7 +68,11 @@ def _worker(rank, world, port, out):
         dist.destroy_process_group()
 
 
-def test_two_rank_gloo_step_bitwise(tmp_path):
+@pytest.mark.parametrize("case,world", [("sedov_c1", 2), ("amr_reflux", 2), ("amr_reflux", 3),
+                                        ("amr_sedov_small", 3)])
+def test_multi_rank_gloo_step_bitwise(tmp_path, case, world):
+    """World 2/3 on CPU (gloo): halo exchange, AMR ghost sources across ranks and the
+    second (flux-slot) exchange for reflux must reproduce the single-rank golden step."""
     import sys
 
     import torch.multiprocessing as mp
@@ -79,6 +83,11 @@ def test_two_rank_gloo_step_bitwise(tmp_path):
     with socket.socket() as s:
         s.bind(("127.0.0.1", 0))
         port = s.getsockname()[1]
-    mp.spawn(_worker, args=(2, port, str(tmp_path)), nprocs=2, join=True)
-    for r in range(2):
+    if case != "sedov_c1":
+        from _cases import case_tree
+
+        t, _ = case_tree(case)
+        assert sum(sum(Partition(t, world, r).flux_send_counts) for r in range(world)) > 0
+    mp.spawn(_worker, args=(world, port, str(tmp_path), case), nprocs=world, join=True)
+    for r in range(world):
         assert int(np.load(tmp_path / f"r{r}.npy")[0]) == 0
