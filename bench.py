@@ -208,7 +208,7 @@ def reference_arm(args, rank, world):
             "config": {"workload": f"{workload_name(level, None)}, reflecting, cfl 0.4; CPU sample per step"},
             "cpu_baseline": {"value": v, "unit": UNIT, "cores": nthr, "kind": "port", "sample": sample},
             "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
-    print(json.dumps(line), flush=True)
+    emit(line)
 
 
 # ---------------------------------------------------------------------------
@@ -407,18 +407,33 @@ def gpu_arm(args, rank, world):
         "clocks": clocks,
         "e2e": e2e,
         "nontrivial_state": nontrivial,
-        "gpu_launches": K * (5 + (6 if world > 1 else 0)),
+        "gpu_launches": K * st.native_launches_per_step(),
         "cfl_abort_in_timed_steps": aborted,
     }
     if not args.no_cpu_baseline and world == 1:
         v, nthr, sample, _ = cpu_run(level, min(args.cpu_leaves, st.batch.L), 1, 0)
         line["cpu_baseline"] = {"value": v, "unit": UNIT, "cores": nthr, "kind": "port", "sample": sample}
-    print(json.dumps(line), flush=True)
+    emit(line)
+
+
+_JSON_OUT = None
+
+
+def emit(line):
+    """Print the one JSON result line on the real stdout (fd 1 is pointed at stderr
+    while the job runs, so NCCL's "NCCL version" banner cannot land on stdout)."""
+    out = _JSON_OUT if _JSON_OUT is not None else sys.stdout
+    out.write(json.dumps(line) + "\n")
+    out.flush()
 
 
 def main():
-    # NCCL writes its version/debug lines to stdout; keep stdout for the single JSON line
+    global _JSON_OUT
+    # NCCL writes its version banner to fd 1 from C; keep stdout for the single JSON line
     os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
+    sys.stdout.flush()
+    _JSON_OUT = os.fdopen(os.dup(1), "w")
+    os.dup2(2, 1)
     args = parse()
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))

@@ -252,6 +252,18 @@ class B200HydroStepper:
         self._state = outs[2]
         return start, outs
 
+    def native_launches_per_step(self):
+        """Kernels of libomb200 one cfl launch + launch_step enqueue (k_cfl_leaf/reduce,
+        then per stage: halo pack/unpack, AMR ghosts, k_stage, flux rows, reflux)."""
+        per = 1
+        p = self.part
+        if p is not None:
+            per += int(sum(p.send_counts) > 0) + int(sum(p.recv_counts) > 0)
+            if getattr(self, "_fsend", None) is not None:
+                per += int(sum(p.flux_send_counts) > 0) + int(sum(p.flux_recv_counts) > 0)
+        per += int(self._amr_tasks is not None) + int(self._rleaf is not None)
+        return 2 + 3 * per
+
     def _reduce_stats(self):
         if self.part is not None:
             self.dist.all_reduce(self._acc[:3], op=self.dist.ReduceOp.MAX, group=self.group)
