@@ -113,12 +113,23 @@ int omb_cfl(const OmbCflDesc *desc, void *stream);
  * unpack such a message into leaf slots first..first+n of a state */
 int omb_pack_leaves(const double *u, long long fstride, const int *idx, int n, double *out, void *stream);
 int omb_unpack_leaves(const double *in, int n, double *u, long long fstride, int first, void *stream);
-/* self-test: counts (into *bad) quotients where the kernels' reciprocal-based division differs from IEEE */
+/* self-test: counts (into bad[0]) quotients where the kernels' reciprocal-based divisions (div_by,
+ * the straight-line KT form, div_nz) differ from IEEE; bad[1..5] = first mismatch (a, b, a/b, div_by, KT form)
+ * as bit patterns, bad[7] = claimed flag.  bad must hold 8 zeroed counters. */
 int omb_selftest_div(unsigned long long seed, long long n, unsigned long long *bad, void *stream);
 /* host (CPU) packing between per-leaf padded arrays (6, n+6, n+6, n+6) -- SubGrid.u, tree.py:47-61 --
  * and the [6][L][n^3] device layout; multithreaded, used around H2D/D2H copies */
 int omb_host_pack(const double *const *leaf_u, int L, int n, long long fstride, double *out);
 int omb_host_unpack(const double *in, int L, int n, long long fstride, double *const *leaf_u);
+/* the same fused with the host<->device copy of a [6][fstride] device state (the e2e path of
+ * HydroStepper's host state of record, step.py:94-102): leaves cut into nchunks chunks, host threads
+ * pack chunk c into the pinned buffer while chunk c-1 is copied (upload), or unpack chunk c while
+ * chunk c+1 is in flight (download).  upload returns with copies still queued on `stream`;
+ * download returns with the host arrays written. */
+int omb_host_upload(const double *const *leaf_u, int L, int n, long long fstride, double *pinned, double *dev,
+                    int nchunks, void *stream);
+int omb_host_download(const double *dev, double *pinned, int L, int n, long long fstride, double *const *leaf_u,
+                      int nchunks, void *stream);
 /* multi-GPU AMR: gather rows idx[0..n) of length `row` into a contiguous message / scatter them back
  * (the exported face-flux slots the reflux of step.py:206-241 reads across ranks) */
 int omb_gather_rows(const double *src, long long row, const int *idx, int n, double *out, void *stream);

@@ -15,6 +15,8 @@ between them are computed once.  Runs are capped at ``max_run`` leaves to
 keep >= a few waves of CTAs on 148 SMs.
 """
 
+import operator
+
 import numpy as np
 
 from ._abi import AMR_TASK_INTS, BC_CODES, LEAF_INFO_DTYPE
@@ -264,12 +266,22 @@ class LeafBatch:
 
     # -- host <-> packed state --------------------------------------------------
     def _leaf_ptrs(self, count):
+        """Data pointers of the first ``count`` leaves' padded host arrays
+        (SubGrid.u), or None if one is not a C-contiguous float64 (6, 14, 14, 14)
+        array.  Cached: rebuilt only when a leaf's array object changed (the
+        cache holds the arrays, so their memory cannot be reused meanwhile)."""
+        arrs = [lf.subgrid.u for lf in self.leaves[:count]]
+        cache = getattr(self, "_ptr_cache", {}).get(count)
+        if cache is not None and all(map(operator.is_, arrs, cache[0])):
+            return cache[1]
         ptrs = np.empty(count, dtype=np.uintp)
-        for i, lf in enumerate(self.leaves[:count]):
-            u = lf.subgrid.u
-            if not (u.flags.c_contiguous and u.dtype == np.float64):
+        for i, u in enumerate(arrs):
+            if not (u.flags.c_contiguous and u.dtype == np.float64 and u.shape == (NFIELDS, 14, 14, 14)):
                 return None
             ptrs[i] = u.__array_interface__["data"][0]
+        if not hasattr(self, "_ptr_cache"):
+            self._ptr_cache = {}
+        self._ptr_cache[count] = (arrs, ptrs)
         return ptrs
 
     def pack(self, out=None, lib=None):

@@ -6,6 +6,9 @@
 #include <stdlib.h>
 #include <string.h>
 
+#include <atomic>
+#include <condition_variable>
+#include <functional>
 #include <mutex>
 #include <thread>
 #include <vector>
@@ -251,6 +254,7 @@ __device__ __forceinline__ void block_reduce(double amax, long long fb, unsigned
 
 template <int NT>
 __global__ void __launch_bounds__(NT, 1) k_stage(StageArgs A) {
+  static_assert(NT >= 2 * NFACEX, "P6 runs on the last 64 threads of the last P1 group");
   extern __shared__ double S[];
   const int tid = threadIdx.x, nthr = blockDim.x;
   Stage st;
@@ -273,16 +277,25 @@ __global__ void __launch_bounds__(NT, 1) k_stage(StageArgs A) {
   __syncthreads();
   for (int X = 0; X < 4; X++) st.convert_plane(X, tid, nthr, Smem::RAW + X * NF * PL);
   __syncthreads();
+  const int ngroups = A.new_mode ? 2 : 1;
   for (int X = 2; X < 8 * R + 4; X++) {
     st.set_plane(X);
     if (X + 2 < 8 * R + 6) st.convert_plane(X + 2, tid, nthr);  // P0
     __syncthreads();
     if (X + 3 < 8 * R + 6) st.prefetch_plane(X + 3, tid, nthr);  // stage next P0 (cp.async)
     async_commit();
-    const int ngroups = A.new_mode ? 2 : 1;
+    // P6 = the update of plane X-2 (its x fluxes sit in the 3-slot FX ring,
+    // its y/z fluxes in FYZ until this plane's P5, its inputs staged in SG6)
+    // runs on the last 64 threads, idle in the last P1 group (<= 400 items)
+    const bool p6 = X >= 3 && st.interior(X - 2);
 #pragma unroll 1
     for (int g = 0; g < ngroups; g++) {
       st.boundary_lines(g, tid, nthr, h);  // P1
+      if (g == ngroups - 1 && p6 && tid >= nthr - NFACEX) {
+        st.set_plane(X - 1);
+        st.update_plane(tid - (nthr - NFACEX), NFACEX);
+        st.set_plane(X);
+      }
       __syncthreads();
       st.store_hi(h);
       if (X >= 3) {  // P2
@@ -293,15 +306,7 @@ __global__ void __launch_bounds__(NT, 1) k_stage(StageArgs A) {
     }
     st.inplane_lines(tid, nthr);  // P3
     __syncthreads();
-    // P4 (in-plane fluxes, <= 306 items) shares a phase with P6 = the update
-    // of plane X-2 (64 items; its x fluxes sit in the 3-slot FX ring, its
-    // y/z fluxes in FYZ until this step's P5, its inputs staged in SG6)
-    if (st.interior(X)) st.inplane_fluxes(tid, nthr);
-    if (X >= 3 && st.interior(X - 2)) {
-      st.set_plane(X - 1);
-      st.update_plane_offset(tid, nthr, NYF + NZF + 2 * NCOR);
-      st.set_plane(X);
-    }
+    if (st.interior(X)) st.inplane_fluxes(tid, nthr);  // P4 (<= 306 items)
     __syncthreads();
     if (st.interior(X - 1)) st.prefetch_update(X - 1, tid, nthr);  // stage next P6
     async_commit();
@@ -496,14 +501,37 @@ __global__ void k_selftest_div(unsigned long long seed, long long n, unsigned lo
     for (int j = 0; j < 2; j++) {
       s ^= s << 13; s ^= s >> 7; s ^= s << 17;
       unsigned long long m = s & 0xFFFFFFFFFFFFFull;
-      int e = (int)((s >> 52) % 121) - 60;
-      unsigned long long bits = ((unsigned long long)(e + 1023) << 52) | m | ((s >> 63) << 63);
+      // 1 in 4: any biased exponent (subnormals, huge, inf/NaN); else |e| <= 60
+      int eb = ((s >> 40) & 3) == 0 ? (int)((s >> 52) % 2048) : (int)((s >> 52) % 121) - 60 + 1023;
+      unsigned long long bits = ((unsigned long long)eb << 52) | m | ((s >> 63) << 63);
       x[j] = __longlong_as_double((long long)bits);
     }
-    if ((s & 7) == 0) x[0] = 0.0;
+    if ((s & 7) == 0) x[0] = (s & 8) ? -0.0 : 0.0;
     double q = __ddiv_rn(x[0], x[1]);
-    double m = div_by(x[0], x[1], __ddiv_rn(1.0, x[1]));
-    if (__double_as_longlong(q) != __double_as_longlong(m)) nb++;
+    double y = __ddiv_rn(1.0, x[1]);
+    double ab = fabs(x[1]);
+    // div_by: divisors in [2^-100, 2^100] only (its precondition)
+    double m1 = (ab > 0x1p-100 && ab < 0x1p+100) ? div_by(x[0], x[1], y) : q;
+    // kt_axis form (positive divisor): range test of the divisor, straight-line quotient, IEEE redo
+    unsigned rare = !div_range_ok(ab);
+    double m2 = div_fast(x[0], ab, __ddiv_rn(1.0, ab), rare);
+    if (rare) m2 = x[0] / ab;
+    double q2 = __ddiv_rn(x[0], ab);
+    bool qn = q != q;  // NaN results: any NaN payload is acceptable
+    bool b1 = qn ? (m1 == m1) : (__double_as_longlong(q) != __double_as_longlong(m1));
+    bool b2 = (q2 != q2) ? (m2 == m2) : (__double_as_longlong(q2) != __double_as_longlong(m2));
+    double m3 = div_nz(x[0], x[1]);
+    bool b3 = qn ? (m3 == m3) : (__double_as_longlong(q) != __double_as_longlong(m3));
+    if (b1 || b2 || b3) {
+      nb++;
+      if (atomicCAS(bad + 7, 0ull, 1ull) == 0ull) {  // first mismatch: a, b, a/b, div_by, kt form
+        bad[1] = (unsigned long long)__double_as_longlong(x[0]);
+        bad[2] = (unsigned long long)__double_as_longlong(x[1]);
+        bad[3] = (unsigned long long)__double_as_longlong(q);
+        bad[4] = (unsigned long long)__double_as_longlong(m1);
+        bad[5] = (unsigned long long)__double_as_longlong(m2);
+      }
+    }
   }
   if (nb) atomicAdd(bad, nb);
 }
@@ -566,6 +594,7 @@ int omb_reconstruct(const double* prim, int m, int new_mode, int contact_on, dou
 int omb_fluxes(const double* lo, const double* hi, int n, double gamma, int new_mode, int override_center, double* fx,
                double* fy, double* fz, unsigned long long* amax_bits, void* stream) {
   if (int rc = lib_init()) return rc;
+  if (!div_range_ok(gamma - 1.0)) return set_err("omb_fluxes: gamma - 1 outside [2^-100, 2^100]");
   int total = 3 * (n + 1) * n * n;
   k_fluxes<<<(total + 127) / 128, 128, 0, (cudaStream_t)stream>>>(lo, hi, n, gamma, gamma - 1.0, new_mode,
                                                                     override_center, fx, fy, fz, amax_bits);
@@ -631,6 +660,7 @@ int omb_reflux_update(const OmbRefluxDesc* d, void* stream) {
 int omb_stage(const OmbStageDesc* d, void* stream) {
   if (int rc = lib_init()) return rc;
   if (d->ucur == d->unext) return set_err("omb_stage: unext must not alias ucur");
+  if (!div_range_ok(d->gm1)) return set_err("omb_stage: gamma - 1 outside [2^-100, 2^100]");
   static bool attr_set = false;
   if (!attr_set) {
     // 512 threads x 128 registers fills the register file; 256/384/576/640 were measured slower
@@ -718,30 +748,109 @@ int omb_selftest_div(unsigned long long seed, long long n, unsigned long long* b
 // host-side packing of the per-leaf padded arrays (the reference's SubGrid.u,
 // (6, m, m, m) C-contiguous) into / out of the [6][L][n^3] device layout;
 // multithreaded memcpy of n-element rows
-static void host_copy(const double* const* leaf_u, int L, int n, long long fstride, double* packed, bool to_packed) {
-  int m = n + 6;
-  long long n3 = (long long)n * n * n;
+// A small persistent pool for the host-side copies: run(f, nt) calls f(t) for
+// t = 0..nt-1, t = 0 on the caller's thread, and returns when all are done.
+// (Spawning 16 threads per transfer cost ~1 ms of the ~5 ms upload.)
+class HostPool {
+ public:
+  void run(const std::function<void(int)>& f, int nt) {
+    std::lock_guard<std::mutex> serial(run_mu_);  // one job at a time
+    ensure(nt - 1);
+    {
+      std::lock_guard<std::mutex> g(mu_);
+      job_ = &f;
+      njob_ = nt;
+      pending_ = nt - 1;
+      gen_++;
+    }
+    cv_.notify_all();
+    f(0);
+    std::unique_lock<std::mutex> g(mu_);
+    done_cv_.wait(g, [&] { return pending_ == 0; });
+    job_ = nullptr;
+  }
+
+ private:
+  void ensure(int n) {
+    while ((int)th_.size() < n) {
+      int id = (int)th_.size() + 1;
+      th_.emplace_back([this, id] { loop(id); });
+      th_.back().detach();
+    }
+  }
+  void loop(int id) {
+    unsigned long long seen = 0;
+    for (;;) {
+      const std::function<void(int)>* f;
+      {
+        std::unique_lock<std::mutex> g(mu_);
+        cv_.wait(g, [&] { return gen_ != seen; });
+        seen = gen_;
+        if (id >= njob_) continue;
+        f = job_;
+      }
+      (*f)(id);
+      std::lock_guard<std::mutex> g(mu_);
+      if (--pending_ == 0) done_cv_.notify_one();
+    }
+  }
+  std::mutex run_mu_, mu_;
+  std::condition_variable cv_, done_cv_;
+  std::vector<std::thread> th_;
+  const std::function<void(int)>* job_ = nullptr;
+  int njob_ = 0, pending_ = 0;
+  unsigned long long gen_ = 0;
+};
+static HostPool& host_pool() {
+  static HostPool* p = new HostPool();  // never destroyed: its detached threads outlive main
+  return *p;
+}
+
+static int host_workers(int L) {
   unsigned nt = std::thread::hardware_concurrency();
   if (nt == 0) nt = 1;
   if (nt > 16) nt = 16;
   if ((long long)nt > L) nt = L > 0 ? (unsigned)L : 1u;
-  auto work = [&](int lo, int hi) {
-    for (int i = lo; i < hi; i++) {
-      const double* u = leaf_u[i];
-      for (int v = 0; v < 6; v++)
-        for (int x = 0; x < n; x++)
-          for (int y = 0; y < n; y++) {
-            double* p = packed + (long long)v * fstride + (long long)i * n3 + ((long long)x * n + y) * n;
-            double* q = const_cast<double*>(u) + (((long long)v * m + x + 3) * m + y + 3) * m + 3;
-            if (to_packed) memcpy(p, q, sizeof(double) * n);
-            else memcpy(q, p, sizeof(double) * n);
-          }
-    }
-  };
-  std::vector<std::thread> th;
-  for (unsigned t = 1; t < nt; t++) th.emplace_back(work, (int)((long long)L * t / nt), (int)((long long)L * (t + 1) / nt));
-  work(0, (int)((long long)L / nt));
-  for (auto& x : th) x.join();
+  return (int)nt;
+}
+}  // extern "C"
+template <int NN>
+static void copy_leaf_n(const double* u, double* packed, int i, long long fstride, bool to_packed) {
+  constexpr int m = NN + 6;
+  constexpr long long n3 = (long long)NN * NN * NN;
+  for (int v = 0; v < 6; v++) {
+    double* P = packed + (long long)v * fstride + (long long)i * n3;
+    double* Q = const_cast<double*>(u) + (long long)v * m * m * m + (3 * m + 3) * m + 3;
+    for (int x = 0; x < NN; x++)
+      for (int y = 0; y < NN; y++) {
+        double* p = P + (x * NN + y) * NN;
+        double* q = Q + (x * m + y) * m;
+        if (to_packed) memcpy(p, q, sizeof(double) * NN);  // constant size: inlined vector moves
+        else memcpy(q, p, sizeof(double) * NN);
+      }
+  }
+}
+extern "C" {
+static void copy_leaf(const double* u, double* packed, int i, int n, long long fstride, bool to_packed) {
+  if (n == 8) return copy_leaf_n<8>(u, packed, i, fstride, to_packed);
+  int m = n + 6;
+  long long n3 = (long long)n * n * n;
+  for (int v = 0; v < 6; v++)
+    for (int x = 0; x < n; x++)
+      for (int y = 0; y < n; y++) {
+        double* p = packed + (long long)v * fstride + (long long)i * n3 + ((long long)x * n + y) * n;
+        double* q = const_cast<double*>(u) + (((long long)v * m + x + 3) * m + y + 3) * m + 3;
+        if (to_packed) memcpy(p, q, sizeof(double) * n);
+        else memcpy(q, p, sizeof(double) * n);
+      }
+}
+
+static void host_copy(const double* const* leaf_u, int L, int n, long long fstride, double* packed, bool to_packed) {
+  const int nt = host_workers(L);
+  host_pool().run([&](int t) {
+    for (int i = (int)((long long)L * t / nt); i < (int)((long long)L * (t + 1) / nt); i++)
+      copy_leaf(leaf_u[i], packed, i, n, fstride, to_packed);
+  }, nt);
 }
 
 int omb_host_pack(const double* const* leaf_u, int L, int n, long long fstride, double* out) {
@@ -751,6 +860,73 @@ int omb_host_pack(const double* const* leaf_u, int L, int n, long long fstride, 
 
 int omb_host_unpack(const double* in, int L, int n, long long fstride, double* const* leaf_u) {
   host_copy((const double* const*)leaf_u, L, n, fstride, const_cast<double*>(in), false);
+  return 0;
+}
+
+// Pipelined host <-> device transfer of the state of record (the leaves'
+// padded host arrays): the leaves are cut into chunks; worker threads pack
+// chunk c into the pinned staging buffer while the copy engine moves chunk
+// c-1 (upload), or unpack chunk c while chunk c+1 is still in flight
+// (download).  One 2D copy per chunk covers the 6 field planes.
+int omb_host_upload(const double* const* leaf_u, int L, int n, long long fstride, double* pinned, double* dev,
+                    int nchunks, void* stream) {
+  if (int rc = lib_init()) return rc;
+  if (L <= 0) return 0;
+  if (nchunks < 1) nchunks = 1;
+  if (nchunks > L) nchunks = L;
+  const int nt = host_workers(L);
+  const long long n3 = (long long)n * n * n;
+  std::vector<std::atomic<int>> done(nchunks);
+  for (auto& d : done) d.store(0);
+  auto lo_of = [&](int c) { return (int)((long long)L * c / nchunks); };
+  std::atomic<int> err(0);
+  std::function<void(int)> work = [&](int t) {
+    for (int c = 0; c < nchunks; c++) {
+      int lo = lo_of(c), hi = lo_of(c + 1);
+      int a = lo + (int)((long long)(hi - lo) * t / nt), b = lo + (int)((long long)(hi - lo) * (t + 1) / nt);
+      for (int i = a; i < b; i++) copy_leaf(leaf_u[i], pinned, i, n, fstride, true);
+      // the thread finishing chunk c last hands it to the copy engine
+      if (done[c].fetch_add(1, std::memory_order_acq_rel) == nt - 1) {
+        cudaError_t e = cudaMemcpy2DAsync(dev + lo * n3, fstride * 8, pinned + lo * n3, fstride * 8,
+                                          (size_t)(hi - lo) * n3 * 8, 6, cudaMemcpyHostToDevice, (cudaStream_t)stream);
+        if (e != cudaSuccess) err.store((int)e);
+      }
+    }
+  };
+  host_pool().run(work, nt);
+  CK((cudaError_t)err.load(), "omb_host_upload copy");
+  return 0;
+}
+
+int omb_host_download(const double* dev, double* pinned, int L, int n, long long fstride, double* const* leaf_u,
+                      int nchunks, void* stream) {
+  if (int rc = lib_init()) return rc;
+  if (L <= 0) return 0;
+  if (nchunks < 1) nchunks = 1;
+  if (nchunks > L) nchunks = L;
+  const int nt = host_workers(L);
+  const long long n3 = (long long)n * n * n;
+  auto lo_of = [&](int c) { return (int)((long long)L * c / nchunks); };
+  std::vector<cudaEvent_t> ev(nchunks);
+  for (int c = 0; c < nchunks; c++) {
+    CK(cudaEventCreateWithFlags(&ev[c], cudaEventDisableTiming), "omb_host_download event");
+    int lo = lo_of(c), hi = lo_of(c + 1);
+    CK(cudaMemcpy2DAsync(pinned + lo * n3, fstride * 8, dev + lo * n3, fstride * 8, (size_t)(hi - lo) * n3 * 8, 6,
+                         cudaMemcpyDeviceToHost, (cudaStream_t)stream), "omb_host_download copy");
+    CK(cudaEventRecord(ev[c], (cudaStream_t)stream), "omb_host_download record");
+  }
+  std::atomic<int> bad(0);
+  std::function<void(int)> work = [&](int t) {
+    for (int c = 0; c < nchunks; c++) {
+      if (cudaEventSynchronize(ev[c]) != cudaSuccess) { bad.store(1); return; }
+      int lo = lo_of(c), hi = lo_of(c + 1);
+      int a = lo + (int)((long long)(hi - lo) * t / nt), b = lo + (int)((long long)(hi - lo) * (t + 1) / nt);
+      for (int i = a; i < b; i++) copy_leaf(leaf_u[i], pinned, i, n, fstride, false);
+    }
+  };
+  host_pool().run(work, nt);
+  for (auto& e : ev) cudaEventDestroy(e);
+  if (bad.load()) return set_err("omb_host_download: copy failed");
   return 0;
 }
 

@@ -39,27 +39,47 @@ OMB_HD int ldz(int l) { return (int)((LDZ_BITS >> (2 * l)) & 3u) - 1; }
 
 // IEEE a/b that never takes CUDA's division slow path for a zero numerator
 // (CUDA routes 0/b through a called subroutine; zero momenta and zero
-// deviations are everywhere in the Sedov ambient).  For a == 0, a/b equals
-// a*(1/b) exactly for every b (finite, 0, inf, NaN), so the numerator is
-// replaced by 1 and the quotient rebuilt -- branch-free, bit-identical.
+// deviations are everywhere in the Sedov ambient).  For a == 0 the quotient
+// t = 2^-100/b is finite for every b != 0 (even subnormal) and a*t carries
+// 0/b's sign (t underflowing to +-0 for huge b keeps it); b = 0, inf, NaN
+// give 0*inf = NaN, +-0, NaN as IEEE does -- branch-free, bit-identical.
 OMB_HD double div_nz(double a, double b) {
   bool z = (a == 0.0);
-  double q = (z ? 1.0 : a) / b;
+  double q = (z ? 0x1p-100 : a) / b;
   return z ? a * q : q;
 }
 
 // IEEE a/b from a precomputed y = RN(1/b) (Markstein): q0 = a*y, then two
 // fma corrections q <- q + (a - b q) y.  q1 is within 1 ulp of a/b, so the
 // second correction returns the correctly rounded quotient (Markstein's
-// theorem; r = a - b q is exact by fma).  Zero, non-finite and extreme-range
-// quotients (where the theorem's no-underflow premise could fail) take the
-// IEEE division instead.  Used where one divisor serves several numerators.
+// theorem, given y normal, a normal quotient and an exact residual a - b q,
+// whose grid 2^(e_b + e_q - 104) must not fall below 2^-1074).  With the
+// divisor in [2^-100, 2^100] (checked once per divisor, or guaranteed by the
+// caller) those premises hold whenever |q1| is in (2^-860, 2^1000): then
+// |a| > 2^-960.  A zero numerator returns a*y, the signed zero (y finite).
+// Straight-line; anything else sets `rare` and the caller redoes the
+// quotient with IEEE division (kt_axis does that once for all six fields).
+// Checked bitwise against IEEE division on 2^30 random pairs covering every
+// exponent (omb_selftest_div, tests/test_gpu_parity.py).
+OMB_HD bool div_range_ok(double b) { return b > 0x1p-100 && b < 0x1p+100; }  // b > 0
+OMB_HD double div_fast(double a, double b, double y, unsigned& rare) {
+  double q0 = a * y;
+  double q1 = fma(fma(-b, q0, a), y, q0);
+  double q2 = fma(fma(-b, q1, a), y, q1);
+  bool zero = (a == 0.0);
+  double m = fabs(q1);
+  rare |= (unsigned)!(zero || (m > 0x1p-860 && m < 0x1p+1000));
+  return zero ? q0 : q2;
+}
+// single quotient by a divisor in [2^-100, 2^100] (caller's guarantee: the
+// EOS's gamma-1 -- checked on the host -- and the Simpson weight 36), with
+// its own rarely taken IEEE fallback
 OMB_HD double div_by(double a, double b, double y) {
   double q0 = a * y;
   double q1 = fma(fma(-b, q0, a), y, q0);
   double q2 = fma(fma(-b, q1, a), y, q1);
   double m = fabs(q1);
-  if (!(m > 0x1p-1000 && m < 0x1p+1000)) q2 = (a == 0.0) ? a * y : a / b;
+  if (!(m > 0x1p-860 && m < 0x1p+1000)) q2 = (a == 0.0) ? q0 : a / b;
   return q2;
 }
 
@@ -189,6 +209,10 @@ OMB_HD double kt_axis(const KtState& P, const KtState& Q, int axis, bool flip, d
   double cQ = flip ? ap : -am;
   double sg = flip ? -apam : apam;
   bool ok = denom > 0.0;
+  // the six quotients straight-line (independent chains), one rare-case
+  // test for all of them (div_fast)
+  double num[NF];
+  unsigned rare = !div_range_ok(denom);
 #pragma unroll
   for (int v = 0; v < NF; v++) {
     double fP = P.u[v] * vnP, fQ = Q.u[v] * vnQ;
@@ -201,8 +225,13 @@ OMB_HD double kt_axis(const KtState& P, const KtState& Q, int axis, bool flip, d
       fP = fP + P.p * vnP;
       fQ = fQ + Q.p * vnQ;
     }
-    double num = (cP * fP + cQ * fQ) + sg * (Q.u[v] - P.u[v]);
-    out[v] = ok ? div_by(num, denom, rden) : (flip ? fQ : fP);
+    num[v] = (cP * fP + cQ * fQ) + sg * (Q.u[v] - P.u[v]);
+    double q = div_fast(num[v], denom, rden, rare);
+    out[v] = ok ? q : (flip ? fQ : fP);
+  }
+  if (ok && rare) {
+#pragma unroll
+    for (int v = 0; v < NF; v++) out[v] = num[v] / denom;
   }
   return dmax(ap, -am);
 }

@@ -17,8 +17,8 @@
 //       (_core.pyx:310-346) and into boundary point values for y/z faces
 //   P3/P4  in-plane lines (1, 2, 7, 8): lo/hi and their fluxes
 //   P5  finish the y/z faces of plane X-1, start those of plane X
-//   P6  conservative update of plane X-1 + sources + dual-energy + floors
-//       (step.py:243-288)
+//   P6  conservative update of plane X-2 + sources + dual-energy + floors
+//       (step.py:243-288), on the last 64 threads during the last P1 group
 //
 // lo/hi and point fluxes never leave shared memory.  Every phase is a loop
 // over independent items separated by barriers; values a thread carries
@@ -634,13 +634,6 @@ struct Stage {
   }
 
   // ---- P6: update the cells of plane X-1 ---------------------------------
-  // run the update on threads [off, off+64) when the block is large enough,
-  // so it overlaps a phase that only occupies the first `off` threads
-  OMB_HD void update_plane_offset(int tid, int nthr, int off) {
-    int base = nthr >= off + NFACEX ? off : 0;
-    update_plane(tid - base, nthr);
-  }
-
   OMB_HD void update_plane(int tid, int nthr) {
     int Xc = X - 1;
     int r = (Xc - 3) >> 3, lx = (Xc - 3) & 7;
@@ -682,6 +675,7 @@ struct Stage {
       for (int v = 0; v < NF; v++) A.unext[v * A.fstride + cell] = out[v];
     }
   }
+
 };
 
 // ---------------------------------------------------------------------------

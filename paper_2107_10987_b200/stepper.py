@@ -107,18 +107,38 @@ class B200HydroStepper:
         self.upload()
 
     # -- host <-> device -------------------------------------------------------------
+    TRANSFER_CHUNKS = 8
+
     def upload(self):
-        """Copy the host leaves' interiors into the device state."""
+        """Copy the host leaves' interiors into the device state (pipelined:
+        host threads pack chunk c while chunk c-1 is on the copy engine)."""
         b = self.batch
-        host = self._pinned.numpy().reshape(6, b.L + b.nvirtual, 8, 8, 8)
-        b.pack(out=host, lib=self.lib)
-        self._buf[self._state].copy_(self._pinned, non_blocking=True)
+        if getattr(self, "_up_ev", None) is not None:
+            self._up_ev.synchronize()  # the previous upload's copies still read the pinned buffer
+        self._up_ev = torch.cuda.Event()
+        ptrs = b._leaf_ptrs(b.L)
+        if ptrs is not None:
+            _lib.check(self.lib.omb_host_upload(ptrs.ctypes.data, b.L, 8, b.fstride, ptr(self._pinned),
+                                                ptr(self._buf[self._state]), self.TRANSFER_CHUNKS,
+                                                stream_handle(None)), "omb_host_upload")
+        else:
+            host = self._pinned.numpy().reshape(6, b.L + b.nvirtual, 8, 8, 8)
+            b.pack(out=host)
+            self._buf[self._state].copy_(self._pinned, non_blocking=True)
+        self._up_ev.record()
 
     def download(self):
-        """Copy the device state back into the host leaves."""
+        """Copy the device state back into the host leaves (the owned ones;
+        pipelined: chunk c is unpacked while chunk c+1 is in flight)."""
         b = self.batch
+        ptrs = b._leaf_ptrs(b.ncompute)
+        if ptrs is not None:
+            _lib.check(self.lib.omb_host_download(ptr(self._buf[self._state]), ptr(self._pinned), b.ncompute, 8,
+                                                  b.fstride, ptrs.ctypes.data, self.TRANSFER_CHUNKS,
+                                                  stream_handle(None)), "omb_host_download")
+            return
         self._pinned.copy_(self._buf[self._state])
-        b.unpack(self._pinned.numpy().reshape(6, b.L + b.nvirtual, 8, 8, 8), lib=self.lib)
+        b.unpack(self._pinned.numpy().reshape(6, b.L + b.nvirtual, 8, 8, 8))
 
     def state_tensor(self):
         return self._buf[self._state]

@@ -14,6 +14,7 @@
 using namespace omb;
 
 extern "C" int emu_stage(const OmbStageDesc* d, int nthr) {
+  if (nthr < 2 * NFACEX) return -1;  // the phase layout needs >= 128 threads
   StageArgs A;
   A.ucur = d->ucur; A.u0 = d->u0; A.unext = d->unext; A.grav = d->grav; A.fstride = d->fstride;
   A.info = (const LeafInfo*)d->info; A.run_off = d->run_off; A.run_leaf = d->run_leaf; A.dt = d->dt;
@@ -34,22 +35,26 @@ extern "C" int emu_stage(const OmbStageDesc* d, int nthr) {
     }
     int R = st[0].R;
 #define ALL(stmt) for (int t = 0; t < nthr; t++) { Stage& s = st[t]; (void)s; stmt; }
+    // the phase sequence of k_stage (omb_kernels.cu), one ALL() per barrier interval
     for (int X = 0; X < 4; X++) ALL(s.prefetch_plane(X, t, nthr, Smem::RAW + X * NF * PL));
     ALL(s.prefetch_plane(4, t, nthr));
     for (int X = 0; X < 4; X++) ALL(s.convert_plane(X, t, nthr, Smem::RAW + X * NF * PL));
+    const int ngroups = A.new_mode ? 2 : 1;
     for (int X = 2; X < 8 * R + 4; X++) {
       ALL(s.set_plane(X));
       ALL(if (X + 2 < 8 * R + 6) s.convert_plane(X + 2, t, nthr));
-      ALL(if (X + 3 < 8 * R + 6) s.prefetch_plane(X + 3, t, nthr);
-          s.boundary_lines(0, t, nthr, h[t]));
-      ALL(s.store_hi(h[t]); if (X >= 3) s.combine_A(t, nthr));
-      if (A.new_mode) {
-        ALL(s.boundary_lines(1, t, nthr, h[t]));
-        ALL(s.store_hi(h[t]); if (X >= 3 && A.quad) s.combine_B(t, nthr));
+      ALL(if (X + 3 < 8 * R + 6) s.prefetch_plane(X + 3, t, nthr));
+      const bool p6 = X >= 3 && st[0].interior(X - 2);
+      for (int g = 0; g < ngroups; g++) {
+        ALL(s.boundary_lines(g, t, nthr, h[t]);
+            if (g == ngroups - 1 && p6 && t >= nthr - NFACEX) {
+              s.set_plane(X - 1); s.update_plane(t - (nthr - NFACEX), NFACEX); s.set_plane(X);
+            });
+        ALL(s.store_hi(h[t]);
+            if (X >= 3) { if (g == 0) s.combine_A(t, nthr); else if (A.quad) s.combine_B(t, nthr); });
       }
       ALL(s.inplane_lines(t, nthr));
-      ALL(if (s.interior(X)) s.inplane_fluxes(t, nthr);
-          if (X >= 3 && s.interior(X - 2)) { s.set_plane(X - 1); s.update_plane_offset(t, nthr, NYF + NZF + 2 * NCOR); s.set_plane(X); });
+      ALL(if (s.interior(X)) s.inplane_fluxes(t, nthr));
       ALL(if (s.interior(X - 1)) s.prefetch_update(X - 1, t, nthr);
           if (X >= 3) s.faces_yz(t, nthr));
     }
