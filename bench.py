@@ -310,6 +310,15 @@ def gpu_arm(args, rank, world):
     amax = acc_h[:, :3].numpy().view(np.float64)
     ratio = dt_h.numpy() * amax / st.dx_min
     aborted = bool(np.any(ratio > 1.0))
+    info = {"nglobal": st.nglobal, "nruns": st.batch.nruns, "L": st.batch.L, "ncompute": st.batch.ncompute,
+            "launches": st.native_launches_per_step()}
+    # free the host tree and device buffers before the e2e / non-flat trees (c3 at 8 ranks:
+    # 4.3 GB of host leaves per rank per tree)
+    del st, tree, part
+    import gc
+
+    gc.collect()
+    torch.cuda.empty_cache()
 
     # end-to-end through the public drop-in API (host state of record, H2D + D2H every step)
     e2e = None
@@ -337,10 +346,14 @@ def gpu_arm(args, rank, world):
             t = torch.tensor([wall], dtype=torch.float64, device="cuda")
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             wall = float(t.item())
-        nbytes = 6 * st2.batch.L * 512 * 8
+        up = 6 * st2.batch.L * 512 * 8  # every batch leaf's interior (owned + halo)
+        down = 6 * st2.batch.ncompute * 512 * 8  # the owned leaves back into the host tree
         e2e = {"value": cells * args.e2e_steps / wall, "unit": UNIT,
-               "h2d_bytes_per_step": nbytes, "d2h_bytes_per_step": nbytes + 2 * 8 + 4 + 6 * 8,
+               "h2d_bytes_per_step": up, "d2h_bytes_per_step": down + 2 * 8 + 4 + 6 * 8,
                "steps": args.e2e_steps, "api": "B200HydroStepper.cfl_dt + rk3_step (host_sync=True)"}
+        del st2, t2, p2
+        gc.collect()
+        torch.cuda.empty_cache()
 
     # the same step on a NON-FLAT state (every cell off the limiter's flat shortcut), same tree
     nontrivial = None
@@ -391,12 +404,12 @@ def gpu_arm(args, rank, world):
         "ms_per_step": ms / K, "higher_is_better": True, "scaling": "weak" if world == 1 else "strong",
         "vs_baseline": None,
         "dtype": "f64", "data": "synthetic (init_sedov Sedov-Taylor, no RNG)",
-        "config": {"workload": f"{workload_name(level, st.nglobal)}: {st.nglobal} sub-grids of 8^3 = {cells} cells, "
+        "config": {"workload": f"{workload_name(level, info['nglobal'])}: {info['nglobal']} sub-grids of 8^3 = {cells} cells, "
                                "reflecting, cfl 0.4, scheme new",
                    "step": "cfl_dt + 3 fused RK stages, dt on device",
                    "l2": "working set (3 x 6 x cells x 8 B = %.0f MB) > 126 MB L2; no flush" % (3 * 48 * cells / 1e6),
-                   "runs": st.batch.nruns, "max_run": args.max_run, "parallelism": f"leaf-partitioned x{world}",
-                   "halo_leaves_per_rank": int(st.batch.L - st.batch.ncompute)},
+                   "runs": info["nruns"], "max_run": args.max_run, "parallelism": f"leaf-partitioned x{world}",
+                   "halo_leaves_per_rank": int(info["L"] - info["ncompute"])},
         "roofline": {"bound": "fp64", "achieved": achieved_tf, "peak": peak64, "unit": "TFLOP/s",
                      "frac": achieved_tf / peak64, "traffic": traffic,
                      "kernel": "k_stage (fused RK stage)", "stage_ms": mean_stage,
@@ -407,11 +420,11 @@ def gpu_arm(args, rank, world):
         "clocks": clocks,
         "e2e": e2e,
         "nontrivial_state": nontrivial,
-        "gpu_launches": K * st.native_launches_per_step(),
+        "gpu_launches": K * info["launches"],
         "cfl_abort_in_timed_steps": aborted,
     }
     if not args.no_cpu_baseline and world == 1:
-        v, nthr, sample, _ = cpu_run(level, min(args.cpu_leaves, st.batch.L), 1, 0)
+        v, nthr, sample, _ = cpu_run(level, min(args.cpu_leaves, info["L"]), 1, 0)
         line["cpu_baseline"] = {"value": v, "unit": UNIT, "cores": nthr, "kind": "port", "sample": sample}
     emit(line)
 
