@@ -195,7 +195,17 @@ OMB_HD void kt_state(const double* w, double gamma, double gm1, double inv_gm1, 
 //     = cP*fP + cQ*fQ + s*(uQ-uP),  (cP,cQ,s) = (ap,-am,ap*am) or (-am,ap,-(ap*am))
 // which is bit-identical (IEEE + commutes, x-y = x+(-y), products negate
 // exactly).  Returns the signal speed max(a+, -a-).
-OMB_HD double kt_axis(const KtState& P, const KtState& Q, int axis, bool flip, double* out) {
+// physical flux of field v through an `axis` face for state S (normal velocity vn)
+OMB_HD double kt_phys(const KtState& S, double vn, int axis, int v) {
+  double f = S.u[v] * vn;
+  if (v == 1 || v == 2 || v == 3) f = (v == 1 + axis) ? f + S.p : f;  // normal momentum picks up p
+  if (v == 4) f = f + S.p * vn;
+  return f;
+}
+// Results go to out[v * stride] as they are computed (no array kept live);
+// the six quotients run straight-line (independent chains) with one
+// rare-case test for all of them (div_fast), whose redo recomputes.
+OMB_HD double kt_axis(const KtState& P, const KtState& Q, int axis, bool flip, double* out, int stride = 1) {
   double vnP = axis == 0 ? P.v[0] : (axis == 1 ? P.v[1] : P.v[2]);
   double vnQ = axis == 0 ? Q.v[0] : (axis == 1 ? Q.v[1] : Q.v[2]);
   double eP = vnP + P.c, eQ = vnQ + Q.c;
@@ -209,29 +219,20 @@ OMB_HD double kt_axis(const KtState& P, const KtState& Q, int axis, bool flip, d
   double cQ = flip ? ap : -am;
   double sg = flip ? -apam : apam;
   bool ok = denom > 0.0;
-  // the six quotients straight-line (independent chains), one rare-case
-  // test for all of them (div_fast)
-  double num[NF];
   unsigned rare = !div_range_ok(denom);
 #pragma unroll
   for (int v = 0; v < NF; v++) {
-    double fP = P.u[v] * vnP, fQ = Q.u[v] * vnQ;
-    if (v == 1 || v == 2 || v == 3) {  // normal momentum picks up the pressure
-      bool nrm = (v == 1 + axis);
-      fP = nrm ? fP + P.p : fP;
-      fQ = nrm ? fQ + Q.p : fQ;
-    }
-    if (v == 4) {
-      fP = fP + P.p * vnP;
-      fQ = fQ + Q.p * vnQ;
-    }
-    num[v] = (cP * fP + cQ * fQ) + sg * (Q.u[v] - P.u[v]);
-    double q = div_fast(num[v], denom, rden, rare);
-    out[v] = ok ? q : (flip ? fQ : fP);
+    double fP = kt_phys(P, vnP, axis, v), fQ = kt_phys(Q, vnQ, axis, v);
+    double num = (cP * fP + cQ * fQ) + sg * (Q.u[v] - P.u[v]);
+    double q = div_fast(num, denom, rden, rare);
+    out[v * stride] = ok ? q : (flip ? fQ : fP);
   }
   if (ok && rare) {
 #pragma unroll
-    for (int v = 0; v < NF; v++) out[v] = num[v] / denom;
+    for (int v = 0; v < NF; v++) {
+      double fP = kt_phys(P, vnP, axis, v), fQ = kt_phys(Q, vnQ, axis, v);
+      out[v * stride] = ((cP * fP + cQ * fQ) + sg * (Q.u[v] - P.u[v])) / denom;
+    }
   }
   return dmax(ap, -am);
 }

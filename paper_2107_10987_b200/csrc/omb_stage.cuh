@@ -400,11 +400,8 @@ struct Stage {
     // the canonical line direction runs against the face normal: the stored
     // lo/hi states swap roles (_core.pyx:299-306)
     bool flip = d < 0;
-    double f[NF];
-    double sp = kt_axis(sP, sQ, axis, flip, f);
+    double sp = kt_axis(sP, sQ, axis, flip, dst, stride);
     if (sp > amax) amax = sp;
-#pragma unroll
-    for (int v = 0; v < NF; v++) dst[v * stride] = f[v];
   }
 
   // ---- P1: boundary lines (d.x = 1) of group g on plane X ----------------
