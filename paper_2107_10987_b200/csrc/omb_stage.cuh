@@ -551,8 +551,10 @@ struct Stage {
   }
 
   // ---- P4: in-plane fluxes (y/z face centres, y/z edge points) -----------
+  // The two axes of an edge point go to two threads (each recomputes the two
+  // states): 468 single-axis items, one round on 512 threads.
   OMB_HD void inplane_fluxes(int tid, int nthr) {
-    int ntot = NYF + NZF + (A.quad ? 2 * NCOR : 0);
+    int ntot = NYF + NZF + (A.quad ? 4 * NCOR : 0);
     for (int it = tid; it < ntot; it += nthr) {
       int ip, py, pz, qy, qz, l, ax0, nax, stride;
       double* dst;
@@ -563,13 +565,14 @@ struct Stage {
         int s2 = it - NYF;
         ip = 1; l = 2; py = 3 + s2 / 9; pz = 2 + s2 % 9; qy = py; qz = pz + 1;
         ax0 = 2; nax = 1; dst = S + Smem::IPCZ + s2; stride = NZF;
-      } else {  // edge point (a+1/2, b+1/2) of lines 7 / 8, axes y and z
-        int j = it - NYF - NZF, li = j / NCOR, c = j % NCOR, a = 2 + c / 9, b = 2 + c % 9;
+      } else {  // edge point (a+1/2, b+1/2) of lines 7 / 8, axis y (k = 0) or z (k = 1)
+        int j = it - NYF - NZF, k = j / (2 * NCOR), jj = j % (2 * NCOR);
+        int li = jj / NCOR, c = jj % NCOR, a = 2 + c / 9, b = 2 + c % 9;
         l = li == 0 ? 7 : 8;
         ip = li + 2;
         py = a; pz = li == 0 ? b : b + 1;
         qy = py + 1; qz = pz + ldz(l);
-        ax0 = 1; nax = 2; dst = S + Smem::IPR + ((li * 2) * NF) * NCOR + c; stride = NCOR;
+        ax0 = 1 + k; nax = 1; dst = S + Smem::IPR + ((li * 2 + k) * NF) * NCOR + c; stride = NCOR;
       }
       KtState sP, sQ;
       lhi_state(ip, 1, py, pz, sP);
