@@ -589,10 +589,12 @@ struct Stage {
   OMB_HD void faces_yz(int tid, int nthr) {
     bool fin = interior(X - 1), start = interior(X);
     bool q = A.quad;
-    for (int it = tid; it < NF * (NYF + NZF); it += nthr) {
-      int zf = it >= NF * NYF;
-      int j = zf ? it - NF * NYF : it;
-      int v = j / NYF, s = j % NYF;  // NYF == NZF
+    // one item = the y face and the z face of slot (v, s): 432 items, one
+    // round on 512 threads, two independent chains per thread
+    for (int it = tid; it < NF * NYF; it += nthr)
+#pragma unroll
+    for (int zf = 0; zf < 2; zf++) {
+      int v = it / NYF, s = it % NYF;  // NYF == NZF
       int y, z;
       if (!zf) { y = 2 + s / 8; z = 3 + s % 8; }
       else { y = 3 + s / 9; z = 2 + s % 9; }
