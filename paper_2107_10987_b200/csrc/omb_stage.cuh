@@ -473,44 +473,46 @@ struct Stage {
   }
 
   // ---- P2A: x-face centre + edges, boundary edge points for y/z faces -----
+  // One item per (field, slot): the x face (slots < 64) and the y/z boundary
+  // edge points of that slot -- 432 items, one round, independent chains.
   OMB_HD void combine_A(int tid, int nthr) {
     double* FXc = S + Smem::FX + (X % 3) * NF * NFACEX;
-    int nx = NF * NFACEX;
-    int ntot = A.quad ? nx + NF * (NYF + NZF) : nx;
+    int ntot = A.quad ? NF * NYF : NF * NFACEX;
     for (int it = tid; it < ntot; it += nthr) {
-      if (it < nx) {
-        int v = it / NFACEX, f = it % NFACEX, y = 3 + f / 8, z = 3 + f % 8;
+      int v = A.quad ? it / NYF : it / NFACEX, f = A.quad ? it % NYF : it % NFACEX;
+      if (f < NFACEX) {
+        int y = 3 + f / 8, z = 3 + f % 8;
         double C = rawA(0, 0, v, y, z);
-        if (!A.quad) {
-          FXc[v * NFACEX + f] = C;
-          if (double* ex = export_slot()) ex[FXO + (v * 9 + (X - 3)) * 64 + f] = C;
-          continue;
-        }
-        double e0 = edge_acc(rawA(5, 0, v, y, z - 1), rawA(6, 0, v, y, z));
-        double e1 = edge_acc(rawA(5, 0, v, y, z), rawA(6, 0, v, y, z + 1));
-        double e2 = edge_acc(rawA(3, 0, v, y - 1, z), rawA(4, 0, v, y, z));
-        double e3 = edge_acc(rawA(3, 0, v, y, z), rawA(4, 0, v, y + 1, z));
-        double edev = (pdev_edge(e0, C) + pdev_edge(e1, C)) + (pdev_edge(e2, C) + pdev_edge(e3, C));
         FXc[v * NFACEX + f] = C;
-        S[Smem::EDEV + v * NFACEX + f] = edev;
-      } else if (it < nx + NF * NYF) {
-        int j = it - nx, v = j / NYF, s = j % NYF, y = 2 + s / 8, z = 3 + s % 8;
-        S[Smem::BYE + v * NYF + s] = edge_acc(rawA(3, 1, v, y, z), rawA(4, 1, v, y + 1, z));
-      } else {
-        int j = it - nx - NF * NYF, v = j / NZF, s = j % NZF, y = 3 + s / 9, z = 2 + s % 9;
-        S[Smem::BZE + v * NZF + s] = edge_acc(rawA(5, 2, v, y, z), rawA(6, 2, v, y, z + 1));
+        if (!A.quad) {
+          if (double* ex = export_slot()) ex[FXO + (v * 9 + (X - 3)) * 64 + f] = C;
+        } else {
+          double e0 = edge_acc(rawA(5, 0, v, y, z - 1), rawA(6, 0, v, y, z));
+          double e1 = edge_acc(rawA(5, 0, v, y, z), rawA(6, 0, v, y, z + 1));
+          double e2 = edge_acc(rawA(3, 0, v, y - 1, z), rawA(4, 0, v, y, z));
+          double e3 = edge_acc(rawA(3, 0, v, y, z), rawA(4, 0, v, y + 1, z));
+          S[Smem::EDEV + v * NFACEX + f] = (pdev_edge(e0, C) + pdev_edge(e1, C)) + (pdev_edge(e2, C) + pdev_edge(e3, C));
+        }
+      }
+      if (A.quad) {  // f < NYF == NZF
+        int y = 2 + f / 8, z = 3 + f % 8;
+        S[Smem::BYE + v * NYF + f] = edge_acc(rawA(3, 1, v, y, z), rawA(4, 1, v, y + 1, z));
+        y = 3 + f / 9;
+        z = 2 + f % 9;
+        S[Smem::BZE + v * NZF + f] = edge_acc(rawA(5, 2, v, y, z), rawA(6, 2, v, y, z + 1));
       }
     }
   }
 
   // ---- P2B: x-face vertices -> final x flux; vertex points for y/z -------
+  // One item per (field, corner): both y/z vertex points of the corner and
+  // (corners < 64) the final x face -- 486 items, one round.
   OMB_HD void combine_B(int tid, int nthr) {
     double* FXc = S + Smem::FX + (X % 3) * NF * NFACEX;
-    int nx = NF * NFACEX;
-    int ntot = nx + 2 * NF * NCOR;
-    for (int it = tid; it < ntot; it += nthr) {
-      if (it < nx) {
-        int v = it / NFACEX, f = it % NFACEX, y = 3 + f / 8, z = 3 + f % 8;
+    for (int it = tid; it < NF * NCOR; it += nthr) {
+      int v = it / NCOR, c = it % NCOR;
+      if (c < NFACEX) {
+        int f = c, y = 3 + f / 8, z = 3 + f % 8;
         double C = FXc[v * NFACEX + f];
         double edev = S[Smem::EDEV + v * NFACEX + f];
         double vdev = (pdev_vert(vertex(0, v, y - 1, z - 1), C) + pdev_vert(vertex(0, v, y - 1, z), C)) +
@@ -518,10 +520,10 @@ struct Stage {
         double Fv = face_final(C, edev, vdev);
         FXc[v * NFACEX + f] = Fv;
         if (double* ex = export_slot()) ex[FXO + (v * 9 + (X - 3)) * 64 + f] = Fv;
-      } else {
-        int j = it - nx, ax = j / (NF * NCOR), rem = j % (NF * NCOR), v = rem / NCOR, c = rem % NCOR;
-        S[Smem::BV + (ax * NF + v) * NCOR + c] = vertex(1 + ax, v, 2 + c / 9, 2 + c % 9);
       }
+#pragma unroll
+      for (int ax = 0; ax < 2; ax++)
+        S[Smem::BV + (ax * NF + v) * NCOR + c] = vertex(1 + ax, v, 2 + c / 9, 2 + c % 9);
     }
   }
 
