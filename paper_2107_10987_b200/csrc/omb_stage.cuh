@@ -445,8 +445,9 @@ struct Stage {
       // axes served by this line: x always; y for lines 3,4; z for 5,6; all for 9..12
       int ax_second = (l == 3 || l == 4) ? 1 : 2;
       int nax = l == 0 ? 1 : (l >= 9 ? 3 : 2);
-#pragma unroll 1
-      for (int q = 0; q < nax; q++) {
+#pragma unroll
+      for (int q = 0; q < 3; q++) {
+        if (q >= nax) break;
         int ax = q == 0 ? 0 : (l >= 9 ? q : ax_second);
         double* dst = g == 0 ? S + Smem::RAWA + (chA(l, ax) * NF) * NP + pp : S + Smem::RAWB + (chB(l, ax) * NF) * NP + pp;
         kt_into(sP, sQ, l, ax, dst, NP);
