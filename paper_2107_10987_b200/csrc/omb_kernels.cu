@@ -252,6 +252,24 @@ __device__ __forceinline__ void block_reduce(double amax, long long fb, unsigned
   }
 }
 
+#ifdef OMB_PHASE_PROF
+// profiling build only (profiles/phase_prof.py): thread 0 of every CTA adds
+// the cycles between consecutive barrier exits to its phase's counter
+__device__ unsigned long long g_phase_cycles[16];
+#define PH(k)                                                        \
+  do {                                                               \
+    if (tid == 0) {                                                  \
+      long long _t = clock64();                                      \
+      atomicAdd(&g_phase_cycles[k], (unsigned long long)(_t - _t0)); \
+      _t0 = _t;                                                      \
+    }                                                                \
+  } while (0)
+#else
+#define PH(k) \
+  do {        \
+  } while (0)
+#endif
+
 template <int NT>
 __global__ void __launch_bounds__(NT, 1) k_stage(StageArgs A) {
   static_assert(NT >= 2 * NFACEX, "P6 runs on the last 64 threads of the last P1 group");
@@ -268,6 +286,9 @@ __global__ void __launch_bounds__(NT, 1) k_stage(StageArgs A) {
   st.fb = 0;
   Hold h;
   const int R = st.R;
+#ifdef OMB_PHASE_PROF
+  long long _t0 = clock64();
+#endif
   // prologue: planes 0..3 staged in the (still unused) RAW union and plane 4
   // in SG0, all loads in flight at once; then planes 0..3 converted
   for (int X = 0; X < 4; X++) st.prefetch_plane(X, tid, nthr, Smem::RAW + X * NF * PL);
@@ -277,11 +298,13 @@ __global__ void __launch_bounds__(NT, 1) k_stage(StageArgs A) {
   __syncthreads();
   for (int X = 0; X < 4; X++) st.convert_plane(X, tid, nthr, Smem::RAW + X * NF * PL);
   __syncthreads();
+  PH(0);
   const int ngroups = A.new_mode ? 2 : 1;
   for (int X = 2; X < 8 * R + 4; X++) {
     st.set_plane(X);
     if (X + 2 < 8 * R + 6) st.convert_plane(X + 2, tid, nthr);  // P0
     __syncthreads();
+    PH(1);
     if (X + 3 < 8 * R + 6) st.prefetch_plane(X + 3, tid, nthr);  // stage next P0 (cp.async)
     async_commit();
     // P6 = the update of plane X-2 (its x fluxes sit in the 3-slot FX ring,
@@ -297,26 +320,32 @@ __global__ void __launch_bounds__(NT, 1) k_stage(StageArgs A) {
         st.set_plane(X);
       }
       __syncthreads();
+      PH(2 + 2 * g);
       st.store_hi(h);
       if (X >= 3) {  // P2
         if (g == 0) st.combine_A(tid, nthr);
         else if (A.quad) st.combine_B(tid, nthr);
       }
       __syncthreads();
+      PH(3 + 2 * g);
     }
     st.inplane_lines(tid, nthr);  // P3
     __syncthreads();
-    if (st.interior(X)) st.inplane_fluxes(tid, nthr);  // P4 (<= 306 items)
+    PH(6);
+    if (st.interior(X)) st.inplane_fluxes(tid, nthr);  // P4 (<= 468 items)
     __syncthreads();
+    PH(7);
     if (st.interior(X - 1)) st.prefetch_update(X - 1, tid, nthr);  // stage next P6
     async_commit();
     if (X >= 3) st.faces_yz(tid, nthr);  // P5
     async_wait_all();
     __syncthreads();
+    PH(8);
   }
   // P6 of the last plane
   st.set_plane(8 * R + 3);
   st.update_plane(tid, nthr);
+  PH(9);
   block_reduce(st.amax, st.fb, A.amax_bits, A.fallback);
 }
 
@@ -570,6 +599,16 @@ extern "C" {
 int omb_abi_version(void) { return OMB_ABI_VERSION; }
 const char* omb_last_error(void) { return g_err.c_str(); }
 int omb_stage_smem_bytes(void) { return Smem::BYTES; }
+#ifdef OMB_PHASE_PROF
+int omb_phase_prof(unsigned long long* out, int reset) {  // profiling build only
+  cudaMemcpyFromSymbol(out, g_phase_cycles, sizeof(unsigned long long) * 16);
+  if (reset) {
+    unsigned long long z[16] = {0};
+    cudaMemcpyToSymbol(g_phase_cycles, z, sizeof(z));
+  }
+  return 0;
+}
+#endif
 
 int omb_primitives(const double* u, int m, double gamma, double eta, double* prim, void* stream) {
   if (int rc = lib_init()) return rc;
