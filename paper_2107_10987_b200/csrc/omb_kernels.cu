@@ -326,6 +326,9 @@ __global__ void __launch_bounds__(NT, 1) k_stage(StageArgs A) {
         if (g == 0) st.combine_A(tid, nthr);
         else if (A.quad) st.combine_B(tid, nthr);
       }
+      // the update inputs staged in the previous plane's P5 (SG6) must have
+      // landed before P1B's update (this plane's SG0 group may still fly)
+      if (g == 0 && ngroups == 2) async_wait_prev();
       __syncthreads();
       PH(3 + 2 * g);
     }
@@ -338,11 +341,15 @@ __global__ void __launch_bounds__(NT, 1) k_stage(StageArgs A) {
     if (st.interior(X - 1)) st.prefetch_update(X - 1, tid, nthr);  // stage next P6
     async_commit();
     if (X >= 3) st.faces_yz(tid, nthr);  // P5
-    async_wait_all();
+    // the next P0 needs SG0 only; the SG6 group just issued has until P2A
+    if (ngroups == 2) async_wait_prev();
+    else async_wait_all();
     __syncthreads();
     PH(8);
   }
   // P6 of the last plane
+  async_wait_all();
+  __syncthreads();
   st.set_plane(8 * R + 3);
   st.update_plane(tid, nthr);
   PH(9);

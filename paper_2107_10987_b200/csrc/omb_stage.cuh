@@ -158,6 +158,12 @@ OMB_HD void async_wait_all() {
   asm volatile("cp.async.wait_all;\n" ::: "memory");
 #endif
 }
+// wait until at most the most recently committed group is still in flight
+OMB_HD void async_wait_prev() {
+#ifdef __CUDA_ARCH__
+  asm volatile("cp.async.wait_group 1;\n" ::: "memory");
+#endif
+}
 
 struct LeafInfo {
   int nbr[27];    // batch index of the same-level (or virtual AMR) neighbour per offset, -1 none
