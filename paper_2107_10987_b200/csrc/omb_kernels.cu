@@ -284,6 +284,9 @@ __global__ void __launch_bounds__(NT, 1) k_stage(StageArgs A) {
   st.leaves = A.run_leaf + off;
   st.amax = 0.0;
   st.fb = 0;
+  st.bind_run_info();
+  st.stage_run_info(tid, nthr);
+  __syncthreads();
   Hold h;
   const int R = st.R;
 #ifdef OMB_PHASE_PROF

@@ -131,7 +131,8 @@ struct Smem {
   static constexpr int FYZ = FP + 2 * 4 * NF * NYF;  // [2][6][72]
   static constexpr int SG0 = FYZ + 2 * NF * NYF;    // [6][196] staged conserved plane (next P0)
   static constexpr int SG6 = SG0 + NF * PL;          // [16][64] staged cur(6) u0(6) grav(4) (next P6)
-  static constexpr int TOTAL = SG6 + 16 * NFACEX;
+  static constexpr int LINFO = SG6 + 16 * NFACEX;    // the run's LeafInfo copies [4] (+ leaf ids [4])
+  static constexpr int TOTAL = LINFO + 4 * 20 + 2;
   static constexpr int BYTES = TOTAL * 8;
 };
 static_assert(Smem::BYTES <= 232448, "stage shared memory exceeds 227 KB");
@@ -174,6 +175,8 @@ struct LeafInfo {
 };
 constexpr int FLUX_SLOT = 3 * NF * 9 * 8 * 8;  // FX (6,9,8,8) | FY (6,8,9,8) | FZ (6,8,8,9)
 constexpr int FXO = 0, FYO = NF * 9 * 64, FZO = 2 * NF * 9 * 64;
+
+static_assert(sizeof(LeafInfo) == 20 * 8, "LeafInfo is 160 bytes (Smem::LINFO)");
 
 struct StageArgs {
   const double* ucur;   // [6][L][512] stage input (halo source)
@@ -248,7 +251,9 @@ struct Stage {
   StageArgs A;
   int run, R, X;
   int ring[5];  // shared-memory offsets of planes X-2 .. X+2 in the prim ring
-  const int* leaves;
+  const int* leaves;      // the run's leaves (global memory; staged into lids)
+  const LeafInfo* LIs;    // shared-memory copies of the run's LeafInfo
+  const int* lids;        // shared-memory copies of the run's leaf indices
   // thread-carried reductions
   double amax;
   long long fb;
@@ -262,10 +267,23 @@ struct Stage {
   }
   OMB_HD const double* ringp(int k, int v) const { return S + ring[k] + v * PL; }
 
+  // copy the run's leaf descriptors into shared memory (read every plane;
+  // global copies would keep missing the small L1 left beside 230 KB of
+  // shared memory).  A barrier must follow.
+  OMB_HD void stage_run_info(int tid, int nthr) {
+    int* dst = (int*)(S + Smem::LINFO);
+    for (int i = tid; i < R * 40; i += nthr) dst[i] = ((const int*)&A.info[leaves[i / 40]])[i % 40];
+    if (tid < R) ((int*)(S + Smem::LINFO + 80))[tid] = leaves[tid];
+  }
+  OMB_HD void bind_run_info() {
+    LIs = (const LeafInfo*)(S + Smem::LINFO);
+    lids = (const int*)(S + Smem::LINFO + 80);
+  }
+
   // flux export slot of this run's leaf (exporting leaves always run alone)
   OMB_HD double* export_slot() const {
     if (R != 1 || A.flux == nullptr) return nullptr;
-    const LeafInfo& LI = A.info[leaves[0]];
+    const LeafInfo& LI = LIs[0];
     return (LI.flags & 1) ? A.flux + (long long)LI.slot * FLUX_SLOT : nullptr;
   }
 
@@ -278,18 +296,16 @@ struct Stage {
   OMB_HD bool interior(int X) const { return X >= 3 && X < 8 * R + 3; }
 
   // ---- P0: gather + primitives of padded plane X into the ring -----------
-  OMB_HD void view_of(int X, int& leaf, int& lx) const {
-    int r;
+  OMB_HD void view_of(int X, int& r, int& lx) const {  // run-local leaf r, padded x in it
     if (X < 3) { r = 0; lx = X; }
     else if (X >= 8 * R + 3) { r = R - 1; lx = X - 8 * (R - 1); }
     else { r = (X - 3) >> 3; lx = 3 + ((X - 3) & 7); }
-    leaf = leaves[r];
   }
 
   OMB_HD void load_plane(int X, int tid, int nthr) {  // synchronous (prologue)
-    int leaf, lx;
-    view_of(X, leaf, lx);
-    const LeafInfo& LI = A.info[leaf];
+    int r, lx;
+    view_of(X, r, lx);
+    const LeafInfo& LI = LIs[r];
     for (int it = tid; it < PL; it += nthr) {
       double u[NF], w[NF];
       gather_cell(A.ucur, A.fstride, LI, A.bc, lx, it / M, it % M, u);
@@ -301,9 +317,9 @@ struct Stage {
 
   // issue the asynchronous gather of padded plane Xn into SG0 (or `stage`)
   OMB_HD void prefetch_plane(int Xn, int tid, int nthr, int stage = Smem::SG0) {
-    int leaf, lx;
-    view_of(Xn, leaf, lx);
-    const LeafInfo& LI = A.info[leaf];
+    int r, lx;
+    view_of(Xn, r, lx);
+    const LeafInfo& LI = LIs[r];
     for (int it = tid; it < PL; it += nthr) {
       int fm;
       long long base = gather_addr(LI, A.bc, lx, it / M, it % M, fm);
@@ -314,9 +330,9 @@ struct Stage {
 
   // P0: primitives of the staged plane Xn into the ring (flips re-derived)
   OMB_HD void convert_plane(int Xn, int tid, int nthr, int stage = Smem::SG0) {
-    int leaf, lx;
-    view_of(Xn, leaf, lx);
-    const LeafInfo& LI = A.info[leaf];
+    int r, lx;
+    view_of(Xn, r, lx);
+    const LeafInfo& LI = LIs[r];
     for (int it = tid; it < PL; it += nthr) {
       int fm;
       gather_addr(LI, A.bc, lx, it / M, it % M, fm);
@@ -335,7 +351,7 @@ struct Stage {
   // issue the asynchronous loads of cur, u0 (and gravity) of plane Xc's cells into SG6
   OMB_HD void prefetch_update(int Xc, int tid, int nthr) {
     int r = (Xc - 3) >> 3, lx = (Xc - 3) & 7;
-    long long base = (long long)leaves[r] * 512 + lx * 64;
+    long long base = (long long)lids[r] * 512 + lx * 64;
     bool grav = A.grav != nullptr;
     for (int it = tid; it < NFACEX; it += nthr) {
       long long cell = base + it;  // (y-3)*8 + (z-3) == it
@@ -648,8 +664,8 @@ struct Stage {
   OMB_HD void update_plane(int tid, int nthr) {
     int Xc = X - 1;
     int r = (Xc - 3) >> 3, lx = (Xc - 3) & 7;
-    int leaf = leaves[r];
-    const LeafInfo& LI = A.info[leaf];
+    int leaf = lids[r];
+    const LeafInfo& LI = LIs[r];
     if (LI.flags & 2) return;  // coarse leaf on a coarse/fine face: omb_reflux_update does it
     const double* FXlo = S + Smem::FX + (Xc % 3) * NF * NFACEX;
     const double* FXhi = S + Smem::FX + (X % 3) * NF * NFACEX;

@@ -35,6 +35,7 @@ extern "C" int emu_stage(const OmbStageDesc* d, int nthr) {
     }
     int R = st[0].R;
 #define ALL(stmt) for (int t = 0; t < nthr; t++) { Stage& s = st[t]; (void)s; stmt; }
+    ALL(s.bind_run_info(); s.stage_run_info(t, nthr));
     // the phase sequence of k_stage (omb_kernels.cu), one ALL() per barrier interval
     for (int X = 0; X < 4; X++) ALL(s.prefetch_plane(X, t, nthr, Smem::RAW + X * NF * PL));
     ALL(s.prefetch_plane(4, t, nthr));
