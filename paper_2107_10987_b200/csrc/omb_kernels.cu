@@ -341,7 +341,8 @@ __global__ void __launch_bounds__(NT, 1) k_stage(StageArgs A) {
     if (st.interior(X)) st.inplane_fluxes(tid, nthr);  // P4 (<= 468 items)
     __syncthreads();
     PH(7);
-    if (st.interior(X - 1)) st.prefetch_update(X - 1, tid, nthr);  // stage next P6
+    // stage the next P6's inputs, on the last 64 threads (idle in P5's 432 items)
+    if (st.interior(X - 1) && tid >= nthr - NFACEX) st.prefetch_update(X - 1, tid - (nthr - NFACEX), NFACEX);
     async_commit();
     if (X >= 3) st.faces_yz(tid, nthr);  // P5
     // the next P0 needs SG0 only; the SG6 group just issued has until P2A

@@ -56,7 +56,7 @@ extern "C" int emu_stage(const OmbStageDesc* d, int nthr) {
       }
       ALL(s.inplane_lines(t, nthr));
       ALL(if (s.interior(X)) s.inplane_fluxes(t, nthr));
-      ALL(if (s.interior(X - 1)) s.prefetch_update(X - 1, t, nthr);
+      ALL(if (s.interior(X - 1) && t >= nthr - NFACEX) s.prefetch_update(X - 1, t - (nthr - NFACEX), NFACEX);
           if (X >= 3) s.faces_yz(t, nthr));
     }
     ALL(s.set_plane(8 * R + 3); s.update_plane(t, nthr));
