@@ -305,13 +305,25 @@ __global__ void __launch_bounds__(NT, 1) k_stage(StageArgs A) {
   const int ngroups = A.new_mode ? 2 : 1;
   for (int X = 2; X < 8 * R + 4; X++) {
     st.set_plane(X);
-    if (X + 2 < 8 * R + 6) st.convert_plane(X + 2, tid, nthr);  // P0
+    // P0: primitives of plane X+2 (threads [0, 196)); beside it P5 of plane
+    // X-1 -- its y/z faces (the next phase overwrites the in-plane fluxes they
+    // read) -- and the staging of the next update's inputs (SG6)
+    if (X + 2 < 8 * R + 6) st.convert_plane(X + 2, tid, nthr);
+    if (X - 1 >= 3) {
+      st.set_plane(X - 1);
+      st.faces_yz(tid, nthr, PL);
+      st.set_plane(X);
+    }
+    // (512 threads: [116, 196) convert a cell and have no face item)
+    constexpr int T6 = NF * NYF - (512 - PL);
+    if (st.interior(X - 2) && tid >= T6 && tid < T6 + NFACEX) st.prefetch_update(X - 2, tid - T6, NFACEX);
+    async_commit();
     __syncthreads();
     PH(1);
     if (X + 3 < 8 * R + 6) st.prefetch_plane(X + 3, tid, nthr);  // stage next P0 (cp.async)
     async_commit();
     // P6 = the update of plane X-2 (its x fluxes sit in the 3-slot FX ring,
-    // its y/z fluxes in FYZ until this plane's P5, its inputs staged in SG6)
+    // its y/z fluxes in FYZ since this plane's P0, its inputs staged in SG6)
     // runs on the last 64 threads, idle in the last P1 group (<= 400 items)
     const bool p6 = X >= 3 && st.interior(X - 2);
 #pragma unroll 1
@@ -329,9 +341,10 @@ __global__ void __launch_bounds__(NT, 1) k_stage(StageArgs A) {
         if (g == 0) st.combine_A(tid, nthr);
         else if (A.quad) st.combine_B(tid, nthr);
       }
-      // the update inputs staged in the previous plane's P5 (SG6) must have
-      // landed before P1B's update (this plane's SG0 group may still fly)
+      // the update inputs staged in this plane's P0 (SG6) must have landed
+      // before P1B's update (this plane's SG0 group may still fly)
       if (g == 0 && ngroups == 2) async_wait_prev();
+      else if (ngroups == 1) async_wait_all();
       __syncthreads();
       PH(3 + 2 * g);
     }
@@ -339,21 +352,19 @@ __global__ void __launch_bounds__(NT, 1) k_stage(StageArgs A) {
     __syncthreads();
     PH(6);
     if (st.interior(X)) st.inplane_fluxes(tid, nthr);  // P4 (<= 468 items)
+    async_wait_all();  // SG0 for the next P0
     __syncthreads();
     PH(7);
-    // stage the next P6's inputs, on the last 64 threads (idle in P5's 432 items)
-    if (st.interior(X - 1) && tid >= nthr - NFACEX) st.prefetch_update(X - 1, tid - (nthr - NFACEX), NFACEX);
-    async_commit();
-    if (X >= 3) st.faces_yz(tid, nthr);  // P5
-    // the next P0 needs SG0 only; the SG6 group just issued has until P2A
-    if (ngroups == 2) async_wait_prev();
-    else async_wait_all();
-    __syncthreads();
-    PH(8);
   }
-  // P6 of the last plane
+  // P5 of the last plane, and the last update's inputs
+  st.set_plane(8 * R + 3);
+  st.faces_yz(tid, nthr);
+  if (tid < NFACEX) st.prefetch_update(8 * R + 2, tid, NFACEX);
+  async_commit();
   async_wait_all();
   __syncthreads();
+  PH(8);
+  // P6 of the last plane
   st.set_plane(8 * R + 3);
   st.update_plane(tid, nthr);
   PH(9);

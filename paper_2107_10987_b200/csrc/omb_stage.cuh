@@ -611,12 +611,16 @@ struct Stage {
   OMB_HD double bv(int axi, int v, int a, int b) { return S[Smem::BV + (axi * NF + v) * NCOR + cslot(a, b)]; }
 
   // ---- P5: finish y/z faces of plane X-1, start those of plane X ---------
-  OMB_HD void faces_yz(int tid, int nthr) {
+  // (thread tid takes items from (tid - first) mod nthr on: P0 runs this
+  // beside the conversion, which occupies threads [0, first))
+  OMB_HD void faces_yz(int tid, int nthr, int first = 0) {
     bool fin = interior(X - 1), start = interior(X);
     bool q = A.quad;
+    int t0 = tid - first;
+    if (t0 < 0) t0 += nthr;
     // one item = the y face and the z face of slot (v, s): 432 items, one
     // round on 512 threads, two independent chains per thread
-    for (int it = tid; it < NF * NYF; it += nthr)
+    for (int it = t0; it < NF * NYF; it += nthr)
 #pragma unroll
     for (int zf = 0; zf < 2; zf++) {
       int v = it / NYF, s = it % NYF;  // NYF == NZF

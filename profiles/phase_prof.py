@@ -10,8 +10,9 @@ import os
 import sys
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
-NAMES = ["prologue", "P0 convert", "P1A lines 0,3-6 + KT", "P2A combine", "P1B lines 9-12 + KT + P6",
-         "P2B combine", "P3 in-plane mono", "P4 in-plane KT", "P5 y/z faces", "epilogue P6"]
+NAMES = ["prologue", "P0 convert + P5 of prev plane", "P1A lines 0,3-6 + KT", "P2A combine",
+         "P1B lines 9-12 + KT + P6", "P2B combine", "P3 in-plane mono", "P4 in-plane KT", "last P5",
+         "epilogue P6"]
 
 
 def main(kind="sedov", level=4, steps=3):

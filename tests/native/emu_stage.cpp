@@ -41,9 +41,12 @@ extern "C" int emu_stage(const OmbStageDesc* d, int nthr) {
     ALL(s.prefetch_plane(4, t, nthr));
     for (int X = 0; X < 4; X++) ALL(s.convert_plane(X, t, nthr, Smem::RAW + X * NF * PL));
     const int ngroups = A.new_mode ? 2 : 1;
+    const int T6 = NF * NYF - (512 - PL);
     for (int X = 2; X < 8 * R + 4; X++) {
       ALL(s.set_plane(X));
-      ALL(if (X + 2 < 8 * R + 6) s.convert_plane(X + 2, t, nthr));
+      ALL(if (X + 2 < 8 * R + 6) s.convert_plane(X + 2, t, nthr);
+          if (X - 1 >= 3) { s.set_plane(X - 1); s.faces_yz(t, nthr, PL); s.set_plane(X); }
+          if (s.interior(X - 2) && t >= T6 && t < T6 + NFACEX) s.prefetch_update(X - 2, t - T6, NFACEX));
       ALL(if (X + 3 < 8 * R + 6) s.prefetch_plane(X + 3, t, nthr));
       const bool p6 = X >= 3 && st[0].interior(X - 2);
       for (int g = 0; g < ngroups; g++) {
@@ -56,9 +59,8 @@ extern "C" int emu_stage(const OmbStageDesc* d, int nthr) {
       }
       ALL(s.inplane_lines(t, nthr));
       ALL(if (s.interior(X)) s.inplane_fluxes(t, nthr));
-      ALL(if (s.interior(X - 1) && t >= nthr - NFACEX) s.prefetch_update(X - 1, t - (nthr - NFACEX), NFACEX);
-          if (X >= 3) s.faces_yz(t, nthr));
     }
+    ALL(s.set_plane(8 * R + 3); s.faces_yz(t, nthr); if (t < NFACEX) s.prefetch_update(8 * R + 2, t, NFACEX));
     ALL(s.set_plane(8 * R + 3); s.update_plane(t, nthr));
     double m = 0.0;
     long long f = 0;
