@@ -2,6 +2,8 @@
 // (include/omb200.h).  Build: see paper_2107_10987_b200/build.py
 // (nvcc -gencode arch=compute_100a,code=sm_100a -fmad=false ...).
 #include <cuda_runtime.h>
+#include <emmintrin.h>
+#include <stdint.h>
 #include <stdio.h>
 #include <stdlib.h>
 #include <string.h>
@@ -879,6 +881,9 @@ template <int NN>
 static void copy_leaf_n(const double* u, double* packed, int i, long long fstride, bool to_packed) {
   constexpr int m = NN + 6;
   constexpr long long n3 = (long long)NN * NN * NN;
+  // packing: whole 64-byte rows of the (pinned) staging buffer are written
+  // with streaming stores -- no read-for-ownership of the destination lines
+  const bool stream = to_packed && NN % 2 == 0 && ((uintptr_t)packed & 15) == 0 && (fstride % 2) == 0;
   for (int v = 0; v < 6; v++) {
     double* P = packed + (long long)v * fstride + (long long)i * n3;
     double* Q = const_cast<double*>(u) + (long long)v * m * m * m + (3 * m + 3) * m + 3;
@@ -886,10 +891,17 @@ static void copy_leaf_n(const double* u, double* packed, int i, long long fstrid
       for (int y = 0; y < NN; y++) {
         double* p = P + (x * NN + y) * NN;
         double* q = Q + (x * m + y) * m;
-        if (to_packed) memcpy(p, q, sizeof(double) * NN);  // constant size: inlined vector moves
-        else memcpy(q, p, sizeof(double) * NN);
+        if (stream) {
+#pragma unroll
+          for (int k = 0; k < NN; k += 2) _mm_stream_pd(p + k, _mm_loadu_pd(q + k));
+        } else if (to_packed) {
+          memcpy(p, q, sizeof(double) * NN);  // constant size: inlined vector moves
+        } else {
+          memcpy(q, p, sizeof(double) * NN);
+        }
       }
   }
+  if (stream) _mm_sfence();
 }
 extern "C" {
 static void copy_leaf(const double* u, double* packed, int i, int n, long long fstride, bool to_packed) {
