@@ -145,6 +145,32 @@ int omb_fp64_peak(double *scratch, int blocks, int iters, void *stream);
 int omb_gather(const double *u, long long fstride, const OmbLeafInfo *info, int leaf, int bc,
                double *out, void *stream);
 
+/* ---- FMM gravity (gravity/solver.py:50-164; _core.pyx:372-608; multipole.py) ----------------------
+ * Order-3 Cartesian FMM over the entity table (octree nodes + each leaf's block hierarchy down to cells).
+ * omb_fmm_traverse (HOST): the dual-tree traversal of build_interactions (_core.pyx:372-459): pairs
+ *   (pa, pb) in discovery order with their lattice keys; returns the count, or -(count) if cap was
+ *   too small.  center [nent][3], width [nent], children [nent][8] (-1 for cells), is_cell [nent].
+ * Device passes (stream-ordered): masses rho*dx^3 into the cell entities' M0 (M = [nent][20]);
+ *   upward per level (parents [np] of that level); M2L per target entity with its contributions
+ *   in the reference's order (off [ntarget+1] into contrib: source | group << 40 | flip << 63,
+ *   D [G][2][20] kernel derivatives and their parity flip, cellcell [G]); downward per level;
+ *   fields phi / gx / gy / gz [nleaf][512] of the cell entities (cell_base [nleaf]). */
+long long omb_fmm_traverse(const double *center, const double *width, const long long *children,
+                           const unsigned char *is_cell, long long nent, long long root, double theta,
+                           long long *pa, long long *pb, long long *pk, long long cap);
+int omb_fmm_masses(const double *rho, const long long *cell_base, int nleaf, const double *dx3, double *M,
+                   void *stream);
+int omb_fmm_upward(const long long *parents, int np, const long long *children, const double *center, double *M,
+                   void *stream);
+int omb_fmm_m2l(const long long *off, const unsigned long long *contrib, const double *D,
+                const unsigned char *cellcell, const double *M, double *L, long long ntarget,
+                const long long *targets, void *stream);
+int omb_fmm_downward(const long long *parents, int np, const long long *children, const double *center, double *L,
+                     void *stream);
+int omb_fmm_fields(const double *L, const long long *cell_base, int nleaf, double *phi, double *gx, double *gy,
+                   double *gz, void *stream);
+const char *omb_fmm_last_error(void);
+
 #ifdef __cplusplus
 }
 #endif

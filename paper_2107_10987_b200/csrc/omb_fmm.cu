@@ -1,0 +1,348 @@
+// omb_fmm.cu -- the FMM gravity solve on the device (SURVEY.md §8(f) rank 4:
+// the paper's other GPU path), behind the reference's FmmSolver
+// (gravity/solver.py:50-164).
+//
+// Host side: the dual-tree traversal that enumerates the interaction pairs
+// (_core.pyx:372-494, build_interactions) -- same stack discipline, same
+// opening criterion, same lattice keys -- so the pair list, its grouping and
+// hence every summation order are the reference's.
+//
+// Device side, per solve (order-3 Cartesian expansions, 20 components):
+//   k_fmm_masses    point masses rho*dx^3 of the cell entities
+//   k_fmm_upward    per level, fine to coarse: parent moments = sum over the 8
+//                   children, in child order, of the translated child moments
+//                   (solver.py:92-103, multipole.py:98-127)
+//   k_fmm_m2l       per target entity, its interactions in the reference's
+//                   global order (group by group, pair by pair; _core.pyx:563-608):
+//                   L += m2l(M_src, D) or the cell-cell monopole form
+//   k_fmm_downward  per level, coarse to fine: child L += shifted parent L
+//                   (solver.py:105-115, multipole.py:130-170)
+//   k_fmm_fields    phi = L0, g = -L1 of the cell entities into per-leaf
+//                   [n^3] arrays (solver.py:117-132)
+// Every expression keeps the reference's association (numpy left to right,
+// numpy's axis-1 sum sequential); compiled with -fmad=false.
+#include <cuda_runtime.h>
+#include <math.h>
+#include <stdlib.h>
+#include <string.h>
+
+#include <string>
+#include <vector>
+
+#include "../../include/omb200.h"
+
+namespace {
+
+constexpr int NC = 20;  // [M0, M1(3), M2(6), M3(10)]
+// symmetric tensor component tables (multipole.py:21-42)
+__constant__ int c_s2a[6] = {0, 0, 0, 1, 1, 2};
+__constant__ int c_s2b[6] = {0, 1, 2, 1, 2, 2};
+__constant__ int c_s3a[10] = {0, 0, 0, 0, 0, 0, 1, 1, 1, 2};
+__constant__ int c_s3b[10] = {0, 0, 0, 1, 1, 2, 1, 1, 2, 2};
+__constant__ int c_s3c[10] = {0, 1, 2, 1, 2, 2, 1, 2, 2, 2};
+__constant__ double c_mult2[6] = {1.0, 2.0, 2.0, 1.0, 2.0, 1.0};
+__constant__ double c_mult3[10] = {1.0, 3.0, 3.0, 3.0, 6.0, 3.0, 1.0, 3.0, 3.0, 1.0};
+
+__device__ __forceinline__ int idx2(int a, int b) {  // (a,b) -> 0..5
+  int lo = a < b ? a : b, hi = a < b ? b : a;
+  return lo == 0 ? hi : (lo == 1 ? 2 + hi : 5);
+}
+__device__ __forceinline__ int idx3(int a, int b, int c) {  // sorted (a,b,c) -> 0..9
+  int x = a, y = b, z = c, t;
+  if (x > y) { t = x; x = y; y = t; }
+  if (y > z) { t = y; y = z; z = t; }
+  if (x > y) { t = x; x = y; y = t; }
+  // S3 order: 000 001 002 011 012 022 111 112 122 222
+  if (x == 0) {
+    if (y == 0) return z;           // 0,1,2
+    if (y == 1) return z == 1 ? 3 : 4;
+    return 5;
+  }
+  if (x == 1) {
+    if (y == 1) return z == 1 ? 6 : 7;
+    return 8;
+  }
+  return 9;
+}
+
+// ---------------------------------------------------------------------------
+// upward: M[p] = sum_k translate_moments(M[child_k], center[child_k] - center[p])
+// ---------------------------------------------------------------------------
+__device__ void translate_add(const double* f, const double t[3], double* out, bool first) {
+  double M0 = f[0];
+  double r[NC];
+  r[0] = M0;
+  for (int a = 0; a < 3; a++) r[1 + a] = f[1 + a] + M0 * t[a];
+  for (int i = 0; i < 6; i++) {
+    int a = c_s2a[i], b = c_s2b[i];
+    r[4 + i] = ((f[4 + i] + f[1 + a] * t[b]) + f[1 + b] * t[a]) + (M0 * t[a]) * t[b];
+  }
+  for (int i = 0; i < 10; i++) {
+    int a = c_s3a[i], b = c_s3b[i], c = c_s3c[i];
+    double m2ab = f[4 + idx2(a, b)], m2ac = f[4 + idx2(a, c)], m2bc = f[4 + idx2(b, c)];
+    r[10 + i] = ((((((f[10 + i] + m2ab * t[c]) + m2ac * t[b]) + m2bc * t[a]) + (f[1 + a] * t[b]) * t[c]) +
+                  (f[1 + b] * t[a]) * t[c]) +
+                 (f[1 + c] * t[a]) * t[b]) +
+                ((M0 * t[a]) * t[b]) * t[c];
+  }
+  for (int k = 0; k < NC; k++) out[k] = first ? r[k] : out[k] + r[k];
+}
+
+__global__ void k_fmm_upward(const long long* parents, int np, const long long* children, const double* center,
+                             double* M) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= np) return;
+  long long p = parents[i];
+  double acc[NC];
+  for (int k = 0; k < 8; k++) {
+    long long c = children[p * 8 + k];
+    double t[3];
+    for (int a = 0; a < 3; a++) t[a] = center[c * 3 + a] - center[p * 3 + a];
+    translate_add(M + c * NC, t, acc, k == 0);
+  }
+  for (int k = 0; k < NC; k++) M[p * NC + k] = acc[k];
+}
+
+// ---------------------------------------------------------------------------
+// M2L: L[x] += contributions in the reference's order (_core.pyx:534-608)
+// ---------------------------------------------------------------------------
+__device__ void m2l_add(const double* M, const double* D, double* L) {
+  double M0 = M[0];
+  double acc = D[0] * M0;
+  for (int a = 0; a < 3; a++) acc = acc - D[1 + a] * M[1 + a];
+  for (int i = 0; i < 6; i++) acc = acc + ((0.5 * c_mult2[i]) * D[4 + i]) * M[4 + i];
+  for (int i = 0; i < 10; i++) acc = acc - ((c_mult3[i] / 6.0) * D[10 + i]) * M[10 + i];
+  L[0] += acc;
+  for (int a = 0; a < 3; a++) {
+    acc = D[1 + a] * M0;
+    for (int b = 0; b < 3; b++) acc = acc - D[4 + idx2(a, b)] * M[1 + b];
+    for (int i = 0; i < 6; i++) acc = acc + ((0.5 * c_mult2[i]) * D[10 + idx3(a, c_s2a[i], c_s2b[i])]) * M[4 + i];
+    L[1 + a] += acc;
+  }
+  for (int i = 0; i < 6; i++) {
+    acc = D[4 + i] * M0;
+    for (int b = 0; b < 3; b++) acc = acc - D[10 + idx3(c_s2a[i], c_s2b[i], b)] * M[1 + b];
+    L[4 + i] += acc;
+  }
+  for (int i = 0; i < 10; i++) L[10 + i] += D[10 + i] * M0;
+}
+
+// contribution word: source entity (bits 0..39) | group (40..62) | flip (63)
+__global__ void k_fmm_m2l(const long long* off, const unsigned long long* contrib, const double* D /*[G][2][20]*/,
+                          const unsigned char* cellcell, const double* M, double* L, long long ntarget,
+                          const long long* targets) {
+  long long ti = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (ti >= ntarget) return;
+  long long x = targets[ti];
+  double l[NC];
+  for (int k = 0; k < NC; k++) l[k] = L[x * NC + k];
+  for (long long q = off[ti]; q < off[ti + 1]; q++) {
+    unsigned long long w = contrib[q];
+    long long src = (long long)(w & 0xFFFFFFFFFFull);
+    long long g = (long long)((w >> 40) & 0x7FFFFFull);
+    int flip = (int)(w >> 63);
+    const double* Dg = D + (g * 2 + flip) * NC;
+    if (cellcell[g]) {
+      // L[eb,0] += ma*D0; L[eb,c] += ma*D_c; L[ea,0] += mb*D0; L[ea,c] += mb*(-D_c)
+      // (the flipped D holds -D_c: x*(-d) is the reference's mb*(-D1))
+      double m = M[src * NC];
+      l[0] += m * Dg[0];
+      for (int c = 0; c < 3; c++) l[1 + c] += m * Dg[1 + c];
+    } else {
+      m2l_add(M + src * NC, Dg, l);
+    }
+  }
+  for (int k = 0; k < NC; k++) L[x * NC + k] = l[k];
+}
+
+// ---------------------------------------------------------------------------
+// downward: L[child] += translate_local(L[p], center[child] - center[p])
+// ---------------------------------------------------------------------------
+__device__ void translate_local(const double* f, const double s[3], double* out) {
+  double acc0 = f[0];
+  for (int a = 0; a < 3; a++) acc0 = acc0 + f[1 + a] * s[a];
+  for (int i = 0; i < 6; i++) {
+    int a = c_s2a[i], b = c_s2b[i];
+    acc0 = acc0 + (((0.5 * c_mult2[i]) * f[4 + i]) * s[a]) * s[b];
+  }
+  for (int i = 0; i < 10; i++) {
+    int a = c_s3a[i], b = c_s3b[i], c = c_s3c[i];
+    acc0 = acc0 + ((((c_mult3[i] / 6.0) * f[10 + i]) * s[a]) * s[b]) * s[c];
+  }
+  out[0] = acc0;
+  for (int a = 0; a < 3; a++) {
+    double acc = f[1 + a];
+    for (int b = 0; b < 3; b++) acc = acc + f[4 + idx2(a, b)] * s[b];
+    for (int i = 0; i < 6; i++) {
+      int b = c_s2a[i], c = c_s2b[i];
+      acc = acc + (((0.5 * c_mult2[i]) * f[10 + idx3(a, b, c)]) * s[b]) * s[c];
+    }
+    out[1 + a] = acc;
+  }
+  for (int i = 0; i < 6; i++) {
+    int a = c_s2a[i], b = c_s2b[i];
+    double acc = f[4 + i];
+    for (int c = 0; c < 3; c++) acc = acc + f[10 + idx3(a, b, c)] * s[c];
+    out[4 + i] = acc;
+  }
+  for (int i = 0; i < 10; i++) out[10 + i] = f[10 + i];
+}
+
+__global__ void k_fmm_downward(const long long* parents, int np, const long long* children, const double* center,
+                               double* L) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= np * 8) return;
+  long long p = parents[i / 8];
+  long long c = children[p * 8 + i % 8];
+  double s[3], sh[NC];
+  for (int a = 0; a < 3; a++) s[a] = center[c * 3 + a] - center[p * 3 + a];
+  translate_local(L + p * NC, s, sh);
+  for (int k = 0; k < NC; k++) L[c * NC + k] = L[c * NC + k] + sh[k];
+}
+
+// cell masses: M[cell_entity(leaf, c)] = rho(leaf, c) * dx3(leaf); other components 0
+__global__ void k_fmm_masses(const double* rho, long long fstride_unused, const long long* cell_base, int L,
+                             const double* dx3, double* M) {
+  long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (i >= (long long)L * 512) return;
+  int leaf = (int)(i / 512), c = (int)(i % 512);
+  double* m = M + (cell_base[leaf] + c) * NC;
+  m[0] = rho[i] * dx3[leaf];
+  for (int k = 1; k < NC; k++) m[k] = 0.0;
+}
+
+__global__ void k_fmm_fields(const double* L, const long long* cell_base, int nleaf, double* phi, double* gx,
+                             double* gy, double* gz) {
+  long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (i >= (long long)nleaf * 512) return;
+  int leaf = (int)(i / 512), c = (int)(i % 512);
+  const double* l = L + (cell_base[leaf] + c) * NC;
+  phi[i] = l[0];
+  gx[i] = -l[1];
+  gy[i] = -l[2];
+  gz[i] = -l[3];
+}
+
+thread_local std::string f_err;
+int ferr(const char* what, cudaError_t e) {
+  f_err = std::string(what) + ": " + cudaGetErrorString(e);
+  return -1;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* omb_fmm_last_error(void) { return f_err.c_str(); }
+
+// Dual-tree traversal (host), _core.pyx:372-459: pairs (pa, pb) in discovery
+// order with their lattice keys.  Returns the pair count, or -(needed) when
+// cap is too small (nothing written beyond cap), or -1 on allocation failure.
+long long omb_fmm_traverse(const double* center, const double* width, const long long* children,
+                           const unsigned char* is_cell, long long nent, long long root, double theta,
+                           long long* pa, long long* pb, long long* pk, long long cap) {
+  double wmin = width[0];
+  for (long long i = 1; i < nent; i++) wmin = width[i] < wmin ? width[i] : wmin;
+  const double quant = 2.0 / wmin;
+  const long long BIAS = 1LL << 16, SPAN = 1LL << 17;
+  std::vector<long long> st;
+  st.reserve(1 << 16);
+  st.push_back(root);
+  st.push_back(root);
+  long long pn = 0;
+  while (!st.empty()) {
+    long long b = st.back();
+    st.pop_back();
+    long long a = st.back();
+    st.pop_back();
+    if (a == b) {
+      if (is_cell[a]) continue;
+      for (int i = 0; i < 8; i++) {
+        st.push_back(children[a * 8 + i]);
+        st.push_back(children[a * 8 + i]);
+        for (int j = i + 1; j < 8; j++) {
+          st.push_back(children[a * 8 + i]);
+          st.push_back(children[a * 8 + j]);
+        }
+      }
+      continue;
+    }
+    double rx = center[b * 3 + 0] - center[a * 3 + 0];
+    double ry = center[b * 3 + 1] - center[a * 3 + 1];
+    double rz = center[b * 3 + 2] - center[a * 3 + 2];
+    double d = sqrt(rx * rx + ry * ry + rz * rz);
+    double wa = width[a], wb = width[b];
+    if (0.5 * (wa + wb) < theta * d) {
+    } else if (is_cell[a] && is_cell[b]) {
+    } else {
+      if (wa > wb) {
+        for (int i = 0; i < 8; i++) { st.push_back(children[a * 8 + i]); st.push_back(b); }
+      } else if (wb > wa) {
+        for (int i = 0; i < 8; i++) { st.push_back(a); st.push_back(children[b * 8 + i]); }
+      } else if (is_cell[a]) {
+        for (int i = 0; i < 8; i++) { st.push_back(a); st.push_back(children[b * 8 + i]); }
+      } else if (is_cell[b]) {
+        for (int i = 0; i < 8; i++) { st.push_back(children[a * 8 + i]); st.push_back(b); }
+      } else {
+        for (int i = 0; i < 8; i++)
+          for (int j = 0; j < 8; j++) { st.push_back(children[a * 8 + i]); st.push_back(children[b * 8 + j]); }
+      }
+      continue;
+    }
+    if (pn < cap) {
+      long long qx = llround(rx * quant), qy = llround(ry * quant), qz = llround(rz * quant);
+      long long flags = (is_cell[a] ? 2 : 0) + (is_cell[b] ? 1 : 0);
+      pa[pn] = a;
+      pb[pn] = b;
+      pk[pn] = (((qx + BIAS) * SPAN + (qy + BIAS)) * SPAN + (qz + BIAS)) * 4 + flags;
+    }
+    pn++;
+  }
+  return pn <= cap ? pn : -pn;
+}
+
+int omb_fmm_masses(const double* rho, const long long* cell_base, int nleaf, const double* dx3, double* M,
+                   void* stream) {
+  long long n = (long long)nleaf * 512;
+  if (n == 0) return 0;
+  k_fmm_masses<<<(unsigned)((n + 255) / 256), 256, 0, (cudaStream_t)stream>>>(rho, 0, cell_base, nleaf, dx3, M);
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? 0 : ferr("omb_fmm_masses", e);
+}
+
+int omb_fmm_upward(const long long* parents, int np, const long long* children, const double* center, double* M,
+                   void* stream) {
+  if (np <= 0) return 0;
+  k_fmm_upward<<<(np + 127) / 128, 128, 0, (cudaStream_t)stream>>>(parents, np, children, center, M);
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? 0 : ferr("omb_fmm_upward", e);
+}
+
+int omb_fmm_m2l(const long long* off, const unsigned long long* contrib, const double* D,
+                const unsigned char* cellcell, const double* M, double* L, long long ntarget, const long long* targets,
+                void* stream) {
+  if (ntarget <= 0) return 0;
+  k_fmm_m2l<<<(unsigned)((ntarget + 127) / 128), 128, 0, (cudaStream_t)stream>>>(off, contrib, D, cellcell, M, L,
+                                                                                  ntarget, targets);
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? 0 : ferr("omb_fmm_m2l", e);
+}
+
+int omb_fmm_downward(const long long* parents, int np, const long long* children, const double* center, double* L,
+                     void* stream) {
+  if (np <= 0) return 0;
+  k_fmm_downward<<<(np * 8 + 127) / 128, 128, 0, (cudaStream_t)stream>>>(parents, np, children, center, L);
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? 0 : ferr("omb_fmm_downward", e);
+}
+
+int omb_fmm_fields(const double* L, const long long* cell_base, int nleaf, double* phi, double* gx, double* gy,
+                   double* gz, void* stream) {
+  long long n = (long long)nleaf * 512;
+  if (n == 0) return 0;
+  k_fmm_fields<<<(unsigned)((n + 255) / 256), 256, 0, (cudaStream_t)stream>>>(L, cell_base, nleaf, phi, gx, gy, gz);
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? 0 : ferr("omb_fmm_fields", e);
+}
+
+}  // extern "C"

@@ -1,0 +1,329 @@
+"""Device FMM gravity: a drop-in for the reference's ``FmmSolver``
+(pkg/src/octomini/gravity/solver.py:50-164), SURVEY.md §8(f) rank 4.
+
+Host, once per tree topology (cached like ``FmmSolver.prepare``):
+  * the entity table -- every octree node plus, below each leaf, the complete
+    hierarchy of its sub-grid's blocks down to single cells
+    (gravity/entities.py:15-139, restated with the same numpy expressions so
+    centres are bit-identical);
+  * the dual-tree traversal in C++ (``omb_fmm_traverse``, the reference's
+    stack discipline, opening criterion and lattice keys, _core.pyx:372-459);
+  * the grouping by key (sorted keys, stable within a group, _core.pyx:476-494)
+    and the per-target contribution lists in the reference's global M2L order
+    (group by group, pair by pair, the b-side before the a-side,
+    _core.pyx:563-608);
+  * kernel derivatives per group with the same numpy expressions as
+    multipole.py:173-191.
+Device, per solve: cell masses -> upward translation per level -> M2L per
+target -> downward translation per level -> phi, g per cell (``omb_fmm_*``).
+Every floating-point operation keeps the reference's order, so phi and g are
+bitwise those of the reference's compiled backend (tests/test_fmm.py).
+"""
+
+import ctypes
+
+import numpy as np
+
+from . import _lib
+from .device import ptr, stream_handle
+
+NCOMP = 20
+S2 = [(0, 0), (0, 1), (0, 2), (1, 1), (1, 2), (2, 2)]
+S3 = [(0, 0, 0), (0, 0, 1), (0, 0, 2), (0, 1, 1), (0, 1, 2), (0, 2, 2), (1, 1, 1), (1, 1, 2), (1, 2, 2), (2, 2, 2)]
+
+
+def kernel_derivatives(R):
+    """D0..D3 of g(R) = -1/|R| (multipole.py:173-191), same numpy operations."""
+    R = np.asarray(R, dtype=float)
+    r2 = float(R @ R)
+    r = np.sqrt(r2)
+    r3 = r2 * r
+    r5 = r3 * r2
+    r7 = r5 * r2
+    D = np.empty(NCOMP)
+    D[0] = -1.0 / r
+    D[1:4] = R / r3
+    for i, (a, b) in enumerate(S2):
+        D[4 + i] = (1.0 if a == b else 0.0) / r3 - 3.0 * R[a] * R[b] / r5
+    for i, (a, b, c) in enumerate(S3):
+        term = 15.0 * R[a] * R[b] * R[c] / r7
+        term -= 3.0 * ((a == b) * R[c] + (a == c) * R[b] + (b == c) * R[a]) / r5
+        D[10 + i] = term
+    return D
+
+
+def flip_derivatives(D):
+    """D at -R: odd ranks negated (multipole.py:194-199)."""
+    out = D.copy()
+    out[..., 1:4] *= -1.0
+    out[..., 10:] *= -1.0
+    return out
+
+
+class EntityTable:
+    """Flat entity table (gravity/entities.py:15-139): centers, widths,
+    children (-1 for cells), is_cell, level; ``cell_base[i]`` is the entity of
+    cell 0 of ``sorted_leaves()[i]`` (its n^3 cells follow, x-major)."""
+
+    def __init__(self, tree):
+        n = tree.n
+        s = int(np.log2(n))
+        assert 2 ** s == n
+        leaves = tree.sorted_leaves()
+        per_leaf = (8 ** (s + 1) - 1) // 7
+        internal = []
+
+        def count_internal(node):
+            if not node.is_leaf:
+                internal.append(node)
+                for c in node.children:
+                    count_internal(c)
+
+        count_internal(tree.root)
+        total = len(internal) + len(leaves) * per_leaf
+        center = np.empty((total, 3), dtype=np.float64)
+        width = np.empty(total, dtype=np.float64)
+        children = np.full((total, 8), -1, dtype=np.int64)
+        is_cell = np.zeros(total, dtype=bool)
+        level = np.empty(total, dtype=np.int32)
+        cell_base = {}
+        cursor = [0]
+
+        def alloc(k):
+            base = cursor[0]
+            cursor[0] += k
+            return base
+
+        def build_leaf(node):
+            bases = [alloc(8 ** j) for j in range(s + 1)]
+            for j in range(s + 1):
+                nb = 2 ** j
+                ids = bases[j] + (np.arange(nb)[:, None, None] * nb + np.arange(nb)[None, :, None]) * nb \
+                    + np.arange(nb)[None, None, :]
+                w = tree.width / (2 ** (node.level + j))
+                corner = tree.lower + node.ipos * (tree.width / 2 ** node.level)
+                bx = np.arange(nb)
+                cx = corner[0] + (bx + 0.5) * w
+                cy = corner[1] + (bx + 0.5) * w
+                cz = corner[2] + (bx + 0.5) * w
+                flat = ids.reshape(-1)
+                center[flat, 0] = np.repeat(cx, nb * nb)
+                center[flat, 1] = np.tile(np.repeat(cy, nb), nb)
+                center[flat, 2] = np.tile(cz, nb * nb)
+                width[flat] = w
+                level[flat] = node.level + j
+                if j < s:
+                    nb2 = 2 * nb
+                    child = bases[j + 1] + (np.arange(nb2)[:, None, None] * nb2 + np.arange(nb2)[None, :, None]) \
+                        * nb2 + np.arange(nb2)[None, None, :]
+                    for kz in (0, 1):
+                        for ky in (0, 1):
+                            for kx in (0, 1):
+                                children[flat, kx + 2 * ky + 4 * kz] = child[kx::2, ky::2, kz::2].reshape(-1)
+                else:
+                    is_cell[flat] = True
+            cell_base[node.path] = bases[s]
+            return bases[0]
+
+        def build(node):
+            if node.is_leaf:
+                return build_leaf(node)
+            eid = alloc(1)
+            w = tree.width / 2 ** node.level
+            corner = tree.lower + node.ipos * w
+            center[eid] = corner + 0.5 * w
+            width[eid] = w
+            level[eid] = node.level
+            for k, c in enumerate(node.children):
+                children[eid, k] = build(c)
+            return eid
+
+        self.root = build(tree.root)
+        assert cursor[0] == total
+        self.center, self.width, self.children, self.is_cell, self.level = center, width, children, is_cell, level
+        self.n = n
+        self.nentities = total
+        self.leaf_paths = [lf.path for lf in leaves]
+        self.cell_base = np.array([cell_base[p] for p in self.leaf_paths], dtype=np.int64)
+
+
+def traverse(lib, table, theta):
+    """Interaction pairs (a, b, key) in the reference's discovery order."""
+    t = table
+    center = np.ascontiguousarray(t.center)
+    width = np.ascontiguousarray(t.width)
+    children = np.ascontiguousarray(t.children)
+    is_cell = np.ascontiguousarray(t.is_cell.astype(np.uint8))
+    cap = max(1 << 16, 160 * t.nentities)
+    while True:
+        pa = np.empty(cap, dtype=np.int64)
+        pb = np.empty(cap, dtype=np.int64)
+        pk = np.empty(cap, dtype=np.int64)
+        n = lib.omb_fmm_traverse(center.ctypes.data, width.ctypes.data, children.ctypes.data, is_cell.ctypes.data,
+                                 t.nentities, t.root, float(theta), pa.ctypes.data, pb.ctypes.data, pk.ctypes.data,
+                                 cap)
+        if n >= 0:
+            return pa[:n], pb[:n], pk[:n]
+        cap = -n
+
+
+def group_pairs(table, pa, pb, pk):
+    """Groups in sorted-key order, pairs stable within a group (_core.pyx:476-494):
+    returns (order, bounds, R per group, a_cell, b_cell per group)."""
+    keys, first_idx, inverse = np.unique(pk, return_index=True, return_inverse=True)
+    order = np.argsort(inverse, kind="stable")
+    bounds = np.searchsorted(inverse[order], np.arange(len(keys) + 1))
+    f = keys & 3
+    R = table.center[pb[first_idx]] - table.center[pa[first_idx]]
+    return order, bounds, R, (f & 2) != 0, (f & 1) != 0
+
+
+class B200FmmSolver:
+    """Order-3 FMM on the device; same API as the reference's ``FmmSolver``
+    (``prepare``, ``solve_density``, ``solve``, ``stats``).  theta in (0, 1]."""
+
+    def __init__(self, theta, device=None):
+        if theta < 0.0 or theta > 1.0:
+            raise ValueError("theta must lie in [0, 1]")
+        if theta == 0.0:
+            raise NotImplementedError("theta = 0 (always-reject direct traversal) is not provided on the device")
+        import torch
+
+        self.theta = float(theta)
+        self.dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+        self.lib = _lib.load()
+        self._signature = None
+        self.stats = {}
+
+    def _topology_signature(self, tree):
+        return (tree.n, tree.width, tuple(leaf.path for leaf in tree.sorted_leaves()))
+
+    def prepare(self, tree):
+        sig = self._topology_signature(tree)
+        if sig == self._signature:
+            return
+        import torch
+
+        from .mesh import check_balance
+
+        check_balance(tree)
+        t = EntityTable(tree)
+        self.table = t
+        pa, pb, pk = traverse(self.lib, t, self.theta)
+        order, bounds, R, a_cell, b_cell = group_pairs(t, pa, pb, pk)
+        G = len(R)
+        self.stats["groups"] = int(G)
+        self.stats["pairs"] = int(len(pa))
+        D = np.empty((G, 2, NCOMP))
+        for g in range(G):
+            D[g, 0] = kernel_derivatives(R[g])
+            D[g, 1] = flip_derivatives(D[g, 0])
+        grp = np.repeat(np.arange(G, dtype=np.int64), np.diff(bounds))  # group of each ordered pair
+        a_o, b_o = pa[order], pb[order]
+        # global contribution sequence: pair by pair, (target b <- a, D) then (target a <- b, Df)
+        tgt = np.empty(2 * len(order), dtype=np.int64)
+        src = np.empty_like(tgt)
+        flip = np.zeros(2 * len(order), dtype=np.uint64)
+        tgt[0::2], tgt[1::2] = b_o, a_o
+        src[0::2], src[1::2] = a_o, b_o
+        flip[1::2] = 1
+        g2 = np.repeat(grp, 2)
+        seq = np.argsort(tgt, kind="stable")  # per target, in the global order
+        tgt_s = tgt[seq]
+        targets, starts = np.unique(tgt_s, return_index=True)
+        off = np.append(starts, len(tgt_s)).astype(np.int64)
+        contrib = (src[seq].astype(np.uint64) | (g2[seq].astype(np.uint64) << np.uint64(40)) |
+                   (flip[seq] << np.uint64(63)))
+        dev = self.dev
+        T = torch
+        self._center = T.from_numpy(np.ascontiguousarray(t.center).reshape(-1)).to(dev)
+        self._children = T.from_numpy(np.ascontiguousarray(t.children).reshape(-1)).to(dev)
+        self._D = T.from_numpy(D.reshape(-1)).to(dev)
+        self._cellcell = T.from_numpy((a_cell & b_cell).astype(np.uint8)).to(dev)
+        self._off = T.from_numpy(off).to(dev)
+        self._contrib = T.from_numpy(contrib.view(np.int64)).to(dev)
+        self._targets = T.from_numpy(targets.astype(np.int64)).to(dev)
+        self._cell_base = T.from_numpy(t.cell_base).to(dev)
+        lv = t.level
+        parents = {int(L): np.nonzero((lv == L) & ~t.is_cell)[0].astype(np.int64) for L in np.unique(lv)}
+        self._up = [(L, T.from_numpy(parents[L]).to(dev)) for L in sorted(parents, reverse=True) if len(parents[L])]
+        self._down = [(L, T.from_numpy(parents[L]).to(dev)) for L in sorted(parents) if len(parents[L])]
+        self._M = T.zeros(t.nentities * NCOMP, dtype=T.float64, device=dev)
+        self._L = T.zeros_like(self._M)
+        self._signature = sig
+
+    # -- device passes ---------------------------------------------------------
+    def _run(self, rho_dev, dx3_dev, stream=None):
+        """rho_dev: [L][512] densities of sorted_leaves(); returns L (entities x 20)."""
+        lib, sh = self.lib, stream_handle(stream)
+        nleaf = len(self.table.leaf_paths)
+        self._M.zero_()
+        self._L.zero_()
+        _lib.check(lib.omb_fmm_masses(ptr(rho_dev), ptr(self._cell_base), nleaf, ptr(dx3_dev), ptr(self._M), sh),
+                   "omb_fmm_masses")
+        for _, par in self._up:
+            _lib.check(lib.omb_fmm_upward(ptr(par), int(par.numel()), ptr(self._children), ptr(self._center),
+                                          ptr(self._M), sh), "omb_fmm_upward")
+        _lib.check(lib.omb_fmm_m2l(ptr(self._off), ptr(self._contrib), ptr(self._D), ptr(self._cellcell),
+                                   ptr(self._M), ptr(self._L), int(self._targets.numel()), ptr(self._targets), sh),
+                   "omb_fmm_m2l")
+        for _, par in self._down:
+            _lib.check(lib.omb_fmm_downward(ptr(par), int(par.numel()), ptr(self._children), ptr(self._center),
+                                            ptr(self._L), sh), "omb_fmm_downward")
+        return self._L
+
+    def fields_device(self, rho_dev, dx3_dev, out4, stream=None):
+        """phi, gx, gy, gz per cell into out4 ([4][L][512] device tensor)."""
+        self._run(rho_dev, dx3_dev, stream)
+        nleaf = len(self.table.leaf_paths)
+        n = nleaf * 512
+        o = out4.reshape(4, -1)
+        _lib.check(self.lib.omb_fmm_fields(ptr(self._L), ptr(self._cell_base), nleaf, ptr(o[0]), ptr(o[1]), ptr(o[2]),
+                                           ptr(o[3]), stream_handle(stream)), "omb_fmm_fields")
+        return o[:, :n]
+
+    # -- the reference's host API ----------------------------------------------
+    def _dx3(self, tree):
+        import torch
+
+        return torch.tensor([lf.subgrid.dx ** 3 for lf in tree.sorted_leaves()], dtype=torch.float64,
+                            device=self.dev)
+
+    def solve_density(self, tree, per_leaf_density=None):
+        """(phi, g) keyed by leaf path, from the current density (or a
+        replacement per-leaf source), as solver.py:117-132."""
+        import torch
+
+        self.prepare(tree)
+        leaves = tree.sorted_leaves()
+        n = tree.n
+        rho = np.empty((len(leaves), n ** 3))
+        for i, lf in enumerate(leaves):
+            src = lf.subgrid.interior[0] if per_leaf_density is None else per_leaf_density[lf.path]
+            rho[i] = np.asarray(src, dtype=np.float64).reshape(-1)
+        out = torch.empty(4 * len(leaves) * 512, dtype=torch.float64, device=self.dev)
+        f = self.fields_device(torch.from_numpy(rho.reshape(-1)).to(self.dev), self._dx3(tree), out).cpu().numpy()
+        f = f.reshape(4, len(leaves), n, n, n)
+        out_phi, out_g = {}, {}
+        for i, lf in enumerate(leaves):
+            out_phi[lf.path] = f[0, i].copy()
+            out_g[lf.path] = f[1:4, i].copy()
+        return out_phi, out_g
+
+    def solve(self, tree, need_derivative=True):
+        """phi and g from rho, and dphi/dt from rho_dot = -div(momentum)
+        (solver.py:134-153; the ghosts of the host sub-grids must be filled,
+        as in the reference)."""
+        from .hydro import GravityField, momentum_divergence_source
+
+        self.prepare(tree)
+        phi, g = self.solve_density(tree)
+        dphi = None
+        if need_derivative:
+            rho_dot = {lf.path: momentum_divergence_source(lf.subgrid) for lf in tree.sorted_leaves()}
+            dphi, _ = self.solve_density(tree, per_leaf_density=rho_dot)
+        field = GravityField()
+        for path in phi:
+            gx, gy, gz = g[path]
+            field.add_leaf(path, phi[path], gx, gy, gz, dphi[path] if dphi is not None else None)
+        return field

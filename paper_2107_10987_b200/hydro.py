@@ -88,3 +88,35 @@ def conserved_from_primitive(rho, v, p, eos):
     u[EGAS] = eint + 0.5 * rho * (vx ** 2 + vy ** 2 + vz ** 2)
     u[TAU] = eint ** (1.0 / eos.gamma)
     return u
+
+
+class GravityField:
+    """Per-leaf potential, acceleration and potential time derivative
+    (gravity/solver.py:33-47); what a gravity solver's ``solve`` returns."""
+
+    def __init__(self):
+        self.per_leaf = {}
+
+    def __getitem__(self, path):
+        return self.per_leaf[path]
+
+    def add_leaf(self, path, phi, gx, gy, gz, dphi_dt=None):
+        self.per_leaf[path] = {"phi": phi, "gx": gx, "gy": gy, "gz": gz,
+                               "dphi_dt": dphi_dt if dphi_dt is not None else np.zeros_like(phi)}
+
+
+def momentum_divergence_source(subgrid):
+    """rho_dot = -div(s) by second-order central differences over the filled
+    ghosts (gravity/solver.py:156-168), same numpy expression."""
+    from .geometry import GHOST
+
+    g = GHOST
+    n = subgrid.n
+    u = subgrid.u
+    inv2dx = 1.0 / (2.0 * subgrid.dx)
+    sl = slice(g, g + n)
+    return -(
+        (u[SX, g + 1: g + n + 1, sl, sl] - u[SX, g - 1: g + n - 1, sl, sl])
+        + (u[SY, sl, g + 1: g + n + 1, sl] - u[SY, sl, g - 1: g + n - 1, sl])
+        + (u[SZ, sl, sl, g + 1: g + n + 1] - u[SZ, sl, sl, g - 1: g + n - 1])
+    ) * inv2dx

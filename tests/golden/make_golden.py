@@ -264,7 +264,63 @@ def checkpoint_case():
     print("wrote amr_reflux_init.omck")
 
 
+def fmm_case():
+    """Gravity FMM (gravity/solver.py): solve_density on a uniform level-1 tree
+    (theta 0.5 and 0.35) and on a corner-refined one, and the full solve with
+    dphi/dt from -div(momentum) (test_gravity.py:31-35 random densities)."""
+    from octomini.gravity import FmmSolver
+
+    def fill(tree, seed, mom=False):
+        rng = np.random.default_rng(seed)
+        for leaf in tree.leaves():
+            leaf.subgrid.interior[0] = rng.uniform(0.1, 2.0, (tree.n,) * 3)
+            if mom:
+                for c in (1, 2, 3):
+                    leaf.subgrid.interior[c] = rng.uniform(-1.0, 1.0, (tree.n,) * 3)
+        return tree
+
+    out = {}
+    cases = []
+    t = fill(build_uniform_tree(1, 8), 5)
+    cases += [("u05", t, 0.5), ("u035", t, 0.35)]
+    t2 = build_uniform_tree(1, 8)
+    t2.split(t2.leaf_at(1, (0, 0, 0)))
+    t2.reindex()
+    cases.append(("amr05", fill(t2, 6), 0.5))
+    for name, tree, theta in cases:
+        solver = FmmSolver(theta)
+        phi, g = solver.solve_density(tree)
+        leaves = tree.sorted_leaves()
+        out[f"{name}_paths"] = np.array([json.dumps(list(lf.path)) for lf in leaves])
+        out[f"{name}_rho"] = np.stack([lf.subgrid.interior[0] for lf in leaves])
+        out[f"{name}_phi"] = np.stack([phi[lf.path] for lf in leaves])
+        out[f"{name}_g"] = np.stack([g[lf.path] for lf in leaves])
+        out[f"{name}_stats"] = np.array([solver.stats["groups"], solver.stats["pairs"]])
+        grp = solver._groups
+        out[f"{name}_R"] = np.array([gr[0] for gr in grp])
+        h = hashlib.sha256()
+        for gr in grp:
+            h.update(np.ascontiguousarray(gr[1], dtype=np.int64).tobytes())
+            h.update(np.ascontiguousarray(gr[2], dtype=np.int64).tobytes())
+            h.update(bytes([int(gr[3]), int(gr[4])]))
+        out[f"{name}_pairs_sha"] = np.array(h.hexdigest())
+        out[f"{name}_theta"] = np.array(theta)
+    # full solve: phi, g and dphi/dt (ghosts filled by the reference)
+    t3 = fill(build_uniform_tree(1, 8, boundary="reflecting"), 7, mom=True)
+    exchange_ghosts(t3)
+    field = FmmSolver(0.5).solve(t3, need_derivative=True)
+    leaves = t3.sorted_leaves()
+    out["full_u"] = np.stack([lf.subgrid.u for lf in leaves])
+    out["full_paths"] = np.array([json.dumps(list(lf.path)) for lf in leaves])
+    for k in ("phi", "gx", "gy", "gz", "dphi_dt"):
+        out[f"full_{k}"] = np.stack([field[lf.path][k] for lf in leaves])
+    save("fmm", **out)
+
+
 def main():
+    if sys.argv[1:] == ["fmm"]:
+        fmm_case()
+        return
     checkpoint_case()
     amr_sedov_case()
     kernel_cases()
@@ -291,6 +347,7 @@ def main():
     random_smooth(t, seed=5)
     step_case("amr_reflux", t, steps=2)
     sources_case()
+    fmm_case()
 
 
 if __name__ == "__main__":

@@ -1,0 +1,86 @@
+"""Device FMM gravity against the reference's own
+FmmSolver (goldens made by tests/golden/make_golden.py fmm with the compiled
+backend): the host preparation (entity table, dual-tree traversal, grouping)
+must reproduce the reference's interaction groups exactly (CPU), and the
+device solve must reproduce phi, g and dphi/dt bitwise (GPU)."""
+
+import hashlib
+import json
+
+import numpy as np
+import pytest
+
+from _cases import golden
+from paper_2107_10987_b200 import gravity, mesh
+
+
+def _fill(tree, g, name):
+    assert [json.loads(p) for p in g[f"{name}_paths"]] == [list(lf.path) for lf in tree.sorted_leaves()]
+    for lf, rho in zip(tree.sorted_leaves(), g[f"{name}_rho"]):
+        lf.subgrid.interior[0] = rho
+    return tree
+
+
+def _tree(name):
+    if name in ("u05", "u035"):
+        return mesh.build_uniform_tree(1, 8)
+    t = mesh.build_uniform_tree(1, 8)
+    t.split(t.leaf_at(1, (0, 0, 0)))
+    t.reindex()
+    return t
+
+
+@pytest.mark.parametrize("name", ["u05", "u035", "amr05"])
+def test_interaction_groups_match_reference(name):
+    from paper_2107_10987_b200 import _lib
+
+    g = golden("fmm")
+    t = _fill(_tree(name), g, name)
+    table = gravity.EntityTable(t)
+    pa, pb, pk = gravity.traverse(_lib.load(), table, float(g[f"{name}_theta"]))
+    order, bounds, R, a_cell, b_cell = gravity.group_pairs(table, pa, pb, pk)
+    assert [len(R), len(pa)] == list(g[f"{name}_stats"])
+    assert np.array_equal(R, g[f"{name}_R"])
+    h = hashlib.sha256()
+    for k in range(len(R)):
+        sel = order[bounds[k]:bounds[k + 1]]
+        h.update(np.ascontiguousarray(pa[sel], dtype=np.int64).tobytes())
+        h.update(np.ascontiguousarray(pb[sel], dtype=np.int64).tobytes())
+        h.update(bytes([int(a_cell[k]), int(b_cell[k])]))
+    assert h.hexdigest() == str(g[f"{name}_pairs_sha"])
+
+
+def test_kernel_derivatives_formula():
+    """D(R) of g = -1/|R|: D0 = -1/r, D1 = R/r^3 (multipole.py:173-191)."""
+    R = np.array([0.3, -0.4, 1.2])
+    D = gravity.kernel_derivatives(R)
+    r = np.sqrt(R @ R)
+    assert D[0] == -1.0 / r
+    assert np.allclose(D[1:4], R / r ** 3, rtol=1e-15)
+    assert np.array_equal(gravity.flip_derivatives(D)[[0, 4, 5, 6, 7, 8, 9]], D[[0, 4, 5, 6, 7, 8, 9]])
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name", ["u05", "u035", "amr05"])
+def test_device_fmm_bitwise(name):
+    g = golden("fmm")
+    t = _fill(_tree(name), g, name)
+    solver = gravity.B200FmmSolver(float(g[f"{name}_theta"]))
+    phi, gg = solver.solve_density(t)
+    assert solver.stats["pairs"] == int(g[f"{name}_stats"][1])
+    for i, lf in enumerate(t.sorted_leaves()):
+        assert np.array_equal(phi[lf.path], g[f"{name}_phi"][i]), (name, i, "phi")
+        assert np.array_equal(gg[lf.path], g[f"{name}_g"][i]), (name, i, "g")
+
+
+@pytest.mark.gpu
+def test_device_fmm_full_solve_with_dphi_dt():
+    g = golden("fmm")
+    t = mesh.build_uniform_tree(1, 8, boundary="reflecting")
+    assert [json.loads(p) for p in g["full_paths"]] == [list(lf.path) for lf in t.sorted_leaves()]
+    for lf, u in zip(t.sorted_leaves(), g["full_u"]):
+        lf.subgrid.u[...] = u  # interiors + the reference's filled ghosts
+    field = gravity.B200FmmSolver(0.5).solve(t, need_derivative=True)
+    for i, lf in enumerate(t.sorted_leaves()):
+        for k in ("phi", "gx", "gy", "gz", "dphi_dt"):
+            assert np.array_equal(field[lf.path][k], g[f"full_{k}"][i]), (i, k)
