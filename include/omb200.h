@@ -169,6 +169,10 @@ int omb_fmm_downward(const long long *parents, int np, const long long *children
                      void *stream);
 int omb_fmm_fields(const double *L, const long long *cell_base, int nleaf, double *phi, double *gx, double *gy,
                    double *gz, void *stream);
+/* rho_dot = -div(momentum) (gravity/solver.py:156-168) of the batch's first nleaf leaves of a [6][fstride]
+ * state, the neighbour cells gathered like the stage kernel's halo (info = the batch's OmbLeafInfo) */
+int omb_fmm_rhodot(const double *u, long long fstride, const OmbLeafInfo *info, int bc, int nleaf, double *out,
+                   void *stream);
 const char *omb_fmm_last_error(void);
 
 #ifdef __cplusplus

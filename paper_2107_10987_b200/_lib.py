@@ -20,7 +20,7 @@ EXPORTS = ("omb_abi_version", "omb_last_error", "omb_stage_smem_bytes", "omb_pri
            "omb_reflux_update", "omb_leaf_sums", "omb_disk_order",
            "omb_gather_rows", "omb_scatter_rows",
            "omb_fmm_traverse", "omb_fmm_masses", "omb_fmm_upward", "omb_fmm_m2l", "omb_fmm_downward",
-           "omb_fmm_fields", "omb_fmm_last_error")
+           "omb_fmm_fields", "omb_fmm_rhodot", "omb_fmm_last_error")
 
 
 def load():
@@ -59,6 +59,7 @@ def load():
     L.omb_fmm_m2l.argtypes = [vp, vp, vp, vp, vp, vp, ll, vp, vp]
     L.omb_fmm_downward.argtypes = [vp, i, vp, vp, vp, vp]
     L.omb_fmm_fields.argtypes = [vp, vp, i, vp, vp, vp, vp, vp]
+    L.omb_fmm_rhodot.argtypes = [vp, ll, vp, i, i, vp, vp]
     L.omb_reflux_update.argtypes = [ctypes.POINTER(OmbRefluxDesc), vp]
     for fn in EXPORTS[3:]:
         getattr(L, fn).restype = i

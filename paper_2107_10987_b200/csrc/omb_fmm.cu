@@ -30,6 +30,7 @@
 #include <vector>
 
 #include "../../include/omb200.h"
+#include "omb_stage.cuh"
 
 namespace {
 
@@ -223,6 +224,32 @@ __global__ void k_fmm_fields(const double* L, const long long* cell_base, int nl
   gz[i] = -l[3];
 }
 
+// rho_dot = -div(momentum) by central differences over the ghost-filled
+// state (gravity/solver.py:156-168): neighbour cells across leaf faces come
+// from the same gather as the hydro halo (same-level / virtual AMR leaves,
+// physical walls with the normal momentum mirrored), i.e. what the
+// reference's ghost fill puts there before the gravity solve (step.py:106-113)
+__global__ void k_fmm_rhodot(const double* U, long long fstride, const omb::LeafInfo* info, int bc, int nleaf,
+                             double* out) {
+  long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (i >= (long long)nleaf * 512) return;
+  int leaf = (int)(i / 512), c = (int)(i % 512);
+  int x = c / 64, y = (c / 8) % 8, z = c % 8;
+  const omb::LeafInfo& LI = info[leaf];
+  auto mom = [&](int comp, int cx, int cy, int cz) {  // padded coords
+    int fm;
+    long long a = omb::gather_addr(LI, bc, cx, cy, cz, fm);
+    double v = U[(long long)comp * fstride + a];
+    return ((fm >> (comp - 1)) & 1) ? -v : v;
+  };
+  int px = x + 3, py = y + 3, pz = z + 3;
+  double dsx = mom(1, px + 1, py, pz) - mom(1, px - 1, py, pz);
+  double dsy = mom(2, px, py + 1, pz) - mom(2, px, py - 1, pz);
+  double dsz = mom(3, px, py, pz + 1) - mom(3, px, py, pz - 1);
+  double inv2dx = 1.0 / (2.0 * LI.dx);
+  out[i] = -((dsx + dsy) + dsz) * inv2dx;
+}
+
 thread_local std::string f_err;
 int ferr(const char* what, cudaError_t e) {
   f_err = std::string(what) + ": " + cudaGetErrorString(e);
@@ -343,6 +370,16 @@ int omb_fmm_fields(const double* L, const long long* cell_base, int nleaf, doubl
   k_fmm_fields<<<(unsigned)((n + 255) / 256), 256, 0, (cudaStream_t)stream>>>(L, cell_base, nleaf, phi, gx, gy, gz);
   cudaError_t e = cudaGetLastError();
   return e == cudaSuccess ? 0 : ferr("omb_fmm_fields", e);
+}
+
+int omb_fmm_rhodot(const double* U, long long fstride, const OmbLeafInfo* info, int bc, int nleaf, double* out,
+                   void* stream) {
+  long long n = (long long)nleaf * 512;
+  if (n == 0) return 0;
+  k_fmm_rhodot<<<(unsigned)((n + 255) / 256), 256, 0, (cudaStream_t)stream>>>(U, fstride, (const omb::LeafInfo*)info,
+                                                                              bc, nleaf, out);
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? 0 : ferr("omb_fmm_rhodot", e);
 }
 
 }  // extern "C"

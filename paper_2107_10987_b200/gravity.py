@@ -248,6 +248,7 @@ class B200FmmSolver:
         parents = {int(L): np.nonzero((lv == L) & ~t.is_cell)[0].astype(np.int64) for L in np.unique(lv)}
         self._up = [(L, T.from_numpy(parents[L]).to(dev)) for L in sorted(parents, reverse=True) if len(parents[L])]
         self._down = [(L, T.from_numpy(parents[L]).to(dev)) for L in sorted(parents) if len(parents[L])]
+        self._dx3_dev = T.tensor([lf.subgrid.dx ** 3 for lf in tree.sorted_leaves()], dtype=T.float64, device=dev)
         self._M = T.zeros(t.nentities * NCOMP, dtype=T.float64, device=dev)
         self._L = T.zeros_like(self._M)
         self._signature = sig
@@ -282,13 +283,29 @@ class B200FmmSolver:
                                            ptr(o[3]), stream_handle(stream)), "omb_fmm_fields")
         return o[:, :n]
 
-    # -- the reference's host API ----------------------------------------------
-    def _dx3(self, tree):
+    def stage_fields(self, U, fstride, info, bc, nleaf, grav, stream=None):
+        """The stepper's per-stage solve (solver.py:134-153 on device data):
+        gx, gy, gz of the density and dphi/dt (the potential of -div(momentum))
+        of the [6][fstride] state U into grav ([4][fstride]: gx gy gz dphi_dt)."""
         import torch
 
-        return torch.tensor([lf.subgrid.dx ** 3 for lf in tree.sorted_leaves()], dtype=torch.float64,
-                            device=self.dev)
+        if not hasattr(self, "_dx3_dev") or self._dx3_dev.numel() != nleaf:
+            raise RuntimeError("stage_fields before prepare() of the stepper's tree")
+        lib, sh = self.lib, stream_handle(stream)
+        n = nleaf * 512
+        if getattr(self, "_scratch", None) is None or self._scratch.numel() < 2 * n:
+            self._scratch = torch.empty(2 * n, dtype=torch.float64, device=self.dev)
+        phi, rhodot = self._scratch[:n], self._scratch[n:2 * n]
+        G = grav.reshape(4, -1)
+        self._run(U[:n], self._dx3_dev, stream)
+        _lib.check(lib.omb_fmm_fields(ptr(self._L), ptr(self._cell_base), nleaf, ptr(phi), ptr(G[0]), ptr(G[1]),
+                                      ptr(G[2]), sh), "omb_fmm_fields")
+        _lib.check(lib.omb_fmm_rhodot(ptr(U), fstride, ptr(info), bc, nleaf, ptr(rhodot), sh), "omb_fmm_rhodot")
+        self._run(rhodot, self._dx3_dev, stream)
+        _lib.check(lib.omb_fmm_fields(ptr(self._L), ptr(self._cell_base), nleaf, ptr(G[3]), ptr(phi), ptr(phi),
+                                      ptr(phi), sh), "omb_fmm_fields")
 
+    # -- the reference's host API ----------------------------------------------
     def solve_density(self, tree, per_leaf_density=None):
         """(phi, g) keyed by leaf path, from the current density (or a
         replacement per-leaf source), as solver.py:117-132."""
@@ -302,7 +319,7 @@ class B200FmmSolver:
             src = lf.subgrid.interior[0] if per_leaf_density is None else per_leaf_density[lf.path]
             rho[i] = np.asarray(src, dtype=np.float64).reshape(-1)
         out = torch.empty(4 * len(leaves) * 512, dtype=torch.float64, device=self.dev)
-        f = self.fields_device(torch.from_numpy(rho.reshape(-1)).to(self.dev), self._dx3(tree), out).cpu().numpy()
+        f = self.fields_device(torch.from_numpy(rho.reshape(-1)).to(self.dev), self._dx3_dev, out).cpu().numpy()
         f = f.reshape(4, len(leaves), n, n, n)
         out_phi, out_g = {}, {}
         for i, lf in enumerate(leaves):

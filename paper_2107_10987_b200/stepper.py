@@ -89,6 +89,15 @@ class B200HydroStepper:
         self._roff = T.from_numpy(b.reflux_off.copy()).to(dev) if len(b.reflux_leaf) else None
         self._rtasks = T.from_numpy(b.reflux_tasks.reshape(-1).copy()).to(dev) if len(b.reflux_leaf) else None
         self._grav = None
+        from .gravity import B200FmmSolver
+
+        # a device FMM (gravity.B200FmmSolver) is solved on the device every stage, in place
+        self._dev_gravity = isinstance(gravity, B200FmmSolver)
+        if self._dev_gravity:
+            if partition is not None:
+                raise NotImplementedError("the device FMM runs on one GPU (the whole tree's moments)")
+            gravity.prepare(tree)
+            self._grav = T.zeros(4 * b.fstride, dtype=T.float64, device=dev)
         self._fresh = False  # device state was just uploaded from the host by cfl_dt
         self.dx_min = float(min(lf.subgrid.dx for lf in tree.leaves()))
         self.nglobal = partition.G if partition is not None else b.L
@@ -240,7 +249,10 @@ class B200HydroStepper:
         cur = self._state
         others = [i for i in range(4) if i != self._state]
         for s, (a, bw) in enumerate(SSP_RK3_STAGES):
-            if self.gravity is not None:
+            nxt = others[s]
+            if self._dev_gravity:
+                pass  # solved on the device below, after the AMR ghost regions are filled
+            elif self.gravity is not None:
                 # the reference re-solves gravity every stage (step.py:111-113); a solver that
                 # returns the same field object again (fixed gravity) is uploaded only once
                 fields = self.gravity.solve(self.tree, need_derivative=True)
@@ -254,6 +266,11 @@ class B200HydroStepper:
                 ad = OmbAmrDesc(u=ptr(self._buf[cur]), fstride=self.batch.fstride, tasks=ptr(self._amr_tasks),
                                 ntasks=self.batch.nvirtual)
                 _lib.check(self.lib.omb_amr_ghosts(ctypes.byref(ad), sh), "omb_amr_ghosts")
+            if self._dev_gravity:
+                # device FMM on this stage's state (the reference's order: ghost fill, then
+                # gravity, then reconstruction -- step.py:106-113)
+                self.gravity.stage_fields(self._buf[cur], self.batch.fstride, self._info, self.batch.bc,
+                                          self.batch.L, self._grav, stream)
             d = self._stage_desc(cur, nxt, s, a, bw)
             if events is not None:
                 events[s][0].record()

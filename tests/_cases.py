@@ -55,6 +55,8 @@ def case_tree(name):
         t.reindex()
     elif name == "amr_sedov_small":
         t = problems.amr_sedov_tree(base_level=2, max_level=4, radii={2: 0.6, 3: 0.35}, eos=EOS)
+    elif name == "gravity_step":
+        t = mesh.build_uniform_tree(1, 8, boundary="reflecting")
     elif name == "sources":
         t = mesh.build_uniform_tree(1, 8, boundary="outflow")
     else:

@@ -317,9 +317,20 @@ def fmm_case():
     save("fmm", **out)
 
 
+def gravity_step_case():
+    """Self-gravitating hydro: HydroStepper with the FMM re-solved every stage
+    (step.py:111-113), rotating frame, reflecting walls, 2 steps."""
+    from octomini.gravity import FmmSolver
+
+    tree = build_uniform_tree(1, 8, boundary="reflecting")
+    random_smooth(tree, seed=9)
+    step_case("gravity_step", tree, steps=2, gravity=FmmSolver(0.5), omega=0.3)
+
+
 def main():
     if sys.argv[1:] == ["fmm"]:
         fmm_case()
+        gravity_step_case()
         return
     checkpoint_case()
     amr_sedov_case()
@@ -348,6 +359,7 @@ def main():
     step_case("amr_reflux", t, steps=2)
     sources_case()
     fmm_case()
+    gravity_step_case()
 
 
 if __name__ == "__main__":

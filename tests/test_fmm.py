@@ -84,3 +84,30 @@ def test_device_fmm_full_solve_with_dphi_dt():
     for i, lf in enumerate(t.sorted_leaves()):
         for k in ("phi", "gx", "gy", "gz", "dphi_dt"):
             assert np.array_equal(field[lf.path][k], g[f"full_{k}"][i]), (i, k)
+
+
+@pytest.mark.gpu
+def test_self_gravitating_steps_match_reference():
+    """HydroStepper + FmmSolver re-solved every stage (step.py:111-113) vs
+    B200HydroStepper + B200FmmSolver solved on the device from the stage
+    state: 2 RK3 steps, rotating frame, reflecting walls."""
+    from _cases import EOS, case_tree, state_of
+
+    from paper_2107_10987_b200 import HydroMode
+    from paper_2107_10987_b200.stepper import B200HydroStepper
+
+    t, g = case_tree("gravity_step")
+    st = B200HydroStepper(t, EOS, HydroMode("new"), gravity=gravity.B200FmmSolver(0.5), omega=0.3)
+    for s in range(2):
+        dt = st.cfl_dt(0.4)
+        assert dt == float(g["dts"][s])
+        stats = st.rk3_step(dt)
+        assert stats.amax == float(g["amax"][s])
+        if s == 0:
+            got, ref = state_of(t), g["state1"]
+            assert np.count_nonzero(got[:, :5] != ref[:, :5]) == 0
+            assert np.all(np.abs(got - ref) <= 1e-12 * np.abs(ref))
+    # after 2 steps: rho, momenta, E bitwise; tau (CUDA pow vs glibc pow, 1 ulp) within 1e-12
+    got, ref = state_of(t), g["final"]
+    assert np.count_nonzero(got[:, :5] != ref[:, :5]) == 0
+    assert np.all(np.abs(got - ref) <= 1e-12 * np.abs(ref))
