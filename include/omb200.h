@@ -158,6 +158,10 @@ int omb_gather(const double *u, long long fstride, const OmbLeafInfo *info, int 
 long long omb_fmm_traverse(const double *center, const double *width, const long long *children,
                            const unsigned char *is_cell, long long nent, long long root, double theta,
                            long long *pa, long long *pb, long long *pk, long long cap);
+/* grouping + per-target contribution lists (HOST, O(pairs)) of a traversal: see omb_fmm.cu */
+long long omb_fmm_build(const long long *pa, const long long *pb, const long long *pk, long long np, long long nent,
+                        long long *group_first, unsigned char *group_flags, long long gcap, long long *off,
+                        unsigned long long *contrib);
 int omb_fmm_masses(const double *rho, const long long *cell_base, int nleaf, const double *dx3, double *M,
                    void *stream);
 int omb_fmm_upward(const long long *parents, int np, const long long *children, const double *center, double *M,

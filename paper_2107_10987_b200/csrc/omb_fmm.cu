@@ -26,7 +26,9 @@
 #include <stdlib.h>
 #include <string.h>
 
+#include <algorithm>
 #include <string>
+#include <unordered_map>
 #include <vector>
 
 #include "../../include/omb200.h"
@@ -326,6 +328,60 @@ long long omb_fmm_traverse(const double* center, const double* width, const long
     pn++;
   }
   return pn <= cap ? pn : -pn;
+}
+
+// Grouping + per-target contribution lists (host), O(pairs): groups are the
+// sorted distinct keys (np.unique order), pairs keep their discovery order
+// within a group (the stable argsort of _core.pyx:476-481), and each target's
+// contributions follow the global M2L sequence -- group by group, pair by
+// pair, (b <- a, D) before (a <- b, flipped D) (_core.pyx:583-608).
+// Outputs: ngroups, group_first [G] (discovery index of the group's first
+// pair, for R), group_flags [G] (2*a_cell + b_cell), off [nent+1] (CSR over
+// ALL entities), contrib [2*np] (source | group << 40 | flip << 63).
+// Returns G, or -1 if G exceeds gcap.
+long long omb_fmm_build(const long long* pa, const long long* pb, const long long* pk, long long np, long long nent,
+                        long long* group_first, unsigned char* group_flags, long long gcap, long long* off,
+                        unsigned long long* contrib) {
+  std::unordered_map<long long, long long> first;  // key -> first discovery index
+  first.reserve(4096);
+  for (long long i = 0; i < np; i++) first.emplace(pk[i], i);
+  std::vector<long long> keys;
+  keys.reserve(first.size());
+  for (auto& kv : first) keys.push_back(kv.first);
+  std::sort(keys.begin(), keys.end());
+  long long G = (long long)keys.size();
+  if (G > gcap) return -1;
+  std::unordered_map<long long, long long> gid;
+  gid.reserve(2 * G);
+  for (long long g = 0; g < G; g++) {
+    gid[keys[g]] = g;
+    group_first[g] = first[keys[g]];
+    group_flags[g] = (unsigned char)(keys[g] & 3);
+  }
+  // pairs bucketed by group, stable
+  std::vector<long long> pg(np), gstart(G + 1, 0);
+  for (long long i = 0; i < np; i++) {
+    pg[i] = gid[pk[i]];
+    gstart[pg[i] + 1]++;
+  }
+  for (long long g = 0; g < G; g++) gstart[g + 1] += gstart[g];
+  std::vector<long long> order(np), fill(gstart.begin(), gstart.end() - 1);
+  for (long long i = 0; i < np; i++) order[fill[pg[i]]++] = i;
+  // per-target counts, then the lists in global sequence order
+  for (long long e = 0; e <= nent; e++) off[e] = 0;
+  for (long long i = 0; i < np; i++) {
+    off[pb[i] + 1]++;
+    off[pa[i] + 1]++;
+  }
+  for (long long e = 0; e < nent; e++) off[e + 1] += off[e];
+  std::vector<long long> pos(off, off + nent);
+  for (long long r = 0; r < np; r++) {
+    long long i = order[r];
+    unsigned long long g = (unsigned long long)pg[i];
+    contrib[pos[pb[i]]++] = (unsigned long long)pa[i] | (g << 40);
+    contrib[pos[pa[i]]++] = (unsigned long long)pb[i] | (g << 40) | (1ull << 63);
+  }
+  return G;
 }
 
 int omb_fmm_masses(const double* rho, const long long* cell_base, int nleaf, const double* dx3, double* M,

@@ -210,30 +210,29 @@ class B200FmmSolver:
         t = EntityTable(tree)
         self.table = t
         pa, pb, pk = traverse(self.lib, t, self.theta)
-        order, bounds, R, a_cell, b_cell = group_pairs(t, pa, pb, pk)
-        G = len(R)
-        self.stats["groups"] = int(G)
+        # groups (sorted keys) and per-target contribution lists in the global M2L order (C++, O(pairs))
+        gcap = 1 << 22
+        gfirst = np.empty(gcap, dtype=np.int64)
+        gflags = np.empty(gcap, dtype=np.uint8)
+        off = np.empty(t.nentities + 1, dtype=np.int64)
+        contrib = np.empty(2 * len(pa), dtype=np.uint64)
+        G = int(self.lib.omb_fmm_build(pa.ctypes.data, pb.ctypes.data, pk.ctypes.data, len(pa), t.nentities,
+                                       gfirst.ctypes.data, gflags.ctypes.data, gcap, off.ctypes.data,
+                                       contrib.ctypes.data))
+        if G < 0:
+            raise RuntimeError("FMM: too many interaction groups")
+        R = t.center[pb[gfirst[:G]]] - t.center[pa[gfirst[:G]]]
+        a_cell, b_cell = (gflags[:G] & 2) != 0, (gflags[:G] & 1) != 0
+        self.stats["groups"] = G
         self.stats["pairs"] = int(len(pa))
         D = np.empty((G, 2, NCOMP))
         for g in range(G):
             D[g, 0] = kernel_derivatives(R[g])
             D[g, 1] = flip_derivatives(D[g, 0])
-        grp = np.repeat(np.arange(G, dtype=np.int64), np.diff(bounds))  # group of each ordered pair
-        a_o, b_o = pa[order], pb[order]
-        # global contribution sequence: pair by pair, (target b <- a, D) then (target a <- b, Df)
-        tgt = np.empty(2 * len(order), dtype=np.int64)
-        src = np.empty_like(tgt)
-        flip = np.zeros(2 * len(order), dtype=np.uint64)
-        tgt[0::2], tgt[1::2] = b_o, a_o
-        src[0::2], src[1::2] = a_o, b_o
-        flip[1::2] = 1
-        g2 = np.repeat(grp, 2)
-        seq = np.argsort(tgt, kind="stable")  # per target, in the global order
-        tgt_s = tgt[seq]
-        targets, starts = np.unique(tgt_s, return_index=True)
-        off = np.append(starts, len(tgt_s)).astype(np.int64)
-        contrib = (src[seq].astype(np.uint64) | (g2[seq].astype(np.uint64) << np.uint64(40)) |
-                   (flip[seq] << np.uint64(63)))
+        cnt = np.diff(off)
+        targets = np.nonzero(cnt)[0].astype(np.int64)
+        off = np.append(off[targets], off[-1]).astype(np.int64)  # CSR over the targets with contributions
+        del pa, pb, pk
         dev = self.dev
         T = torch
         self._center = T.from_numpy(np.ascontiguousarray(t.center).reshape(-1)).to(dev)
