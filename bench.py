@@ -52,9 +52,11 @@ def parse():
     p.add_argument("--e2e-steps", type=int, default=8)
     p.add_argument("--cpu-leaves", type=int, default=512)
     p.add_argument("--no-cpu-baseline", action="store_true")
-    p.add_argument("--config", default=None, choices=["c2", "c3", "c4", "c5"],
+    p.add_argument("--config", default=None, choices=["c2", "c3", "c4", "c5", "c5g"],
                    help="c2: uniform 128^3 (N=1 default); c3: uniform 256^3 (N>1 default); c4: AMR Sedov, "
-                        "levels 3-6; c5: rotating polytrope stand-in, fixed gravity, 128^3")
+                        "levels 3-6; c5: rotating polytrope stand-in, fixed gravity, 128^3; c5g: the same star "
+                        "self-gravitating (device FMM re-solved every stage, theta 0.5; --level sets the tree, "
+                        "default 4 = 128^3)")
     return p.parse_args()
 
 
@@ -71,7 +73,7 @@ def sedov_tree(level):
 
 
 def resolve_level(args, world):
-    if args.config in ("c4", "c5"):
+    if args.config in ("c4", "c5", "c5g"):
         return args.config
     if args.config == "c3":
         return 5
@@ -84,6 +86,10 @@ def workload_name(level, nleaves):
     if level == "c5":
         return ("star_uniform_L4_n8 (config c5 stand-in: closed-form n=1 polytrope, rotating frame, fixed "
                 "self-gravity, rho floor 1e-4, outflow, gamma 5/3)")
+    if level == "c5g":
+        return ("star_uniform_n8 self-gravitating (config c5: closed-form rotating n=1 polytrope, floors, outflow, "
+                "gamma 5/3; gravity = device FMM theta 0.5 re-solved every stage from the stage state, phi/g and "
+                "dphi/dt, as HydroStepper + FmmSolver)")
     if level == "c4":
         return f"sedov_amr_L3-6_n8 (config c4): {nleaves} sub-grids of 8^3 on levels 3-6 (SURVEY.md 8d construction)"
     return f"sedov_uniform_L{level}_n8"
@@ -255,6 +261,14 @@ def gpu_arm(args, rank, world):
 
         tree, eos, grav, om, fl = synthetic_star(level=4)
         extra = dict(gravity=grav, omega=om, floors=fl)
+    elif level == "c5g":
+        from paper_2107_10987_b200.gravity import B200FmmSolver
+        from paper_2107_10987_b200.problems import synthetic_star
+
+        if world > 1:
+            raise SystemExit("c5g (device FMM) runs on one GPU")
+        tree, eos, _, om, fl = synthetic_star(level=args.level or 4)
+        extra = dict(gravity=B200FmmSolver(0.5), omega=om, floors=fl)
     else:
         tree = sedov_tree(level)
         eos = EosConfig(gamma=1.4)
@@ -263,8 +277,10 @@ def gpu_arm(args, rank, world):
 
     if world > 1:
         part = Partition(tree, world, rank)
+    t_prep = time.perf_counter()
     st = B200HydroStepper(tree, eos, HydroMode("new"), host_sync=False, max_run=args.max_run, partition=part,
                           **extra)
+    t_prep = time.perf_counter() - t_prep
     lib = _lib.load()
     cells = st.nglobal * 512  # whole job
     local_cells = st.batch.ncompute * 512
@@ -312,6 +328,20 @@ def gpu_arm(args, rank, world):
     aborted = bool(np.any(ratio > 1.0))
     info = {"nglobal": st.nglobal, "nruns": st.batch.nruns, "L": st.batch.L, "ncompute": st.batch.ncompute,
             "launches": st.native_launches_per_step()}
+    fmm = None
+    if level == "c5g":  # the per-stage FMM solve on its own (density + dphi/dt), CUDA events
+        fs = st.gravity
+        f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        f0.record()
+        for _ in range(3):
+            fs.stage_fields(st._buf[st._state], st.batch.fstride, st._info, st.batch.bc, st.batch.L, st._grav)
+        f1.record()
+        torch.cuda.synchronize()
+        fmm_ms = f0.elapsed_time(f1) / 3
+        fmm = {"stage_ms": fmm_ms, "solves_per_stage": 2, "pairs": fs.stats["pairs"], "groups": fs.stats["groups"],
+               "entities": int(fs.table.nentities), "theta": fs.theta,
+               "interactions_per_s": 2 * 2 * fs.stats["pairs"] / (fmm_ms / 1e3),
+               "prepare_s_host": t_prep, "share_of_step": 3 * fmm_ms / (ms / K)}
     # free the host tree and device buffers before the e2e / non-flat trees (c3 at 8 ranks:
     # 4.3 GB of host leaves per rank per tree)
     del st, tree, part
@@ -327,6 +357,9 @@ def gpu_arm(args, rank, world):
         if level == "c5":
             t2, _, g2, om2, fl2 = synthetic_star(level=4)
             extra2 = dict(gravity=g2, omega=om2, floors=fl2)
+        elif level == "c5g":  # same topology: the FMM preparation is reused
+            t2, _, _, om2, fl2 = synthetic_star(level=args.level or 4)
+            extra2 = dict(gravity=extra["gravity"], omega=om2, floors=fl2)
         else:
             t2 = sedov_tree(level)
         p2 = Partition(t2, world, rank) if world > 1 else None
@@ -421,9 +454,10 @@ def gpu_arm(args, rank, world):
         "e2e": e2e,
         "nontrivial_state": nontrivial,
         "gpu_launches": K * info["launches"],
+        "fmm": fmm,
         "cfl_abort_in_timed_steps": aborted,
     }
-    if not args.no_cpu_baseline and world == 1:
+    if not args.no_cpu_baseline and world == 1 and level != "c5g":
         v, nthr, sample, _ = cpu_run(level, min(args.cpu_leaves, info["L"]), 1, 0)
         line["cpu_baseline"] = {"value": v, "unit": UNIT, "cores": nthr, "kind": "port", "sample": sample}
     emit(line)

@@ -282,6 +282,11 @@ class B200FmmSolver:
                                            ptr(o[3]), stream_handle(stream)), "omb_fmm_fields")
         return o[:, :n]
 
+    def launches_per_stage(self):
+        """Kernels of one stage_fields call: 2 solves x (masses, upward levels, M2L,
+        downward levels, fields) + the -div(momentum) source."""
+        return 2 * (3 + len(self._up) + len(self._down)) + 1
+
     def stage_fields(self, U, fstride, info, bc, nleaf, grav, stream=None):
         """The stepper's per-stage solve (solver.py:134-153 on device data):
         gx, gy, gz of the density and dphi/dt (the potential of -div(momentum))

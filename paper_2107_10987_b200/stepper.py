@@ -299,6 +299,8 @@ class B200HydroStepper:
             if getattr(self, "_fsend", None) is not None:
                 per += int(sum(p.flux_send_counts) > 0) + int(sum(p.flux_recv_counts) > 0)
         per += int(self._amr_tasks is not None) + int(self._rleaf is not None)
+        if self._dev_gravity:
+            per += self.gravity.launches_per_stage()
         return 2 + 3 * per
 
     def _reduce_stats(self):
