@@ -37,6 +37,9 @@
 namespace {
 
 constexpr int NC = 20;  // [M0, M1(3), M2(6), M3(10)]
+#ifndef FMM_M2L_MINB
+#define FMM_M2L_MINB 2  // 255 registers; capping them (more warps, spills) was slower
+#endif
 // symmetric tensor component tables (multipole.py:21-42)
 __constant__ int c_s2a[6] = {0, 0, 0, 1, 1, 2};
 __constant__ int c_s2b[6] = {0, 1, 2, 1, 2, 2};
@@ -131,7 +134,7 @@ __device__ void m2l_add(const double* M, const double* D, double* L) {
 }
 
 // contribution word: source entity (bits 0..39) | group (40..62) | flip (63)
-__global__ void k_fmm_m2l(const long long* off, const unsigned long long* contrib, const double* D /*[G][2][20]*/,
+__global__ void __launch_bounds__(128, FMM_M2L_MINB) k_fmm_m2l(const long long* off, const unsigned long long* contrib, const double* D /*[G][2][20]*/,
                           const unsigned char* cellcell, const double* M, double* L, long long ntarget,
                           const long long* targets) {
   long long ti = blockIdx.x * (long long)blockDim.x + threadIdx.x;
