@@ -37,9 +37,6 @@
 namespace {
 
 constexpr int NC = 20;  // [M0, M1(3), M2(6), M3(10)]
-#ifndef FMM_M2L_MINB
-#define FMM_M2L_MINB 2  // 255 registers; capping them (more warps, spills) was slower
-#endif
 // symmetric tensor component tables (multipole.py:21-42)
 __constant__ int c_s2a[6] = {0, 0, 0, 1, 1, 2};
 __constant__ int c_s2b[6] = {0, 1, 2, 1, 2, 2};
@@ -112,53 +109,78 @@ __global__ void k_fmm_upward(const long long* parents, int np, const long long* 
 // ---------------------------------------------------------------------------
 // M2L: L[x] += contributions in the reference's order (_core.pyx:534-608)
 // ---------------------------------------------------------------------------
-__device__ void m2l_add(const double* M, const double* D, double* L) {
-  double M0 = M[0];
-  double acc = D[0] * M0;
-  for (int a = 0; a < 3; a++) acc = acc - D[1 + a] * M[1 + a];
-  for (int i = 0; i < 6; i++) acc = acc + ((0.5 * c_mult2[i]) * D[4 + i]) * M[4 + i];
-  for (int i = 0; i < 10; i++) acc = acc - ((c_mult3[i] / 6.0) * D[10 + i]) * M[10 + i];
-  L[0] += acc;
-  for (int a = 0; a < 3; a++) {
-    acc = D[1 + a] * M0;
-    for (int b = 0; b < 3; b++) acc = acc - D[4 + idx2(a, b)] * M[1 + b];
-    for (int i = 0; i < 6; i++) acc = acc + ((0.5 * c_mult2[i]) * D[10 + idx3(a, c_s2a[i], c_s2b[i])]) * M[4 + i];
-    L[1 + a] += acc;
-  }
-  for (int i = 0; i < 6; i++) {
-    acc = D[4 + i] * M0;
-    for (int b = 0; b < 3; b++) acc = acc - D[10 + idx3(c_s2a[i], c_s2b[i], b)] * M[1 + b];
-    L[4 + i] += acc;
-  }
-  for (int i = 0; i < 10; i++) L[10 + i] += D[10 + i] * M0;
-}
-
 // contribution word: source entity (bits 0..39) | group (40..62) | flip (63)
-__global__ void __launch_bounds__(128, FMM_M2L_MINB) k_fmm_m2l(const long long* off, const unsigned long long* contrib, const double* D /*[G][2][20]*/,
-                          const unsigned char* cellcell, const double* M, double* L, long long ntarget,
-                          const long long* targets) {
+//
+// Two passes over each target's contributions, each owning a subset of the
+// 20 local components (every component still accumulates its contributions
+// in the reference's order, so the split is exact): PART 0 = L0..L3 (needs
+// all of M and D), PART 1 = L4..L19 (needs M0..M3 and D4..D19).  Fewer live
+// accumulators per pass: 128 registers, twice the warps of the fused pass
+// against the latency of the source-moment loads.
+template <int PART>
+__global__ void __launch_bounds__(128, 4) k_fmm_m2l(const long long* off, const unsigned long long* contrib,
+                                                    const double* D /*[G][2][20]*/, const unsigned char* cellcell,
+                                                    const double* M, double* L, long long ntarget,
+                                                    const long long* targets) {
   long long ti = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   if (ti >= ntarget) return;
   long long x = targets[ti];
-  double l[NC];
-  for (int k = 0; k < NC; k++) l[k] = L[x * NC + k];
+  constexpr int K0 = PART == 0 ? 0 : 4, KN = PART == 0 ? 4 : 16;
+  double l[KN];
+#pragma unroll
+  for (int k = 0; k < KN; k++) l[k] = L[x * NC + K0 + k];
   for (long long q = off[ti]; q < off[ti + 1]; q++) {
-    unsigned long long w = contrib[q];
+    unsigned long long w = __ldg(contrib + q);
     long long src = (long long)(w & 0xFFFFFFFFFFull);
     long long g = (long long)((w >> 40) & 0x7FFFFFull);
     int flip = (int)(w >> 63);
     const double* Dg = D + (g * 2 + flip) * NC;
+    const double* Ms = M + src * NC;
     if (cellcell[g]) {
       // L[eb,0] += ma*D0; L[eb,c] += ma*D_c; L[ea,0] += mb*D0; L[ea,c] += mb*(-D_c)
       // (the flipped D holds -D_c: x*(-d) is the reference's mb*(-D1))
-      double m = M[src * NC];
-      l[0] += m * Dg[0];
-      for (int c = 0; c < 3; c++) l[1 + c] += m * Dg[1 + c];
+      if (PART == 0) {
+        double m = __ldg(Ms);
+        l[0] += m * __ldg(Dg);
+#pragma unroll
+        for (int c = 0; c < 3; c++) l[1 + c] += m * __ldg(Dg + 1 + c);
+      }
+      continue;
+    }
+    double M0 = __ldg(Ms);
+    if (PART == 0) {
+      double acc = __ldg(Dg) * M0;
+#pragma unroll
+      for (int a = 0; a < 3; a++) acc = acc - __ldg(Dg + 1 + a) * __ldg(Ms + 1 + a);
+#pragma unroll
+      for (int i = 0; i < 6; i++) acc = acc + ((0.5 * c_mult2[i]) * __ldg(Dg + 4 + i)) * __ldg(Ms + 4 + i);
+#pragma unroll
+      for (int i = 0; i < 10; i++) acc = acc - ((c_mult3[i] / 6.0) * __ldg(Dg + 10 + i)) * __ldg(Ms + 10 + i);
+      l[0] += acc;
+#pragma unroll
+      for (int a = 0; a < 3; a++) {
+        acc = __ldg(Dg + 1 + a) * M0;
+#pragma unroll
+        for (int b = 0; b < 3; b++) acc = acc - __ldg(Dg + 4 + idx2(a, b)) * __ldg(Ms + 1 + b);
+#pragma unroll
+        for (int i = 0; i < 6; i++)
+          acc = acc + ((0.5 * c_mult2[i]) * __ldg(Dg + 10 + idx3(a, c_s2a[i], c_s2b[i]))) * __ldg(Ms + 4 + i);
+        l[1 + a] += acc;
+      }
     } else {
-      m2l_add(M + src * NC, Dg, l);
+#pragma unroll
+      for (int i = 0; i < 6; i++) {
+        double acc = __ldg(Dg + 4 + i) * M0;
+#pragma unroll
+        for (int b = 0; b < 3; b++) acc = acc - __ldg(Dg + 10 + idx3(c_s2a[i], c_s2b[i], b)) * __ldg(Ms + 1 + b);
+        l[i] += acc;
+      }
+#pragma unroll
+      for (int i = 0; i < 10; i++) l[6 + i] += __ldg(Dg + 10 + i) * M0;
     }
   }
-  for (int k = 0; k < NC; k++) L[x * NC + k] = l[k];
+#pragma unroll
+  for (int k = 0; k < KN; k++) L[x * NC + K0 + k] = l[k];
 }
 
 // ---------------------------------------------------------------------------
@@ -408,8 +430,9 @@ int omb_fmm_m2l(const long long* off, const unsigned long long* contrib, const d
                 const unsigned char* cellcell, const double* M, double* L, long long ntarget, const long long* targets,
                 void* stream) {
   if (ntarget <= 0) return 0;
-  k_fmm_m2l<<<(unsigned)((ntarget + 127) / 128), 128, 0, (cudaStream_t)stream>>>(off, contrib, D, cellcell, M, L,
-                                                                                  ntarget, targets);
+  unsigned nb = (unsigned)((ntarget + 127) / 128);
+  k_fmm_m2l<0><<<nb, 128, 0, (cudaStream_t)stream>>>(off, contrib, D, cellcell, M, L, ntarget, targets);
+  k_fmm_m2l<1><<<nb, 128, 0, (cudaStream_t)stream>>>(off, contrib, D, cellcell, M, L, ntarget, targets);
   cudaError_t e = cudaGetLastError();
   return e == cudaSuccess ? 0 : ferr("omb_fmm_m2l", e);
 }
