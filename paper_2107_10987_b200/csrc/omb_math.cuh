@@ -120,7 +120,15 @@ OMB_HD void mono(double a, double& lv, double& hv) {
   double d2 = diff * diff;
   double q = d2 * (1.0 / 6.0);
   double band = 0x1p-49 * fabs(q) + 0x1p-1000;
-  if (!(fabs(dm - q) > band) || !(fabs(dm + q) > band)) q = d2 / 6.0;
+  if (!(fabs(dm - q) > band) || !(fabs(dm + q) > band)) {
+    double dd = d2;
+#ifdef __CUDA_ARCH__
+    // keep the exact division inside this rare branch: without the opaque
+    // copy the compiler speculates the IEEE division for every field
+    asm volatile("" : "+d"(dd));
+#endif
+    q = dd / 6.0;
+  }
   double nlv = lv, nhv = hv;
   if (dm > q) nlv = 3.0 * a - 2.0 * hv;
   if (-q > dm) nhv = 3.0 * a - 2.0 * nlv;
