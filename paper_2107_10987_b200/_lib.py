@@ -75,5 +75,8 @@ def load():
 
 def check(rc, what):
     if rc != 0:
-        msg = load().omb_last_error().decode(errors="replace")
+        L = load()
+        # the FMM passes (omb_fmm.cu) keep their own thread-local message
+        raw = L.omb_fmm_last_error() if what.startswith("omb_fmm") else L.omb_last_error()
+        msg = (raw or b"").decode(errors="replace")
         raise NativeError(f"{what} failed ({rc}): {msg}")
