@@ -16,15 +16,21 @@
 //       in the reference's deviation form and summation order
 //       (_core.pyx:310-346) and into boundary point values for y/z faces
 //   P3/P4  in-plane lines (1, 2, 7, 8): lo/hi and their fluxes
-//   P5  finish the y/z faces of plane X-1, start those of plane X
+//   P5  finish the y/z faces of plane X-1, start those of plane X -- run in
+//       the NEXT plane's P0 phase, beside the conversion
 //   P6  conservative update of plane X-2 + sources + dual-energy + floors
 //       (step.py:243-288), on the last 64 threads during the last P1 group
+// i.e. 7 barriers per plane: P0+P5 | P1A | P2A | P1B+P6 | P2B | P3 | P4.
 //
 // lo/hi and point fluxes never leave shared memory.  Every phase is a loop
 // over independent items separated by barriers; values a thread carries
-// across a barrier live in `Hold`.  The same code is compiled for the host
-// by the CPU emulation harness (tests/native), which runs each phase for
-// every thread index in turn.
+// across a barrier live in `Hold`.  The kernel is latency-bound per phase
+// (one item chain per thread, 16 warps per SM), so items are cut so that the
+// longest chain of a phase is short: independent parts of an item go to
+// threads that would idle, or one thread carries two independent chains
+// instead of two rounds (profiles/README.md).  The same code is compiled for
+// the host by the CPU emulation harness (tests/native), which runs each phase
+// for every thread index in turn in the kernel's barrier order.
 #pragma once
 #include "omb_math.cuh"
 
