@@ -23,7 +23,7 @@
 extern "C" {
 #endif
 
-#define OMB_ABI_VERSION 2
+#define OMB_ABI_VERSION 3
 
 /* per-leaf topology / geometry record (device array, one per leaf) */
 typedef struct {
@@ -58,6 +58,11 @@ typedef struct {
     unsigned long long *amax_bits;  /* device: running max of the signal speed (bits of a non-negative double) */
     unsigned long long *fallback;   /* device: running positivity-fallback count */
     double *flux;         /* face-flux export slots (AMR coarse/fine faces), may be NULL if no leaf exports */
+    /* multi-GPU, NVLink peer reads (replaces the halo exchange of ghosts.py:115-150 across ranks):
+     * halo[k] = address of the field-0 block of the leaf in halo slot nown + k inside its OWNER's
+     * stage-input buffer (CUDA IPC peer memory, same fstride on every rank); NULL: halo slots local */
+    const double *const *halo;
+    int nown;
 } OmbStageDesc;
 
 /* AMR ghost regions: each task fills, in the interior of a VIRTUAL leaf (batch index >= number of real
@@ -96,6 +101,12 @@ typedef struct {
 int omb_abi_version(void);
 const char *omb_last_error(void);
 int omb_stage_smem_bytes(void);
+/* multi-GPU NVLink halo reads: allocate (zeroed) device memory with its CUDA IPC handle (64 bytes), and
+ * open a peer's handle in the current device's context (lazy peer access) */
+int omb_ipc_alloc(long long bytes, void **ptr, void *handle64);
+int omb_ipc_open(const void *handle64, void **ptr);
+/* enable kernels of the current device to read peer_device's memory (multi-GPU NVLink halo reads) */
+int omb_enable_peer_access(int peer_device);
 
 int omb_primitives(const double *u, int m, double gamma, double eta, double *prim, void *stream);
 int omb_reconstruct(const double *prim, int m, int new_mode, int contact_on, double gamma,

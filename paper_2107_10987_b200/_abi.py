@@ -31,7 +31,7 @@ class OmbStageDesc(ctypes.Structure):
         ("floor_rho", ctypes.c_double), ("floor_tau", ctypes.c_double), ("floor_vmax", ctypes.c_double),
         ("bc", ctypes.c_int), ("new_mode", ctypes.c_int), ("override_center", ctypes.c_int),
         ("contact", ctypes.c_int), ("amax_bits", ctypes.c_void_p), ("fallback", ctypes.c_void_p),
-        ("flux", ctypes.c_void_p),
+        ("flux", ctypes.c_void_p), ("halo", ctypes.c_void_p), ("nown", ctypes.c_int),
     ]
 
 

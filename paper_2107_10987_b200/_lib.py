@@ -12,13 +12,13 @@ from .errors import NativeError
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 SO_PATH = os.environ.get("OMB_LIB_PATH") or os.path.join(_HERE, "libomb200.so")  # override: A/B experiments
-ABI_VERSION = 2
+ABI_VERSION = 3
 _lib = None
 
 EXPORTS = ("omb_abi_version", "omb_last_error", "omb_stage_smem_bytes", "omb_primitives", "omb_reconstruct",
            "omb_fluxes", "omb_stage", "omb_cfl", "omb_gather", "omb_fp64_peak", "omb_pack_leaves", "omb_unpack_leaves", "omb_selftest_div", "omb_host_pack", "omb_host_unpack", "omb_host_upload", "omb_host_download", "omb_amr_ghosts",
            "omb_reflux_update", "omb_leaf_sums", "omb_disk_order",
-           "omb_gather_rows", "omb_scatter_rows",
+           "omb_gather_rows", "omb_scatter_rows", "omb_enable_peer_access", "omb_ipc_alloc", "omb_ipc_open",
            "omb_fmm_traverse", "omb_fmm_build", "omb_fmm_masses", "omb_fmm_upward", "omb_fmm_m2l", "omb_fmm_downward",
            "omb_fmm_fields", "omb_fmm_rhodot", "omb_fmm_last_error")
 
@@ -53,6 +53,9 @@ def load():
     L.omb_disk_order.argtypes = [vp, ll, i, vp, vp]
     L.omb_gather_rows.argtypes = [vp, ll, vp, i, vp, vp]
     L.omb_scatter_rows.argtypes = [vp, ll, vp, i, vp, vp]
+    L.omb_enable_peer_access.argtypes = [i]
+    L.omb_ipc_alloc.argtypes = [ll, vp, vp]
+    L.omb_ipc_open.argtypes = [vp, vp]
     L.omb_fmm_traverse.argtypes = [vp, vp, vp, vp, ll, ll, ctypes.c_double, vp, vp, vp, ll]
     L.omb_fmm_build.argtypes = [vp, vp, vp, ll, ll, vp, vp, ll, vp, vp]
     L.omb_fmm_masses.argtypes = [vp, vp, i, vp, vp, vp]

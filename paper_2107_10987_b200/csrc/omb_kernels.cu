@@ -623,6 +623,41 @@ extern "C" {
 int omb_abi_version(void) { return OMB_ABI_VERSION; }
 const char* omb_last_error(void) { return g_err.c_str(); }
 int omb_stage_smem_bytes(void) { return Smem::BYTES; }
+
+// CUDA IPC for the multi-GPU halo reads: a rank allocates its state buffers
+// itself (so the IPC handle covers exactly them), peers open them in their
+// own device's context with lazy peer access
+int omb_ipc_alloc(long long bytes, void** ptr, void* handle64) {
+  if (int rc = lib_init()) return rc;
+  CK(cudaMalloc(ptr, (size_t)bytes), "omb_ipc_alloc cudaMalloc");
+  CK(cudaMemset(*ptr, 0, (size_t)bytes), "omb_ipc_alloc cudaMemset");
+  cudaIpcMemHandle_t h;
+  CK(cudaIpcGetMemHandle(&h, *ptr), "cudaIpcGetMemHandle");
+  memcpy(handle64, &h, sizeof(h));
+  return 0;
+}
+int omb_ipc_open(const void* handle64, void** ptr) {
+  cudaIpcMemHandle_t h;
+  memcpy(&h, handle64, sizeof(h));
+  CK(cudaIpcOpenMemHandle(ptr, h, cudaIpcMemLazyEnablePeerAccess), "cudaIpcOpenMemHandle");
+  return 0;
+}
+
+// let kernels of the current device read another device's memory (NVLink peer access)
+int omb_enable_peer_access(int peer_device) {
+  int cur = -1, ok = 0;
+  CK(cudaGetDevice(&cur), "cudaGetDevice");
+  if (peer_device == cur) return 0;
+  CK(cudaDeviceCanAccessPeer(&ok, cur, peer_device), "cudaDeviceCanAccessPeer");
+  if (!ok) return set_err("omb_enable_peer_access: no peer access between these devices");
+  cudaError_t e = cudaDeviceEnablePeerAccess(peer_device, 0);
+  if (e == cudaErrorPeerAccessAlreadyEnabled) {
+    cudaGetLastError();
+    return 0;
+  }
+  CK(e, "cudaDeviceEnablePeerAccess");
+  return 0;
+}
 #ifdef OMB_PHASE_PROF
 int omb_phase_prof(unsigned long long* out, int reset) {  // profiling build only
   cudaMemcpyFromSymbol(out, g_phase_cycles, sizeof(unsigned long long) * 16);
@@ -694,6 +729,8 @@ static StageArgs stage_args(const OmbStageDesc* d) {
   A.amax_bits = d->amax_bits;
   A.fallback = d->fallback;
   A.flux = d->flux;
+  A.halo = d->halo;
+  A.nown = d->nown;
   return A;
 }
 

@@ -203,6 +203,8 @@ struct StageArgs {
   unsigned long long* amax_bits;  // per-stage accumulators
   unsigned long long* fallback;
   double* flux;                   // face-flux export slots (AMR), or null
+  const double* const* halo;      // multi-GPU: halo slot k's block in its owner's buffer, or null
+  int nown;                       // first halo slot
 };
 
 // conserved state of padded cell c (local coords in [0,14)^3) of a leaf, as
@@ -329,8 +331,11 @@ struct Stage {
     for (int it = tid; it < PL; it += nthr) {
       int fm;
       long long base = gather_addr(LI, A.bc, lx, it / M, it % M, fm);
+      int src = (int)(base >> 9);
+      // a neighbour leaf owned by another GPU is read from its owner's buffer over NVLink
+      const double* p = (A.halo != nullptr && src >= A.nown) ? A.halo[src - A.nown] + (base & 511) : A.ucur + base;
 #pragma unroll
-      for (int v = 0; v < NF; v++) async_copy8(S + stage + v * PL + it, A.ucur + v * A.fstride + base);
+      for (int v = 0; v < NF; v++) async_copy8(S + stage + v * PL + it, p + v * A.fstride);
     }
   }
 

@@ -23,6 +23,8 @@ reference leaves it when it raises.
 """
 
 import ctypes
+import os
+import sys
 
 import numpy as np
 
@@ -32,6 +34,13 @@ from .batch import LeafBatch
 from .device import ptr, require_cuda, stream_handle, torch
 from .errors import NumericsError
 from .hydro import SSP_RK3_STAGES, FloorConfig, StepStats
+
+
+class _DeviceArray:
+    """A float64 device array by pointer, for torch.as_tensor (__cuda_array_interface__)."""
+
+    def __init__(self, ptr, n):
+        self.__cuda_array_interface__ = {"shape": (n,), "typestr": "<f8", "data": (ptr, False), "version": 3}
 
 
 class B200HydroStepper:
@@ -66,13 +75,30 @@ class B200HydroStepper:
         b = self.batch
         T = torch
         dev = self.dev
+        # multi-GPU halo: uniform partitions read neighbour leaves straight from their owners'
+        # buffers over NVLink (CUDA IPC, OmbStageDesc.halo); AMR partitions exchange with NCCL
+        self._p2p = (partition is not None and not partition.amr
+                     and os.environ.get("OMB_HALO", "p2p") == "p2p")
+        if self._p2p:
+            fs = T.tensor([b.fstride], dtype=T.int64, device=dev)
+            self.dist.all_reduce(fs, op=self.dist.ReduceOp.MAX, group=group)
+            b.fstride = int(fs.item())  # one field stride on every rank: peer addressing
         self._info = T.from_numpy(b.info.view(np.uint8).copy()).to(dev)
         self._run_off = T.from_numpy(b.run_off.copy()).to(dev)
         self._run_leaf = T.from_numpy(b.run_leaf.copy()).to(dev)
         self._dx = T.from_numpy(b.dx.copy()).to(dev)
         n = 6 * b.fstride
         # A: state / u0, B, C: stage 1, 2 outputs, D: stage 3 output
-        self._buf = [T.empty(n, dtype=T.float64, device=dev) for _ in range(4)]
+        if self._p2p:  # own allocations, shareable with the peer ranks (CUDA IPC)
+            self._buf, self._ipc = [], []
+            for _ in range(4):
+                p_ = ctypes.c_void_p()
+                h = ctypes.create_string_buffer(64)
+                _lib.check(self.lib.omb_ipc_alloc(8 * n, ctypes.byref(p_), h), "omb_ipc_alloc")
+                self._ipc.append(h.raw)
+                self._buf.append(T.as_tensor(_DeviceArray(p_.value, n), device=dev))
+        else:
+            self._buf = [T.empty(n, dtype=T.float64, device=dev) for _ in range(4)]
         self._state = 0
         self._dt = T.zeros(1, dtype=T.float64, device=dev)
         self._acc = T.zeros(6, dtype=T.int64, device=dev)  # amax bits x3, fallback x3
@@ -106,6 +132,16 @@ class B200HydroStepper:
             self._sendbuf = T.empty(max(1, sum(partition.send_counts)) * 3072, dtype=T.float64, device=dev)
             self._recvbuf = T.empty(max(1, sum(partition.recv_counts)) * 3072, dtype=T.float64, device=dev)
             self._gids = partition.gids
+            if self._p2p:
+                ok = 1
+                try:
+                    self._setup_p2p()
+                except Exception as e:  # noqa: BLE001 -- e.g. no peer access between the devices
+                    ok = 0
+                    sys.stderr.write(f"NVLink halo reads unavailable ({e}); exchanging with NCCL\n")
+                flag = torch.tensor([ok], dtype=torch.int64, device=dev)
+                self.dist.all_reduce(flag, op=self.dist.ReduceOp.MIN, group=group)
+                self._p2p = bool(flag.item())  # every rank takes the same path
             if partition.amr and (sum(partition.flux_send_counts) or sum(partition.flux_recv_counts)):
                 self._fsend = T.from_numpy(partition.flux_send_slots.copy()).to(dev)
                 self._frecv = T.from_numpy(partition.flux_recv_slots.copy()).to(dev)
@@ -151,6 +187,35 @@ class B200HydroStepper:
 
     def state_tensor(self):
         return self._buf[self._state]
+
+    # -- multi-GPU halo: NVLink peer reads ---------------------------------------------
+    def _setup_p2p(self):
+        """Open every rank's 4 state buffers (CUDA IPC through torch's storage sharing)
+        and build, per buffer index, the table of halo-leaf addresses in their owners'
+        buffers (the stage kernel reads them directly; no halo exchange)."""
+        p = self.part
+        world = p.world
+        allh = [None] * world
+        self.dist.all_gather_object(allh, self._ipc, group=self.group)
+        base = [[0] * 4 for _ in range(world)]
+        for r in range(world):
+            for i in range(4):
+                if r == p.rank:
+                    base[r][i] = self._buf[i].data_ptr()
+                else:
+                    q = ctypes.c_void_p()
+                    _lib.check(self.lib.omb_ipc_open(ctypes.create_string_buffer(allh[r][i], 64), ctypes.byref(q)),
+                               "omb_ipc_open")
+                    base[r][i] = q.value
+        halo = np.asarray(p.halo, dtype=np.int64)
+        owner = p.owner[halo]
+        local = halo - np.asarray(p.bounds, dtype=np.int64)[owner]  # the owner's leaf index
+        tab = np.zeros((4, max(1, len(halo))), dtype=np.uint64)
+        for i in range(4):
+            b_i = np.array([base[r][i] for r in range(world)], dtype=np.uint64)
+            tab[i, :len(halo)] = b_i[owner] + (local * 512 * 8).astype(np.uint64)
+        self._halo_tab = torch.from_numpy(tab.view(np.int64)).to(self.dev)
+        self._bar = torch.zeros(1, dtype=torch.float64, device=self.dev)
 
     # -- multi-GPU halo exchange ------------------------------------------------------
     def _exchange(self, buf_index, stream=None):
@@ -260,7 +325,12 @@ class B200HydroStepper:
                     self._grav = torch.from_numpy(self.batch.pack_gravity(fields).reshape(-1)).to(self.dev)
                     self._grav_src = fields
             nxt = others[s]
-            self._exchange(cur, stream)
+            if self._p2p:
+                # every rank has finished the previous stage (its output = this stage's input)
+                # before anyone reads it; also no rank writes a buffer a peer still reads
+                self.dist.all_reduce(self._bar, group=self.group)
+            else:
+                self._exchange(cur, stream)
             sh = stream_handle(stream)
             if self._amr_tasks is not None:
                 ad = OmbAmrDesc(u=ptr(self._buf[cur]), fstride=self.batch.fstride, tasks=ptr(self._amr_tasks),
@@ -272,6 +342,9 @@ class B200HydroStepper:
                 self.gravity.stage_fields(self._buf[cur], self.batch.fstride, self._info, self.batch.bc,
                                           self.batch.L, self._grav, stream)
             d = self._stage_desc(cur, nxt, s, a, bw)
+            if self._p2p:
+                d.halo = self._halo_tab[cur].data_ptr()
+                d.nown = self.batch.ncompute
             if events is not None:
                 events[s][0].record()
             _lib.check(self.lib.omb_stage(ctypes.byref(d), sh), "omb_stage")
@@ -295,7 +368,8 @@ class B200HydroStepper:
         per = 1
         p = self.part
         if p is not None:
-            per += int(sum(p.send_counts) > 0) + int(sum(p.recv_counts) > 0)
+            if not self._p2p:  # (NVLink peer reads: no pack / unpack)
+                per += int(sum(p.send_counts) > 0) + int(sum(p.recv_counts) > 0)
             if getattr(self, "_fsend", None) is not None:
                 per += int(sum(p.flux_send_counts) > 0) + int(sum(p.flux_recv_counts) > 0)
         per += int(self._amr_tasks is not None) + int(self._rleaf is not None)
