@@ -137,6 +137,8 @@ int omb_host_unpack(const double *in, int L, int n, long long fstride, double *c
  * pack chunk c into the pinned buffer while chunk c-1 is copied (upload), or unpack chunk c while
  * chunk c+1 is in flight (download).  upload returns with copies still queued on `stream`;
  * download returns with the host arrays written. */
+/* host threads used by omb_host_pack/unpack/upload/download (0 = all cores, capped at 16) */
+int omb_set_host_threads(int n);
 int omb_host_upload(const double *const *leaf_u, int L, int n, long long fstride, double *pinned, double *dev,
                     int nchunks, void *stream);
 int omb_host_download(const double *dev, double *pinned, int L, int n, long long fstride, double *const *leaf_u,

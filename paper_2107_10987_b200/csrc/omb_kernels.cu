@@ -906,8 +906,9 @@ static HostPool& host_pool() {
   return *p;
 }
 
+static std::atomic<int> g_host_threads(0);  // 0: hardware_concurrency (capped at 16)
 static int host_workers(int L) {
-  unsigned nt = std::thread::hardware_concurrency();
+  unsigned nt = g_host_threads.load() > 0 ? (unsigned)g_host_threads.load() : std::thread::hardware_concurrency();
   if (nt == 0) nt = 1;
   if (nt > 16) nt = 16;
   if ((long long)nt > L) nt = L > 0 ? (unsigned)L : 1u;
@@ -961,6 +962,12 @@ static void host_copy(const double* const* leaf_u, int L, int n, long long fstri
     for (int i = (int)((long long)L * t / nt); i < (int)((long long)L * (t + 1) / nt); i++)
       copy_leaf(leaf_u[i], packed, i, n, fstride, to_packed);
   }, nt);
+}
+
+// host threads of the pack / unpack / transfer pool (0 = all cores); ranks sharing a host split them
+int omb_set_host_threads(int n) {
+  g_host_threads.store(n < 0 ? 0 : n);
+  return 0;
 }
 
 int omb_host_pack(const double* const* leaf_u, int L, int n, long long fstride, double* out) {

@@ -68,6 +68,10 @@ class B200HydroStepper:
             import torch.distributed as dist
 
             self.dist = dist
+            # ranks on one host share its cores for the host-side packing
+            per_host = int(os.environ.get("LOCAL_WORLD_SIZE", "1"))
+            if per_host > 1:
+                self.lib.omb_set_host_threads(max(1, (os.cpu_count() or 1) // per_host))
             self.batch = partition.batch(tree, max_run=max_run)
         else:
             self.dist = None
