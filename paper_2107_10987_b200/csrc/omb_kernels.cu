@@ -326,16 +326,11 @@ __global__ void __launch_bounds__(NT, 1) k_stage(StageArgs A) {
     async_commit();
     // P6 = the update of plane X-2 (its x fluxes sit in the 3-slot FX ring,
     // its y/z fluxes in FYZ since this plane's P0, its inputs staged in SG6)
-    // runs on the last 64 threads, idle in the last P1 group (<= 400 items)
+    // runs beside P3 on the last 64 threads, which P3's <= 400 items leave idle
     const bool p6 = X >= 3 && st.interior(X - 2);
 #pragma unroll 1
     for (int g = 0; g < ngroups; g++) {
       st.boundary_lines(g, tid, nthr, h);  // P1
-      if (g == ngroups - 1 && p6 && tid >= nthr - NFACEX) {
-        st.set_plane(X - 1);
-        st.update_plane(tid - (nthr - NFACEX), NFACEX);
-        st.set_plane(X);
-      }
       __syncthreads();
       PH(2 + 2 * g);
       st.store_hi(h);
@@ -350,7 +345,12 @@ __global__ void __launch_bounds__(NT, 1) k_stage(StageArgs A) {
       __syncthreads();
       PH(3 + 2 * g);
     }
-    st.inplane_lines(tid, nthr);  // P3
+    st.inplane_lines(tid, nthr);  // P3 (<= 400 items)
+    if (p6 && tid >= nthr - NFACEX) {  // P6 on the last 64 threads
+      st.set_plane(X - 1);
+      st.update_plane(tid - (nthr - NFACEX), NFACEX);
+      st.set_plane(X);
+    }
     __syncthreads();
     PH(6);
     if (st.interior(X)) st.inplane_fluxes(tid, nthr);  // P4 (<= 468 items)

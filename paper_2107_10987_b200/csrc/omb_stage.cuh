@@ -19,8 +19,8 @@
 //   P5  finish the y/z faces of plane X-1, start those of plane X -- run in
 //       the NEXT plane's P0 phase, beside the conversion
 //   P6  conservative update of plane X-2 + sources + dual-energy + floors
-//       (step.py:243-288), on the last 64 threads during the last P1 group
-// i.e. 7 barriers per plane: P0+P5 | P1A | P2A | P1B+P6 | P2B | P3 | P4.
+//       (step.py:243-288), on the last 64 threads during P3
+// i.e. 7 barriers per plane: P0+P5 | P1A | P2A | P1B | P2B | P3+P6 | P4.
 //
 // lo/hi and point fluxes never leave shared memory.  Every phase is a loop
 // over independent items separated by barriers; values a thread carries

@@ -11,7 +11,7 @@ import sys
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 NAMES = ["prologue", "P0 convert + P5 of prev plane", "P1A lines 0,3-6 + KT", "P2A combine",
-         "P1B lines 9-12 + KT + P6", "P2B combine", "P3 in-plane mono", "P4 in-plane KT", "last P5",
+         "P1B lines 9-12 + KT", "P2B combine", "P3 in-plane mono + P6", "P4 in-plane KT", "last P5",
          "epilogue P6"]
 
 

@@ -50,14 +50,12 @@ extern "C" int emu_stage(const OmbStageDesc* d, int nthr) {
       ALL(if (X + 3 < 8 * R + 6) s.prefetch_plane(X + 3, t, nthr));
       const bool p6 = X >= 3 && st[0].interior(X - 2);
       for (int g = 0; g < ngroups; g++) {
-        ALL(s.boundary_lines(g, t, nthr, h[t]);
-            if (g == ngroups - 1 && p6 && t >= nthr - NFACEX) {
-              s.set_plane(X - 1); s.update_plane(t - (nthr - NFACEX), NFACEX); s.set_plane(X);
-            });
+        ALL(s.boundary_lines(g, t, nthr, h[t]));
         ALL(s.store_hi(h[t]);
             if (X >= 3) { if (g == 0) s.combine_A(t, nthr); else if (A.quad) s.combine_B(t, nthr); });
       }
-      ALL(s.inplane_lines(t, nthr));
+      ALL(s.inplane_lines(t, nthr);
+          if (p6 && t >= nthr - NFACEX) { s.set_plane(X - 1); s.update_plane(t - (nthr - NFACEX), NFACEX); s.set_plane(X); });
       ALL(if (s.interior(X)) s.inplane_fluxes(t, nthr));
     }
     ALL(s.set_plane(8 * R + 3); s.faces_yz(t, nthr); if (t < NFACEX) s.prefetch_update(8 * R + 2, t, NFACEX));
