@@ -37,10 +37,6 @@
 namespace {
 
 constexpr int NC = 20;  // [M0, M1(3), M2(6), M3(10)]
-#ifndef FMM_M2L_UNROLL
-#define FMM_M2L_UNROLL 1
-#endif
-constexpr int kM2LUnroll = FMM_M2L_UNROLL;
 // symmetric tensor component tables (multipole.py:21-42)
 __constant__ int c_s2a[6] = {0, 0, 0, 1, 1, 2};
 __constant__ int c_s2b[6] = {0, 1, 2, 1, 2, 2};
@@ -133,7 +129,6 @@ __global__ void __launch_bounds__(128, 4) k_fmm_m2l(const long long* off, const 
   double l[KN];
 #pragma unroll
   for (int k = 0; k < KN; k++) l[k] = L[x * NC + K0 + k];
-#pragma unroll kM2LUnroll
   for (long long q = off[ti]; q < off[ti + 1]; q++) {
     unsigned long long w = __ldg(contrib + q);
     long long src = (long long)(w & 0xFFFFFFFFFFull);
