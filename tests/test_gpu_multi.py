@@ -24,8 +24,11 @@ def _ngpus():
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("halo", ["p2p", "nccl"])
 @pytest.mark.parametrize("world", [2, 4])
-def test_partitioned_steps_match_single_process(world):
+def test_partitioned_steps_match_single_process(world, halo):
+    """halo: uniform trees read neighbour leaves over NVLink peer memory (default) or exchange
+    them with NCCL (OMB_HALO=nccl); AMR trees always exchange."""
     if _ngpus() < world:
         pytest.skip(f"needs {world} GPUs")
     with socket.socket() as s:
@@ -33,6 +36,7 @@ def test_partitioned_steps_match_single_process(world):
         port = s.getsockname()[1]
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nproc-per-node", str(world), "--master-addr",
            "127.0.0.1", "--master-port", str(port), os.path.join(HERE, "gpu_dist_check.py")]
-    r = subprocess.run(cmd, capture_output=True, text=True, timeout=900)
+    env = dict(os.environ, OMB_HALO=halo)
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=900, env=env)
     assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
     assert f"multi-GPU parity on {world} ranks: OK" in r.stdout + r.stderr
