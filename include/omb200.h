@@ -175,6 +175,13 @@ long long omb_fmm_traverse(const double *center, const double *width, const long
 long long omb_fmm_build(const long long *pa, const long long *pb, const long long *pk, long long np, long long nent,
                         long long *group_first, unsigned char *group_flags, long long gcap, long long *off,
                         unsigned long long *contrib);
+/* theta = 0 (direct_traversal_eval, _core.pyx:611-690): per-target lists in traversal order (HOST), and the
+ * direct cell-cell sums into phi / g of the cells (device) */
+int omb_fmm_build_direct(const long long *pa, const long long *pb, long long np, long long nent, long long *off,
+                         unsigned long long *contrib);
+int omb_fmm_direct(const long long *off, const unsigned long long *contrib, const double *center, const double *M,
+                   const long long *cell_base, int nleaf, double *phi, double *gx, double *gy, double *gz,
+                   void *stream);
 int omb_fmm_masses(const double *rho, const long long *cell_base, int nleaf, const double *dx3, double *M,
                    void *stream);
 int omb_fmm_upward(const long long *parents, int np, const long long *children, const double *center, double *M,

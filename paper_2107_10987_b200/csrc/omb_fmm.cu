@@ -277,6 +277,46 @@ __global__ void k_fmm_rhodot(const double* U, long long fstride, const omb::Leaf
   out[i] = -((dsx + dsy) + dsz) * inv2dx;
 }
 
+// theta = 0 (always reject): direct cell-cell sums in the traversal's order
+// (_core.pyx:611-690, direct_traversal_eval).  contrib word: partner | side
+// << 63 (side 1: this target is the pair's a).  Writes phi, g of the cells.
+__global__ void k_fmm_direct(const long long* off, const unsigned long long* contrib, const double* center,
+                             const double* M, const long long* cell_base, int nleaf, double* phi, double* gx,
+                             double* gy, double* gz) {
+  long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (i >= (long long)nleaf * 512) return;
+  long long x = cell_base[i / 512] + i % 512;
+  double p = 0.0, g0 = 0.0, g1 = 0.0, g2 = 0.0;
+  for (long long q = off[x]; q < off[x + 1]; q++) {
+    unsigned long long w = contrib[q];
+    long long o = (long long)(w & 0xFFFFFFFFFFull);
+    bool is_a = (w >> 63) != 0;
+    long long a = is_a ? x : o, b = is_a ? o : x;
+    double rx = center[b * 3 + 0] - center[a * 3 + 0];
+    double ry = center[b * 3 + 1] - center[a * 3 + 1];
+    double rz = center[b * 3 + 2] - center[a * 3 + 2];
+    double r2 = rx * rx + ry * ry + rz * rz;
+    double d = sqrt(r2);
+    double inv_r = 1.0 / d;
+    double inv_r3 = inv_r / r2;
+    double m = M[o * NC];
+    p -= m * inv_r;
+    if (is_a) {
+      g0 += m * rx * inv_r3;
+      g1 += m * ry * inv_r3;
+      g2 += m * rz * inv_r3;
+    } else {
+      g0 -= m * rx * inv_r3;
+      g1 -= m * ry * inv_r3;
+      g2 -= m * rz * inv_r3;
+    }
+  }
+  phi[i] = p;
+  gx[i] = g0;
+  gy[i] = g1;
+  gz[i] = g2;
+}
+
 thread_local std::string f_err;
 int ferr(const char* what, cudaError_t e) {
   f_err = std::string(what) + ": " + cudaGetErrorString(e);
@@ -407,6 +447,35 @@ long long omb_fmm_build(const long long* pa, const long long* pb, const long lon
     contrib[pos[pa[i]]++] = (unsigned long long)pb[i] | (g << 40) | (1ull << 63);
   }
   return G;
+}
+
+// per-target lists of a theta = 0 traversal, in traversal order (b-side
+// before a-side of each pair): off [nent+1], contrib [2*np] (partner | side << 63)
+int omb_fmm_build_direct(const long long* pa, const long long* pb, long long np, long long nent, long long* off,
+                         unsigned long long* contrib) {
+  for (long long e = 0; e <= nent; e++) off[e] = 0;
+  for (long long i = 0; i < np; i++) {
+    off[pb[i] + 1]++;
+    off[pa[i] + 1]++;
+  }
+  for (long long e = 0; e < nent; e++) off[e + 1] += off[e];
+  std::vector<long long> pos(off, off + nent);
+  for (long long i = 0; i < np; i++) {
+    contrib[pos[pb[i]]++] = (unsigned long long)pa[i];
+    contrib[pos[pa[i]]++] = (unsigned long long)pb[i] | (1ull << 63);
+  }
+  return 0;
+}
+
+int omb_fmm_direct(const long long* off, const unsigned long long* contrib, const double* center, const double* M,
+                   const long long* cell_base, int nleaf, double* phi, double* gx, double* gy, double* gz,
+                   void* stream) {
+  long long n = (long long)nleaf * 512;
+  if (n == 0) return 0;
+  k_fmm_direct<<<(unsigned)((n + 127) / 128), 128, 0, (cudaStream_t)stream>>>(off, contrib, center, M, cell_base,
+                                                                              nleaf, phi, gx, gy, gz);
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? 0 : ferr("omb_fmm_direct", e);
 }
 
 int omb_fmm_masses(const double* rho, const long long* cell_base, int nleaf, const double* dx3, double* M,

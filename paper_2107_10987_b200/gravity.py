@@ -180,13 +180,12 @@ def group_pairs(table, pa, pb, pk):
 
 class B200FmmSolver:
     """Order-3 FMM on the device; same API as the reference's ``FmmSolver``
-    (``prepare``, ``solve_density``, ``solve``, ``stats``).  theta in (0, 1]."""
+    (``prepare``, ``solve_density``, ``solve``, ``stats``).  theta in [0, 1]; theta = 0 is the
+    reference's always-reject direct summation (direct_traversal_eval, _core.pyx:611-690)."""
 
     def __init__(self, theta, device=None):
         if theta < 0.0 or theta > 1.0:
             raise ValueError("theta must lie in [0, 1]")
-        if theta == 0.0:
-            raise NotImplementedError("theta = 0 (always-reject direct traversal) is not provided on the device")
         import torch
 
         self.theta = float(theta)
@@ -210,6 +209,10 @@ class B200FmmSolver:
         t = EntityTable(tree)
         self.table = t
         pa, pb, pk = traverse(self.lib, t, self.theta)
+        if self.theta == 0.0:
+            self._prepare_direct(tree, t, pa, pb)
+            self._signature = sig
+            return
         # groups (sorted keys) and per-target contribution lists in the global M2L order (C++, O(pairs))
         gcap = 1 << 22
         gfirst = np.empty(gcap, dtype=np.int64)
@@ -252,6 +255,42 @@ class B200FmmSolver:
         self._L = T.zeros_like(self._M)
         self._signature = sig
 
+    def _prepare_direct(self, tree, t, pa, pb):
+        """theta = 0: per-target cell-cell lists in the traversal's order."""
+        import torch
+
+        off = np.empty(t.nentities + 1, dtype=np.int64)
+        contrib = np.empty(2 * len(pa), dtype=np.uint64)
+        _lib.check(self.lib.omb_fmm_build_direct(pa.ctypes.data, pb.ctypes.data, len(pa), t.nentities,
+                                                 off.ctypes.data, contrib.ctypes.data), "omb_fmm_build_direct")
+        self.stats = {}  # the reference's direct path records no groups/pairs
+        dev = self.dev
+        self._center = torch.from_numpy(np.ascontiguousarray(t.center).reshape(-1)).to(dev)
+        self._off = torch.from_numpy(off).to(dev)
+        self._contrib = torch.from_numpy(contrib.view(np.int64)).to(dev)
+        self._cell_base = torch.from_numpy(t.cell_base).to(dev)
+        self._dx3_dev = torch.tensor([lf.subgrid.dx ** 3 for lf in tree.sorted_leaves()], dtype=torch.float64,
+                                     device=dev)
+        self._M = torch.zeros(t.nentities * NCOMP, dtype=torch.float64, device=dev)
+        self._L = None
+        self._up, self._down = [], []
+
+    def _solve_into(self, rho_dev, dx3_dev, phi, gx, gy, gz, stream=None):
+        """One solve of the density rho_dev ([L][512]) into phi, gx, gy, gz of the cells."""
+        nleaf = len(self.table.leaf_paths)
+        if self.theta == 0.0:
+            lib, sh = self.lib, stream_handle(stream)
+            self._M.zero_()
+            _lib.check(lib.omb_fmm_masses(ptr(rho_dev), ptr(self._cell_base), nleaf, ptr(dx3_dev), ptr(self._M), sh),
+                       "omb_fmm_masses")
+            _lib.check(lib.omb_fmm_direct(ptr(self._off), ptr(self._contrib), ptr(self._center), ptr(self._M),
+                                          ptr(self._cell_base), nleaf, ptr(phi), ptr(gx), ptr(gy), ptr(gz), sh),
+                       "omb_fmm_direct")
+            return
+        self._run(rho_dev, dx3_dev, stream)
+        _lib.check(self.lib.omb_fmm_fields(ptr(self._L), ptr(self._cell_base), nleaf, ptr(phi), ptr(gx), ptr(gy),
+                                           ptr(gz), stream_handle(stream)), "omb_fmm_fields")
+
     # -- device passes ---------------------------------------------------------
     def _run(self, rho_dev, dx3_dev, stream=None):
         """rho_dev: [L][512] densities of sorted_leaves(); returns L (entities x 20)."""
@@ -274,18 +313,17 @@ class B200FmmSolver:
 
     def fields_device(self, rho_dev, dx3_dev, out4, stream=None):
         """phi, gx, gy, gz per cell into out4 ([4][L][512] device tensor)."""
-        self._run(rho_dev, dx3_dev, stream)
         nleaf = len(self.table.leaf_paths)
         n = nleaf * 512
         o = out4.reshape(4, -1)
-        _lib.check(self.lib.omb_fmm_fields(ptr(self._L), ptr(self._cell_base), nleaf, ptr(o[0]), ptr(o[1]), ptr(o[2]),
-                                           ptr(o[3]), stream_handle(stream)), "omb_fmm_fields")
+        self._solve_into(rho_dev, dx3_dev, o[0], o[1], o[2], o[3], stream)
         return o[:, :n]
 
     def launches_per_stage(self):
         """Kernels of one stage_fields call: 2 solves x (masses, upward levels, M2L,
         downward levels, fields) + the -div(momentum) source."""
-        return 2 * (3 + len(self._up) + len(self._down)) + 1
+        per = 2 if self.theta == 0.0 else 3 + len(self._up) + len(self._down)
+        return 2 * per + 1
 
     def stage_fields(self, U, fstride, info, bc, nleaf, grav, stream=None):
         """The stepper's per-stage solve (solver.py:134-153 on device data):
@@ -301,13 +339,9 @@ class B200FmmSolver:
             self._scratch = torch.empty(2 * n, dtype=torch.float64, device=self.dev)
         phi, rhodot = self._scratch[:n], self._scratch[n:2 * n]
         G = grav.reshape(4, -1)
-        self._run(U[:n], self._dx3_dev, stream)
-        _lib.check(lib.omb_fmm_fields(ptr(self._L), ptr(self._cell_base), nleaf, ptr(phi), ptr(G[0]), ptr(G[1]),
-                                      ptr(G[2]), sh), "omb_fmm_fields")
+        self._solve_into(U[:n], self._dx3_dev, phi, G[0], G[1], G[2], stream)
         _lib.check(lib.omb_fmm_rhodot(ptr(U), fstride, ptr(info), bc, nleaf, ptr(rhodot), sh), "omb_fmm_rhodot")
-        self._run(rhodot, self._dx3_dev, stream)
-        _lib.check(lib.omb_fmm_fields(ptr(self._L), ptr(self._cell_base), nleaf, ptr(G[3]), ptr(phi), ptr(phi),
-                                      ptr(phi), sh), "omb_fmm_fields")
+        self._solve_into(rhodot, self._dx3_dev, G[3], phi, phi, phi, stream)
 
     # -- the reference's host API ----------------------------------------------
     def solve_density(self, tree, per_leaf_density=None):

@@ -282,7 +282,7 @@ def fmm_case():
     out = {}
     cases = []
     t = fill(build_uniform_tree(1, 8), 5)
-    cases += [("u05", t, 0.5), ("u035", t, 0.35)]
+    cases += [("u05", t, 0.5), ("u035", t, 0.35), ("u0", t, 0.0)]
     t2 = build_uniform_tree(1, 8)
     t2.split(t2.leaf_at(1, (0, 0, 0)))
     t2.reindex()
@@ -295,6 +295,9 @@ def fmm_case():
         out[f"{name}_rho"] = np.stack([lf.subgrid.interior[0] for lf in leaves])
         out[f"{name}_phi"] = np.stack([phi[lf.path] for lf in leaves])
         out[f"{name}_g"] = np.stack([g[lf.path] for lf in leaves])
+        out[f"{name}_theta"] = np.array(theta)
+        if theta == 0.0:  # direct traversal: no groups
+            continue
         out[f"{name}_stats"] = np.array([solver.stats["groups"], solver.stats["pairs"]])
         grp = solver._groups
         out[f"{name}_R"] = np.array([gr[0] for gr in grp])
