@@ -107,6 +107,10 @@ def peaks():
 # clocks during the timed region (B200_PROFILING.md recipe)
 # ---------------------------------------------------------------------------
 class ClockSampler:
+    """nvidia-smi every 50 ms from before the warm-up on; stop(t0, t1) keeps the
+    samples taken inside the timed wall-clock window [t0, t1] (the nearest ones
+    when the window is shorter than the sampling period)."""
+
     def __init__(self, index):
         self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
         q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
@@ -114,25 +118,40 @@ class ClockSampler:
              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
         try:
             self.p = subprocess.Popen(["nvidia-smi", f"--id={index}", f"--query-gpu={q}", "--format=csv,noheader,nounits",
-                                       "-lms", "100"], stdout=self.f, stderr=subprocess.DEVNULL)
+                                       "-lms", "50"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True,
+                                      bufsize=1)
+            import threading
+
+            self.rows = []
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
         except Exception:  # noqa: BLE001
             self.p = None
 
-    def stop(self):
+    def _read(self):
+        for line in self.p.stdout:  # stamp each sample with the host wall clock
+            self.rows.append((time.time(), line.strip().split(",")))
+
+    def stop(self, t0=None, t1=None):
         if self.p is None:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.06)
         self.p.terminate()
         self.p.wait()
-        self.f.seek(0)
-        rows = [r.split(",") for r in self.f.read().strip().splitlines() if r.strip()]
+        self.t.join(timeout=1.0)
         os.unlink(self.f.name)
-        sm = [float(r[1]) for r in rows if len(r) >= 9 and r[1].strip().replace(".", "").isdigit()]
-        mx = [float(r[2]) for r in rows if len(r) >= 9 and r[2].strip().replace(".", "").isdigit()]
+        rows = [(ts, r) for ts, r in self.rows if len(r) >= 9]
+        if t0 is not None and rows:
+            inside = [(ts, r) for ts, r in rows if t0 <= ts <= t1]
+            if not inside:  # window shorter than the period: the samples around it
+                inside = sorted(rows, key=lambda x: min(abs(x[0] - t0), abs(x[0] - t1)))[:2]
+            rows = inside
+        rows = [r for _, r in rows]
+        sm = [float(r[1]) for r in rows if r[1].strip().replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in rows if r[2].strip().replace(".", "").isdigit()]
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         reasons = set()
         for r in rows:
-            if len(r) < 9:
-                continue
             for k, nm in enumerate(names):
                 if r[5 + k].strip().lower() == "active":
                     reasons.add(nm)
@@ -286,7 +305,8 @@ def gpu_arm(args, rank, world):
     local_cells = st.batch.ncompute * 512
     peak64 = fp64_peak(lib, torch)
 
-    # warm-up
+    # warm-up (the clock sampler runs from here on)
+    clk = ClockSampler(torch.cuda.current_device())
     for _ in range(args.warmup):
         st._cfl_launch(0.4)
         st.launch_step(None)
@@ -300,10 +320,9 @@ def gpu_arm(args, rank, world):
     if dist is not None:
         dist.barrier()
     torch.cuda.synchronize()
-    clk = ClockSampler(torch.cuda.current_device())
-    time.sleep(0.3)
     t_start = torch.cuda.Event(enable_timing=True)
     t_end = torch.cuda.Event(enable_timing=True)
+    w_start = time.time()
     t_start.record()
     for k in range(K):
         st._cfl_launch(0.4)
@@ -312,7 +331,8 @@ def gpu_arm(args, rank, world):
         dt_h[k].copy_(st._dt, non_blocking=True)
     t_end.record()
     torch.cuda.synchronize()
-    clocks = clk.stop()
+    w_end = time.time()
+    clocks = clk.stop(w_start, w_end)
     if dist is not None:
         dist.barrier()
     ms = t_start.elapsed_time(t_end)
