@@ -138,7 +138,8 @@ struct Smem {
   static constexpr int SG0 = FYZ + 2 * NF * NYF;    // [6][196] staged conserved plane (next P0)
   static constexpr int SG6 = SG0 + NF * PL;          // [16][64] staged cur(6) u0(6) grav(4) (next P6)
   static constexpr int LINFO = SG6 + 16 * NFACEX;    // the run's LeafInfo copies [4] (+ leaf ids [4])
-  static constexpr int TOTAL = LINFO + 4 * 20 + 2;
+  static constexpr int FLIPS = LINFO + 4 * 20 + 2;  // [196] bytes: wall-mirror flips of the SG0 plane
+  static constexpr int TOTAL = FLIPS + (PL + 7) / 8;
   static constexpr int BYTES = TOTAL * 8;
 };
 static_assert(Smem::BYTES <= 232448, "stage shared memory exceeds 227 KB");
@@ -336,17 +337,20 @@ struct Stage {
       const double* p = (A.halo != nullptr && src >= A.nown) ? A.halo[src - A.nown] + (base & 511) : A.ucur + base;
 #pragma unroll
       for (int v = 0; v < NF; v++) async_copy8(S + stage + v * PL + it, p + v * A.fstride);
+      if (stage == Smem::SG0) ((unsigned char*)(S + Smem::FLIPS))[it] = (unsigned char)fm;  // for P0
     }
   }
 
-  // P0: primitives of the staged plane Xn into the ring (flips re-derived)
+  // P0: primitives of the staged plane Xn into the ring (wall flips recorded
+  // by the prefetch for the SG0 plane, re-derived for the prologue's planes)
   OMB_HD void convert_plane(int Xn, int tid, int nthr, int stage = Smem::SG0) {
     int r, lx;
     view_of(Xn, r, lx);
     const LeafInfo& LI = LIs[r];
     for (int it = tid; it < PL; it += nthr) {
       int fm;
-      gather_addr(LI, A.bc, lx, it / M, it % M, fm);
+      if (stage == Smem::SG0) fm = ((const unsigned char*)(S + Smem::FLIPS))[it];  // recorded by the prefetch
+      else gather_addr(LI, A.bc, lx, it / M, it % M, fm);
       double u[NF], w[NF];
 #pragma unroll
       for (int v = 0; v < NF; v++) u[v] = S[stage + v * PL + it];
