@@ -325,12 +325,16 @@ __global__ void __launch_bounds__(NT, 1) k_stage(StageArgs A) {
     if (X + 3 < 8 * R + 6) st.prefetch_plane(X + 3, tid, nthr);  // stage next P0 (cp.async)
     async_commit();
     // P6 = the update of plane X-2 (its x fluxes sit in the 3-slot FX ring,
-    // its y/z fluxes in FYZ since this plane's P0, its inputs staged in SG6)
-    // runs beside P3 on the last 64 threads, which P3's <= 400 items leave idle
+    // its y/z fluxes in FYZ since this plane's P0, its inputs staged in SG6),
+    // in two halves on the last 64 threads: fluxes + sources + RK beside P2A
+    // (432 items), dual energy + floors + store beside P3 (<= 400 items)
     const bool p6 = X >= 3 && st.interior(X - 2);
 #pragma unroll 1
     for (int g = 0; g < ngroups; g++) {
       st.boundary_lines(g, tid, nthr, h);  // P1
+      // the update inputs staged in this plane's P0 (SG6) land before P6 part A
+      // (this plane's SG0 group, committed last, may still be in flight)
+      if (g == 0) async_wait_prev();
       __syncthreads();
       PH(2 + 2 * g);
       st.store_hi(h);
@@ -338,17 +342,18 @@ __global__ void __launch_bounds__(NT, 1) k_stage(StageArgs A) {
         if (g == 0) st.combine_A(tid, nthr);
         else if (A.quad) st.combine_B(tid, nthr);
       }
-      // the update inputs staged in this plane's P0 (SG6) must have landed
-      // before P1B's update (this plane's SG0 group may still fly)
-      if (g == 0 && ngroups == 2) async_wait_prev();
-      else if (ngroups == 1) async_wait_all();
+      if (g == 0 && p6 && tid >= nthr - NFACEX) {  // P6 part A on the threads P2A leaves idle
+        st.set_plane(X - 1);
+        st.update_plane_a(tid - (nthr - NFACEX), NFACEX);
+        st.set_plane(X);
+      }
       __syncthreads();
       PH(3 + 2 * g);
     }
     st.inplane_lines(tid, nthr);  // P3 (<= 400 items)
-    if (p6 && tid >= nthr - NFACEX) {  // P6 on the last 64 threads
+    if (p6 && tid >= nthr - NFACEX) {  // P6 part B on the last 64 threads
       st.set_plane(X - 1);
-      st.update_plane(tid - (nthr - NFACEX), NFACEX);
+      st.update_plane_b(tid - (nthr - NFACEX), NFACEX);
       st.set_plane(X);
     }
     __syncthreads();

@@ -301,8 +301,9 @@ struct UpdateParams {
   int has_src, has_grav;
 };
 
-OMB_HD void update_cell(const UpdateParams& P, const double* u, const double* u0, double* r, double x, double y,
-                        const double* g /* gx gy gz dphi_dt or null */, double* out) {
+// first part: sources and the RK combination -> nw
+OMB_HD void update_cell_rk(const UpdateParams& P, const double* u, const double* u0, double* r, double x, double y,
+                           const double* g /* gx gy gz dphi_dt or null */, double* nw) {
   if (P.has_src) {
     if (P.omega != 0.0) {
       double w2 = P.omega * P.omega;
@@ -326,12 +327,15 @@ OMB_HD void update_cell(const UpdateParams& P, const double* u, const double* u0
       r[5] = r[5] + 0.0;
     }
   }
-  double nw[NF];
 #pragma unroll
   for (int v = 0; v < NF; v++) {
     double st = u[v] + P.dt * r[v];
     nw[v] = (P.a != 0.0) ? P.a * u0[v] + P.b * st : st;
   }
+}
+
+// second part: dual-energy resync and floors (nw in, out)
+OMB_HD void update_cell_fin(const UpdateParams& P, double* nw, double* out) {
   {  // dual_energy_sync
     double kin = div_nz(0.5 * ((nw[1] * nw[1] + nw[2] * nw[2]) + nw[3] * nw[3]), nw[0]);
     double e1 = nw[4] - kin;
@@ -354,6 +358,13 @@ OMB_HD void update_cell(const UpdateParams& P, const double* u, const double* u0
   if (P.floor_tau > 0.0 && nw[5] < P.floor_tau) nw[5] = P.floor_tau;
 #pragma unroll
   for (int v = 0; v < NF; v++) out[v] = nw[v];
+}
+
+OMB_HD void update_cell(const UpdateParams& P, const double* u, const double* u0, double* r, double x, double y,
+                        const double* g /* gx gy gz dphi_dt or null */, double* out) {
+  double nw[NF];
+  update_cell_rk(P, u, u0, r, x, y, g, nw);
+  update_cell_fin(P, nw, out);
 }
 
 }  // namespace omb

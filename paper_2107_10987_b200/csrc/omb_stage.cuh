@@ -19,8 +19,9 @@
 //   P5  finish the y/z faces of plane X-1, start those of plane X -- run in
 //       the NEXT plane's P0 phase, beside the conversion
 //   P6  conservative update of plane X-2 + sources + dual-energy + floors
-//       (step.py:243-288), on the last 64 threads during P3
-// i.e. 7 barriers per plane: P0+P5 | P1A | P2A | P1B | P2B | P3+P6 | P4.
+//       (step.py:243-288), on the last 64 threads: fluxes/sources/RK during
+//       P2A, dual energy/floors/store during P3
+// i.e. 7 barriers per plane: P0+P5 | P1A | P2A+P6a | P1B | P2B | P3+P6b | P4.
 //
 // lo/hi and point fluxes never leave shared memory.  Every phase is a loop
 // over independent items separated by barriers; values a thread carries
@@ -680,6 +681,69 @@ struct Stage {
   }
 
   // ---- P6: update the cells of plane X-1 ---------------------------------
+  // The update split in two so each half hides beside a phase's own items:
+  // part A (fluxes, sources, RK combination) leaves the 6 combined values in
+  // SG6's `cur` rows (consumed by then); part B (dual energy, floors) stores.
+  OMB_HD UpdateParams update_params() const {
+    UpdateParams P;
+    P.dt = *A.dt; P.a = A.a; P.b = A.b;
+    P.gamma = A.gamma; P.eta = A.eta; P.inv_gamma = A.inv_gamma; P.omega = A.omega;
+    P.floor_rho = A.floor_rho; P.floor_tau = A.floor_tau; P.floor_vmax = A.floor_vmax;
+    P.has_grav = A.grav != nullptr;
+    P.has_src = (A.omega != 0.0) || P.has_grav;
+    return P;
+  }
+  OMB_HD void update_plane_a(int tid, int nthr) {
+    int Xc = X - 1;
+    int r = (Xc - 3) >> 3, lx = (Xc - 3) & 7;
+    const LeafInfo& LI = LIs[r];
+    if (LI.flags & 2) return;
+    const double* FXlo = S + Smem::FX + (Xc % 3) * NF * NFACEX;
+    const double* FXhi = S + Smem::FX + (X % 3) * NF * NFACEX;
+    const UpdateParams P = update_params();
+    for (int it = tid; it < NFACEX; it += nthr) {
+      int y = 3 + it / 8, z = 3 + it % 8;
+      double u[NF], u0[NF], rr[NF], nw[NF], g[4] = {0, 0, 0, 0};
+#pragma unroll
+      for (int v = 0; v < NF; v++) {
+        u[v] = S[Smem::SG6 + v * NFACEX + it];
+        u0[v] = S[Smem::SG6 + (NF + v) * NFACEX + it];
+        double dfx = FXhi[v * NFACEX + it] - FXlo[v * NFACEX + it];
+        double dfy = S[Smem::FYZ + v * NYF + yslot(y, z)] - S[Smem::FYZ + v * NYF + yslot(y - 1, z)];
+        double dfz = S[Smem::FYZ + (NF + v) * NYF + zslot(y, z)] - S[Smem::FYZ + (NF + v) * NYF + zslot(y, z - 1)];
+        double t = 0.0 - dfx * LI.inv_dx;
+        t = t - dfy * LI.inv_dx;
+        t = t - dfz * LI.inv_dx;
+        rr[v] = t;
+      }
+      if (P.has_grav)
+#pragma unroll
+        for (int k = 0; k < 4; k++) g[k] = S[Smem::SG6 + (2 * NF + k) * NFACEX + it];
+      double xc = LI.ox + LI.dx * (double)lx;
+      double yc = LI.oy + LI.dx * (double)(y - 3);
+      update_cell_rk(P, u, u0, rr, xc, yc, g, nw);
+#pragma unroll
+      for (int v = 0; v < NF; v++) S[Smem::SG6 + v * NFACEX + it] = nw[v];
+    }
+  }
+  OMB_HD void update_plane_b(int tid, int nthr) {
+    int Xc = X - 1;
+    int r = (Xc - 3) >> 3, lx = (Xc - 3) & 7;
+    int leaf = lids[r];
+    const LeafInfo& LI = LIs[r];
+    if (LI.flags & 2) return;
+    const UpdateParams P = update_params();
+    for (int it = tid; it < NFACEX; it += nthr) {
+      long long cell = (long long)leaf * 512 + lx * 64 + it;  // (y-3)*8 + (z-3) == it
+      double nw[NF], out[NF];
+#pragma unroll
+      for (int v = 0; v < NF; v++) nw[v] = S[Smem::SG6 + v * NFACEX + it];
+      update_cell_fin(P, nw, out);
+#pragma unroll
+      for (int v = 0; v < NF; v++) A.unext[v * A.fstride + cell] = out[v];
+    }
+  }
+
   OMB_HD void update_plane(int tid, int nthr) {
     int Xc = X - 1;
     int r = (Xc - 3) >> 3, lx = (Xc - 3) & 7;

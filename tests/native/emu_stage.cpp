@@ -52,10 +52,11 @@ extern "C" int emu_stage(const OmbStageDesc* d, int nthr) {
       for (int g = 0; g < ngroups; g++) {
         ALL(s.boundary_lines(g, t, nthr, h[t]));
         ALL(s.store_hi(h[t]);
-            if (X >= 3) { if (g == 0) s.combine_A(t, nthr); else if (A.quad) s.combine_B(t, nthr); });
+            if (X >= 3) { if (g == 0) s.combine_A(t, nthr); else if (A.quad) s.combine_B(t, nthr); }
+            if (g == 0 && p6 && t >= nthr - NFACEX) { s.set_plane(X - 1); s.update_plane_a(t - (nthr - NFACEX), NFACEX); s.set_plane(X); });
       }
       ALL(s.inplane_lines(t, nthr);
-          if (p6 && t >= nthr - NFACEX) { s.set_plane(X - 1); s.update_plane(t - (nthr - NFACEX), NFACEX); s.set_plane(X); });
+          if (p6 && t >= nthr - NFACEX) { s.set_plane(X - 1); s.update_plane_b(t - (nthr - NFACEX), NFACEX); s.set_plane(X); });
       ALL(if (s.interior(X)) s.inplane_fluxes(t, nthr));
     }
     ALL(s.set_plane(8 * R + 3); s.faces_yz(t, nthr); if (t < NFACEX) s.prefetch_update(8 * R + 2, t, NFACEX));
