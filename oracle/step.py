@@ -12,7 +12,7 @@ import ctypes
 
 import numpy as np
 
-from . import _p, fluxes as _fluxes, leaf_speed, lib
+from . import _p, leaf_speed, lib
 from .ghosts import exchange
 
 RK3 = ((0.0, 1.0), (0.75, 0.25), (1.0 / 3.0, 2.0 / 3.0))

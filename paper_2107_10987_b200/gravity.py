@@ -20,8 +20,6 @@ Every floating-point operation keeps the reference's order, so phi and g are
 bitwise those of the reference's compiled backend (tests/test_fmm.py).
 """
 
-import ctypes
-
 import numpy as np
 
 from . import _lib

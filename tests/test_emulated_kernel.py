@@ -7,9 +7,6 @@ import pytest
 from _cases import bitwise_mismatch, case_tree, golden, sources_gravity, state_of
 from emu import EmuStepper, lib
 
-import oracle
-from oracle.step import OracleStepper
-
 
 @pytest.mark.parametrize("name", ["smooth_periodic", "smooth_reflecting"])
 @pytest.mark.parametrize("max_run,nthr", [(1, 512), (2, 512), (2, 256), (3, 384)])

@@ -2,7 +2,6 @@
 
 import os
 
-import numpy as np
 import pytest
 
 from _cases import GOLD, bitwise_mismatch, case_tree, golden, state_of

@@ -14,7 +14,7 @@ from oracle.ghosts import exchange
 from oracle.step import OracleStepper
 from paper_2107_10987_b200 import mesh
 
-from _cases import EOS, bitwise_mismatch, case_tree, golden, random_smooth, sources_gravity, state_of
+from _cases import bitwise_mismatch, case_tree, golden, sources_gravity, state_of
 
 CORE = (slice(None), slice(None), slice(2, 12), slice(2, 12), slice(2, 12))
 
