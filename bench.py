@@ -284,8 +284,6 @@ def gpu_arm(args, rank, world):
         from paper_2107_10987_b200.gravity import B200FmmSolver
         from paper_2107_10987_b200.problems import synthetic_star
 
-        if world > 1:
-            raise SystemExit("c5g (device FMM) runs on one GPU")
         tree, eos, _, om, fl = synthetic_star(level=args.level or 4)
         extra = dict(gravity=B200FmmSolver(0.5), omega=om, floors=fl)
     else:
@@ -354,7 +352,11 @@ def gpu_arm(args, rank, world):
         f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         f0.record()
         for _ in range(3):
-            fs.stage_fields(st._buf[st._state], st.batch.fstride, st._info, st.batch.bc, st.batch.L, st._grav)
+            if world > 1:  # this rank's targets; masses all-gathered
+                fs.stage_fields_partitioned(st._buf[st._state], st.batch.fstride, st._info, st.batch.bc, st._grav,
+                                            st._halo_tab[st._state] if st._p2p else None, dist, None)
+            else:
+                fs.stage_fields(st._buf[st._state], st.batch.fstride, st._info, st.batch.bc, st.batch.L, st._grav)
         f1.record()
         torch.cuda.synchronize()
         fmm_ms = f0.elapsed_time(f1) / 3

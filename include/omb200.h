@@ -23,7 +23,7 @@
 extern "C" {
 #endif
 
-#define OMB_ABI_VERSION 3
+#define OMB_ABI_VERSION 4
 
 /* per-leaf topology / geometry record (device array, one per leaf) */
 typedef struct {
@@ -188,15 +188,16 @@ int omb_fmm_upward(const long long *parents, int np, const long long *children, 
                    void *stream);
 int omb_fmm_m2l(const long long *off, const unsigned long long *contrib, const double *D,
                 const unsigned char *cellcell, const double *M, double *L, long long ntarget,
-                const long long *targets, void *stream);
+                const long long *targets, const long long *subset /* NULL: all ntarget targets */, void *stream);
 int omb_fmm_downward(const long long *parents, int np, const long long *children, const double *center, double *L,
                      void *stream);
 int omb_fmm_fields(const double *L, const long long *cell_base, int nleaf, double *phi, double *gx, double *gy,
                    double *gz, void *stream);
 /* rho_dot = -div(momentum) (gravity/solver.py:156-168) of the batch's first nleaf leaves of a [6][fstride]
- * state, the neighbour cells gathered like the stage kernel's halo (info = the batch's OmbLeafInfo) */
-int omb_fmm_rhodot(const double *u, long long fstride, const OmbLeafInfo *info, int bc, int nleaf, double *out,
-                   void *stream);
+ * state, the neighbour cells gathered like the stage kernel's halo (info = the batch's OmbLeafInfo;
+ * halo / nown as OmbStageDesc: peer reads of other GPUs' leaves, or NULL) */
+int omb_fmm_rhodot(const double *u, long long fstride, const OmbLeafInfo *info, int bc, int nleaf,
+                   const double *const *halo, int nown, double *out, void *stream);
 const char *omb_fmm_last_error(void);
 
 #ifdef __cplusplus

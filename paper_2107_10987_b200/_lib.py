@@ -12,7 +12,7 @@ from .errors import NativeError
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 SO_PATH = os.environ.get("OMB_LIB_PATH") or os.path.join(_HERE, "libomb200.so")  # override: A/B experiments
-ABI_VERSION = 3
+ABI_VERSION = 4
 _lib = None
 
 EXPORTS = ("omb_abi_version", "omb_last_error", "omb_stage_smem_bytes", "omb_primitives", "omb_reconstruct",
@@ -63,10 +63,10 @@ def load():
     L.omb_fmm_build_direct.argtypes = [vp, vp, ll, ll, vp, vp]
     L.omb_fmm_direct.argtypes = [vp, vp, vp, vp, vp, i, vp, vp, vp, vp, vp]
     L.omb_fmm_upward.argtypes = [vp, i, vp, vp, vp, vp]
-    L.omb_fmm_m2l.argtypes = [vp, vp, vp, vp, vp, vp, ll, vp, vp]
+    L.omb_fmm_m2l.argtypes = [vp, vp, vp, vp, vp, vp, ll, vp, vp, vp]
     L.omb_fmm_downward.argtypes = [vp, i, vp, vp, vp, vp]
     L.omb_fmm_fields.argtypes = [vp, vp, i, vp, vp, vp, vp, vp]
-    L.omb_fmm_rhodot.argtypes = [vp, ll, vp, i, i, vp, vp]
+    L.omb_fmm_rhodot.argtypes = [vp, ll, vp, i, i, vp, i, vp, vp]
     L.omb_reflux_update.argtypes = [ctypes.POINTER(OmbRefluxDesc), vp]
     for fn in EXPORTS[3:]:
         getattr(L, fn).restype = i

@@ -121,9 +121,10 @@ template <int PART>
 __global__ void __launch_bounds__(128, 4) k_fmm_m2l(const long long* off, const unsigned long long* contrib,
                                                     const double* D /*[G][2][20]*/, const unsigned char* cellcell,
                                                     const double* M, double* L, long long ntarget,
-                                                    const long long* targets) {
-  long long ti = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-  if (ti >= ntarget) return;
+                                                    const long long* targets, const long long* subset) {
+  long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (k >= ntarget) return;
+  long long ti = subset ? subset[k] : k;  // a rank of a partitioned run solves only its targets
   long long x = targets[ti];
   constexpr int K0 = PART == 0 ? 0 : 4, KN = PART == 0 ? 4 : 16;
   double l[KN];
@@ -257,7 +258,7 @@ __global__ void k_fmm_fields(const double* L, const long long* cell_base, int nl
 // physical walls with the normal momentum mirrored), i.e. what the
 // reference's ghost fill puts there before the gravity solve (step.py:106-113)
 __global__ void k_fmm_rhodot(const double* U, long long fstride, const omb::LeafInfo* info, int bc, int nleaf,
-                             double* out) {
+                             const double* const* halo, int nown, double* out) {
   long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   if (i >= (long long)nleaf * 512) return;
   int leaf = (int)(i / 512), c = (int)(i % 512);
@@ -266,7 +267,9 @@ __global__ void k_fmm_rhodot(const double* U, long long fstride, const omb::Leaf
   auto mom = [&](int comp, int cx, int cy, int cz) {  // padded coords
     int fm;
     long long a = omb::gather_addr(LI, bc, cx, cy, cz, fm);
-    double v = U[(long long)comp * fstride + a];
+    int src = (int)(a >> 9);  // a neighbour owned by another GPU: its owner's buffer (NVLink)
+    const double* p = (halo != nullptr && src >= nown) ? halo[src - nown] + (a & 511) : U + a;
+    double v = p[(long long)comp * fstride];
     return ((fm >> (comp - 1)) & 1) ? -v : v;
   };
   int px = x + 3, py = y + 3, pz = z + 3;
@@ -497,11 +500,11 @@ int omb_fmm_upward(const long long* parents, int np, const long long* children, 
 
 int omb_fmm_m2l(const long long* off, const unsigned long long* contrib, const double* D,
                 const unsigned char* cellcell, const double* M, double* L, long long ntarget, const long long* targets,
-                void* stream) {
+                const long long* subset, void* stream) {
   if (ntarget <= 0) return 0;
   unsigned nb = (unsigned)((ntarget + 127) / 128);
-  k_fmm_m2l<0><<<nb, 128, 0, (cudaStream_t)stream>>>(off, contrib, D, cellcell, M, L, ntarget, targets);
-  k_fmm_m2l<1><<<nb, 128, 0, (cudaStream_t)stream>>>(off, contrib, D, cellcell, M, L, ntarget, targets);
+  k_fmm_m2l<0><<<nb, 128, 0, (cudaStream_t)stream>>>(off, contrib, D, cellcell, M, L, ntarget, targets, subset);
+  k_fmm_m2l<1><<<nb, 128, 0, (cudaStream_t)stream>>>(off, contrib, D, cellcell, M, L, ntarget, targets, subset);
   cudaError_t e = cudaGetLastError();
   return e == cudaSuccess ? 0 : ferr("omb_fmm_m2l", e);
 }
@@ -523,12 +526,12 @@ int omb_fmm_fields(const double* L, const long long* cell_base, int nleaf, doubl
   return e == cudaSuccess ? 0 : ferr("omb_fmm_fields", e);
 }
 
-int omb_fmm_rhodot(const double* U, long long fstride, const OmbLeafInfo* info, int bc, int nleaf, double* out,
-                   void* stream) {
+int omb_fmm_rhodot(const double* U, long long fstride, const OmbLeafInfo* info, int bc, int nleaf,
+                   const double* const* halo, int nown, double* out, void* stream) {
   long long n = (long long)nleaf * 512;
   if (n == 0) return 0;
   k_fmm_rhodot<<<(unsigned)((n + 255) / 256), 256, 0, (cudaStream_t)stream>>>(U, fstride, (const omb::LeafInfo*)info,
-                                                                              bc, nleaf, out);
+                                                                              bc, nleaf, halo, nown, out);
   cudaError_t e = cudaGetLastError();
   return e == cudaSuccess ? 0 : ferr("omb_fmm_rhodot", e);
 }

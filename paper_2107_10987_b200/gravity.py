@@ -301,9 +301,11 @@ class B200FmmSolver:
         for _, par in self._up:
             _lib.check(lib.omb_fmm_upward(ptr(par), int(par.numel()), ptr(self._children), ptr(self._center),
                                           ptr(self._M), sh), "omb_fmm_upward")
+        sub = getattr(self, "_subset", None)  # partitioned: this rank's targets only
+        nt = int(sub.numel()) if sub is not None else int(self._targets.numel())
         _lib.check(lib.omb_fmm_m2l(ptr(self._off), ptr(self._contrib), ptr(self._D), ptr(self._cellcell),
-                                   ptr(self._M), ptr(self._L), int(self._targets.numel()), ptr(self._targets), sh),
-                   "omb_fmm_m2l")
+                                   ptr(self._M), ptr(self._L), nt, ptr(self._targets),
+                                   ptr(sub) if sub is not None else None, sh), "omb_fmm_m2l")
         for _, par in self._down:
             _lib.check(lib.omb_fmm_downward(ptr(par), int(par.numel()), ptr(self._children), ptr(self._center),
                                             ptr(self._L), sh), "omb_fmm_downward")
@@ -338,8 +340,71 @@ class B200FmmSolver:
         phi, rhodot = self._scratch[:n], self._scratch[n:2 * n]
         G = grav.reshape(4, -1)
         self._solve_into(U[:n], self._dx3_dev, phi, G[0], G[1], G[2], stream)
-        _lib.check(lib.omb_fmm_rhodot(ptr(U), fstride, ptr(info), bc, nleaf, ptr(rhodot), sh), "omb_fmm_rhodot")
+        _lib.check(lib.omb_fmm_rhodot(ptr(U), fstride, ptr(info), bc, nleaf, None, 0, ptr(rhodot), sh),
+                   "omb_fmm_rhodot")
         self._solve_into(rhodot, self._dx3_dev, G[3], phi, phi, phi, stream)
+
+    # -- leaf-partitioned runs (one rank per GPU) -------------------------------
+    def set_partition(self, part):
+        """This rank solves M2L only for its own leaves' entities (blocks and
+        cells) and the octree's internal nodes -- everything the downward pass
+        to its cells reads; the masses come from all ranks (all_gather).
+        Bitwise the single-GPU result for this rank's cells."""
+        import torch
+
+        if self.theta == 0.0:
+            raise NotImplementedError("theta = 0 with a partition")
+        t = self.table
+        b0, b1 = part.bounds[part.rank], part.bounds[part.rank + 1]
+        # a leaf's entities (its block hierarchy, then its cells) are contiguous, ending at cell_base + n^3;
+        # the octree's internal nodes belong to no leaf and every rank's downward pass needs them
+        n3 = t.n ** 3
+        per_leaf = (8 * n3 - 1) // 7
+        in_leaf = np.zeros(t.nentities, dtype=bool)
+        mine = np.zeros(t.nentities, dtype=bool)
+        for i, cb in enumerate(t.cell_base):
+            lo = cb + n3 - per_leaf
+            in_leaf[lo:cb + n3] = True
+            if b0 <= i < b1:
+                mine[lo:cb + n3] = True
+        tg = self._targets.cpu().numpy()
+        keep = mine[tg] | ~in_leaf[tg]
+        self._subset = torch.from_numpy(np.nonzero(keep)[0].astype(np.int64)).to(self.dev)
+        self._part = part
+        self._my_cell_base = torch.from_numpy(t.cell_base[b0:b1].copy()).to(self.dev)
+
+    def stage_fields_partitioned(self, U, fstride, info, bc, grav, halo, dist, group, stream=None):
+        """stage_fields for a rank of a leaf partition: rho and rho_dot of the owned
+        leaves are all-gathered, the solves run on this rank's targets, and gx, gy,
+        gz, dphi/dt of the owned leaves land in grav."""
+        import torch
+
+        p = self._part
+        lib, sh = self.lib, stream_handle(stream)
+        nown = p.nown
+        G = len(self.table.leaf_paths)
+        width = max(p.bounds[r + 1] - p.bounds[r] for r in range(p.world)) * 512
+        if getattr(self, "_gather", None) is None:
+            self._gather = torch.zeros(p.world * width * 2, dtype=torch.float64, device=self.dev)
+            self._rho_all = torch.zeros(2 * G * 512, dtype=torch.float64, device=self.dev)
+            self._sendb = torch.zeros(2 * width, dtype=torch.float64, device=self.dev)
+            self._scr = torch.empty(nown * 512, dtype=torch.float64, device=self.dev)
+        send = self._sendb
+        send[:nown * 512].copy_(U[:nown * 512])  # owned densities
+        _lib.check(lib.omb_fmm_rhodot(ptr(U), fstride, ptr(info), bc, nown, ptr(halo) if halo is not None else None,
+                                      nown, ptr(send[width:]), sh), "omb_fmm_rhodot")
+        dist.all_gather_into_tensor(self._gather, send, group=group)
+        ga = self._gather.view(p.world, 2, width)
+        for r in range(p.world):  # global leaf order: rank r owns [bounds[r], bounds[r+1])
+            a, b = p.bounds[r] * 512, p.bounds[r + 1] * 512
+            self._rho_all[a:b].copy_(ga[r, 0, :b - a])
+            self._rho_all[G * 512 + a:G * 512 + b].copy_(ga[r, 1, :b - a])
+        Gv = grav.reshape(4, -1)
+        for k, (rho, outs) in enumerate(((self._rho_all[:G * 512], (self._scr, Gv[0], Gv[1], Gv[2])),
+                                         (self._rho_all[G * 512:], (Gv[3], self._scr, self._scr, self._scr)))):
+            self._run(rho, self._dx3_dev, stream)
+            _lib.check(lib.omb_fmm_fields(ptr(self._L), ptr(self._my_cell_base), nown, *[ptr(o) for o in outs], sh),
+                       "omb_fmm_fields")
 
     # -- the reference's host API ----------------------------------------------
     def solve_density(self, tree, per_leaf_density=None):

@@ -124,9 +124,9 @@ class B200HydroStepper:
         # a device FMM (gravity.B200FmmSolver) is solved on the device every stage, in place
         self._dev_gravity = isinstance(gravity, B200FmmSolver)
         if self._dev_gravity:
-            if partition is not None:
-                raise NotImplementedError("the device FMM runs on one GPU (the whole tree's moments)")
             gravity.prepare(tree)
+            if partition is not None:
+                gravity.set_partition(partition)
             self._grav = T.zeros(4 * b.fstride, dtype=T.float64, device=dev)
         self._fresh = False  # device state was just uploaded from the host by cfl_dt
         self.dx_min = float(min(lf.subgrid.dx for lf in tree.leaves()))
@@ -343,8 +343,13 @@ class B200HydroStepper:
             if self._dev_gravity:
                 # device FMM on this stage's state (the reference's order: ghost fill, then
                 # gravity, then reconstruction -- step.py:106-113)
-                self.gravity.stage_fields(self._buf[cur], self.batch.fstride, self._info, self.batch.bc,
-                                          self.batch.L, self._grav, stream)
+                if self.part is not None:
+                    self.gravity.stage_fields_partitioned(
+                        self._buf[cur], self.batch.fstride, self._info, self.batch.bc, self._grav,
+                        self._halo_tab[cur] if self._p2p else None, self.dist, self.group, stream)
+                else:
+                    self.gravity.stage_fields(self._buf[cur], self.batch.fstride, self._info, self.batch.bc,
+                                              self.batch.L, self._grav, stream)
             d = self._stage_desc(cur, nxt, s, a, bw)
             if self._p2p:
                 d.halo = self._halo_tab[cur].data_ptr()

@@ -3,8 +3,9 @@
     python -m torch.distributed.run --nproc-per-node N --master-addr 127.0.0.1 tests/gpu_dist_check.py
 
 Each rank advances its leaf partition of the Sedov c1 tree (and of the
-smooth periodic case and two AMR trees, whose coarse/fine ghost sources and
-reflux face fluxes cross ranks) with the NCCL halo + flux-slot exchanges and compares its leaves
+smooth periodic case, two AMR trees, whose coarse/fine ghost sources and
+reflux face fluxes cross ranks, and a self-gravitating tree with the device FMM
+split over the ranks) with the halo reads / exchanges and compares its leaves
 with the single-process golden state bitwise; dt must equal the golden dt.
 Exit code 0 = parity."""
 
@@ -32,10 +33,14 @@ def main():
     dist.init_process_group("nccl", device_id=torch.device("cuda", lr))
     rank, world = dist.get_rank(), dist.get_world_size()
     bad = 0
-    for name, steps in (("sedov_c1", 3), ("smooth_periodic", 1), ("amr_reflux", 2), ("amr_sedov_small", 1)):
+    from paper_2107_10987_b200.gravity import B200FmmSolver
+
+    for name, steps in (("sedov_c1", 3), ("smooth_periodic", 1), ("amr_reflux", 2), ("amr_sedov_small", 1),
+                        ("gravity_step", 2)):
         t, g = case_tree(name)
         part = Partition(t, world, rank)
-        st = B200HydroStepper(t, EOS, HydroMode("new"), partition=part, max_run=2)
+        kw = dict(gravity=B200FmmSolver(0.5), omega=0.3) if name == "gravity_step" else {}
+        st = B200HydroStepper(t, EOS, HydroMode("new"), partition=part, max_run=2, **kw)
         for s in range(steps):
             dt = st.cfl_dt(0.4)
             if dt != float(g["dts"][s]):
