@@ -401,11 +401,13 @@ def gpu_arm(args, rank, world):
             t = torch.tensor([wall], dtype=torch.float64, device="cuda")
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             wall = float(t.item())
-        up = 6 * st2.batch.L * 512 * 8  # every batch leaf's interior (owned + halo)
+        up = 6 * st2.batch.ncompute * 512 * 8  # the owned leaves' interiors (halo leaves come from peers)
         down = 6 * st2.batch.ncompute * 512 * 8  # the owned leaves back into the host tree
         e2e = {"value": cells * args.e2e_steps / wall, "unit": UNIT,
                "h2d_bytes_per_step": up, "d2h_bytes_per_step": down + 2 * 8 + 4 + 6 * 8,
-               "steps": args.e2e_steps, "api": "B200HydroStepper.cfl_dt + rk3_step (host_sync=True)"}
+               "steps": args.e2e_steps, "api": "B200HydroStepper.cfl_dt + rk3_step (host_sync=True)",
+               "transfer": "mapped (GPU reads/writes the pinned host leaves)" if st2._mapped is not None
+               else "threads (host packing + DMA)"}
         del st2, t2, p2
         gc.collect()
         torch.cuda.empty_cache()

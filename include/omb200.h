@@ -143,6 +143,14 @@ int omb_host_upload(const double *const *leaf_u, int L, int n, long long fstride
                     int nchunks, void *stream);
 int omb_host_download(const double *dev, double *pinned, int L, int n, long long fstride, double *const *leaf_u,
                       int nchunks, void *stream);
+/* zero-copy host transfers (n = 8): leaf_u is a DEVICE array of L pointers to padded (6, 14, 14, 14)
+ * arrays in mapped pinned host memory (the stepper re-homes SubGrid.u into one pinned slab).  The GPU
+ * reads / writes them over PCIe in whole-cache-line spans (rows y = 3..10, all z); the ghost z of those
+ * rows go to / come from `stash` (L * 2304 doubles of device memory), so the host ghost cells are
+ * written back unchanged.  Both are asynchronous on `stream`. */
+int omb_host_gather(const double *const *leaf_u, int L, long long fstride, double *dev, double *stash, void *stream);
+int omb_host_scatter(const double *dev, const double *stash, int L, long long fstride, double *const *leaf_u,
+                     void *stream);
 /* multi-GPU AMR: gather rows idx[0..n) of length `row` into a contiguous message / scatter them back
  * (the exported face-flux slots the reflux of step.py:206-241 reads across ranks) */
 int omb_gather_rows(const double *src, long long row, const int *idx, int n, double *out, void *stream);

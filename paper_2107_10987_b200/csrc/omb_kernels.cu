@@ -1052,6 +1052,76 @@ int omb_host_download(const double* dev, double* pinned, int L, int n, long long
   return 0;
 }
 
+/* Zero-copy host transfers: the leaves' padded arrays live in mapped pinned host
+   memory (the stepper re-homes SubGrid.u into one pinned slab), and these kernels
+   read / write them over PCIe directly -- no host thread touches the data.  The unit
+   is a (leaf, field, x) span: rows y = 3..10 of the padded array with all 14 z
+   (896 B; whole host cache lines but at its two ends).  Its interior z = 3..10 go
+   to / come from the device state, its ghost z to / from `stash`, so the download
+   writes whole spans (no partial-line read-modify-write on the host) and leaves the
+   host ghost cells exactly as they were.  Replaces the per-leaf interior copies of
+   octomini's host state of record (mesh/tree.py:58-61). */
+constexpr int SPAN = 8 * 14;          // doubles per span
+constexpr int SPANS_PER_LEAF = 6 * 8;  // (field, x)
+constexpr int STASH_PER_SPAN = 8 * 6;  // ghost z per span
+
+__device__ __forceinline__ int span_src(int f, int x) { return ((f * 14 + x + 3) * 14 + 3) * 14; }
+
+__global__ void __launch_bounds__(256) k_host_gather(const double* const* __restrict__ leaf_u, unsigned total,
+                                                     long long fstride, double* __restrict__ dev,
+                                                     double* __restrict__ stash) {
+  for (unsigned i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
+    unsigned sp = i / SPAN, j = i - sp * SPAN;
+    unsigned leaf = sp / SPANS_PER_LEAF, fx = sp - leaf * SPANS_PER_LEAF;
+    int f = fx >> 3, x = fx & 7, y = j / 14, z = j - y * 14;
+    double v = __ldcs(leaf_u[leaf] + span_src(f, x) + j);
+    if (z >= 3 && z <= 10)
+      dev[f * fstride + leaf * 512LL + x * 64 + y * 8 + (z - 3)] = v;
+    else
+      stash[sp * STASH_PER_SPAN + y * 6 + (z < 3 ? z : z - 8)] = v;
+  }
+}
+
+__global__ void __launch_bounds__(256) k_host_scatter(const double* __restrict__ dev, const double* __restrict__ stash,
+                                                      unsigned total, long long fstride,
+                                                      double* const* __restrict__ leaf_u) {
+  for (unsigned i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
+    unsigned sp = i / SPAN, j = i - sp * SPAN;
+    unsigned leaf = sp / SPANS_PER_LEAF, fx = sp - leaf * SPANS_PER_LEAF;
+    int f = fx >> 3, x = fx & 7, y = j / 14, z = j - y * 14;
+    double v = (z >= 3 && z <= 10) ? dev[f * fstride + leaf * 512LL + x * 64 + y * 8 + (z - 3)]
+                                   : stash[sp * STASH_PER_SPAN + y * 6 + (z < 3 ? z : z - 8)];
+    __stcs(leaf_u[leaf] + span_src(f, x) + j, v);
+  }
+}
+
+static int host_xfer_grid(long long total) {
+  long long b = (total + 255) / 256;
+  return (int)(b < 148 * 8 ? b : 148 * 8);
+}
+
+int omb_host_gather(const double* const* leaf_u, int L, long long fstride, double* dev, double* stash,
+                    void* stream) {
+  if (int rc = lib_init()) return rc;
+  if (L <= 0) return 0;
+  if ((long long)L * SPANS_PER_LEAF * SPAN >= (1LL << 32)) return set_err("omb_host_gather: too many leaves");
+  unsigned total = (unsigned)L * SPANS_PER_LEAF * SPAN;
+  k_host_gather<<<host_xfer_grid(total), 256, 0, (cudaStream_t)stream>>>(leaf_u, total, fstride, dev, stash);
+  CK(cudaGetLastError(), "omb_host_gather launch");
+  return 0;
+}
+
+int omb_host_scatter(const double* dev, const double* stash, int L, long long fstride, double* const* leaf_u,
+                     void* stream) {
+  if (int rc = lib_init()) return rc;
+  if (L <= 0) return 0;
+  if ((long long)L * SPANS_PER_LEAF * SPAN >= (1LL << 32)) return set_err("omb_host_scatter: too many leaves");
+  unsigned total = (unsigned)L * SPANS_PER_LEAF * SPAN;
+  k_host_scatter<<<host_xfer_grid(total), 256, 0, (cudaStream_t)stream>>>(dev, stash, total, fstride, leaf_u);
+  CK(cudaGetLastError(), "omb_host_scatter launch");
+  return 0;
+}
+
 /* FP64 peak probe: launches blocks x 256 threads x 8 chains x iters DFMAs */
 int omb_fp64_peak(double* scratch, int blocks, int iters, void* stream) {
   k_dfma_peak<<<blocks, 256, 0, (cudaStream_t)stream>>>(scratch, iters);

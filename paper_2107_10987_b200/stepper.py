@@ -110,7 +110,7 @@ class B200HydroStepper:
         self._cfl_bad = T.empty(b.L, dtype=T.int32, device=dev)
         self._cfl_out = T.empty(2, dtype=T.float64, device=dev)
         self._cfl_badleaf = T.empty(1, dtype=T.int32, device=dev)
-        self._pinned = T.zeros(n, dtype=T.float64).pin_memory()
+        self._pinned = None  # staging buffer of the host-thread transfer path (allocated on first use)
         # AMR (coarse/fine neighbours): virtual-leaf ghost tasks, flux export slots, reflux lists
         self._amr_tasks = T.from_numpy(b.amr_tasks.reshape(-1).copy()).to(dev) if b.nvirtual else None
         self._flux = T.empty(max(1, b.flux_slots) * FLUX_SLOT_DOUBLES, dtype=T.float64, device=dev) \
@@ -129,6 +129,18 @@ class B200HydroStepper:
                 gravity.set_partition(partition)
             self._grav = T.zeros(4 * b.fstride, dtype=T.float64, device=dev)
         self._fresh = False  # device state was just uploaded from the host by cfl_dt
+        # host_sync transfers.  "mapped": the owned leaves' arrays move into mapped pinned
+        # memory that the GPU reads / writes directly (omb_host_gather/scatter) -- no host
+        # thread touches the data, which pays when several ranks share the host's memory
+        # bandwidth (4 ranks: 2x faster than the threads path).  "threads": the arrays stay
+        # in place and host threads pack them around DMA copies (1 rank: 8 % faster).
+        # OMB_HOST_XFER=mapped|threads overrides the choice.
+        self._mapped = None
+        xfer = os.environ.get("OMB_HOST_XFER", "auto")
+        if xfer == "auto":
+            xfer = "mapped" if int(os.environ.get("LOCAL_WORLD_SIZE", "1")) > 1 else "threads"
+        if host_sync and xfer == "mapped":
+            self._rehome()
         self.dx_min = float(min(lf.subgrid.dx for lf in tree.leaves()))
         self.nglobal = partition.G if partition is not None else b.L
         if partition is not None:
@@ -158,16 +170,60 @@ class B200HydroStepper:
     # -- host <-> device -------------------------------------------------------------
     TRANSFER_CHUNKS = 8
 
-    def upload(self):
-        """Copy the host leaves' interiors into the device state (pipelined:
-        host threads pack chunk c while chunk c-1 is on the copy engine)."""
+    SPAN_STASH = 2304  # ghost z doubles per leaf of the zero-copy spans (omb_host_gather)
+
+    def _rehome(self):
+        """Move the owned leaves' padded arrays (SubGrid.u) into one pinned host slab,
+        mapped into the device address space, and point each SubGrid at its slot
+        (values copied; the leaf's arrays stay ordinary C-contiguous float64 numpy
+        arrays).  Skipped for subgrid types without the reference's ``_u`` slot."""
         b = self.batch
+        nc = b.ncompute
+        sgs = [lf.subgrid for lf in b.leaves[:nc]]
+        if nc == 0 or not all(hasattr(sg, "_u") and sg.n == 8 for sg in sgs):
+            return
+        slab = torch.empty((nc, 6, 14, 14, 14), dtype=torch.float64, pin_memory=True)
+        arr = slab.numpy()
+        views = []
+        for k, sg in enumerate(sgs):
+            arr[k] = sg.u
+            sg._u = arr[k]
+            views.append(sg._u)
+        base = slab.data_ptr()
+        ptrs = torch.arange(nc, dtype=torch.int64) * (6 * 14 ** 3 * 8) + base
+        self._mapped = {"slab": slab, "views": views, "sgs": sgs, "ptrs": ptrs.to(self.dev),
+                        "stash": torch.empty(nc * self.SPAN_STASH, dtype=torch.float64, device=self.dev)}
+
+    def _mapped_check(self):
+        """Leaves whose array was replaced since the re-homing (a user assigned a new
+        SubGrid.u) are copied into their slab slot again."""
+        m = self._mapped
+        for k, (sg, v) in enumerate(zip(m["sgs"], m["views"])):
+            if sg._u is not v:
+                if sg._u is not None:
+                    v[...] = sg._u
+                sg._u = v
+
+    def upload(self):
+        """Copy the host leaves' interiors into the device state.  Mapped slab: one
+        kernel reads them over PCIe.  Otherwise pipelined: host threads pack chunk c
+        while chunk c-1 is on the copy engine.  Only owned leaves: halo leaves come
+        from their owners every stage."""
+        b = self.batch
+        if self._mapped is not None:
+            self._mapped_check()
+            m = self._mapped
+            _lib.check(self.lib.omb_host_gather(ptr(m["ptrs"]), b.ncompute, b.fstride, ptr(self._buf[self._state]),
+                                                ptr(m["stash"]), stream_handle(None)), "omb_host_gather")
+            return
+        if self._pinned is None:
+            self._pinned = torch.zeros(6 * b.fstride, dtype=torch.float64).pin_memory()
         if getattr(self, "_up_ev", None) is not None:
             self._up_ev.synchronize()  # the previous upload's copies still read the pinned buffer
         self._up_ev = torch.cuda.Event()
-        ptrs = b._leaf_ptrs(b.L)
+        ptrs = b._leaf_ptrs(b.ncompute)
         if ptrs is not None:
-            _lib.check(self.lib.omb_host_upload(ptrs.ctypes.data, b.L, 8, b.fstride, ptr(self._pinned),
+            _lib.check(self.lib.omb_host_upload(ptrs.ctypes.data, b.ncompute, 8, b.fstride, ptr(self._pinned),
                                                 ptr(self._buf[self._state]), self.TRANSFER_CHUNKS,
                                                 stream_handle(None)), "omb_host_upload")
         else:
@@ -177,9 +233,19 @@ class B200HydroStepper:
         self._up_ev.record()
 
     def download(self):
-        """Copy the device state back into the host leaves (the owned ones;
-        pipelined: chunk c is unpacked while chunk c+1 is in flight)."""
+        """Copy the device state back into the host leaves (the owned ones).  Mapped
+        slab: one kernel writes them over PCIe, then the stream is synchronised.
+        Otherwise pipelined: chunk c is unpacked while chunk c+1 is in flight."""
         b = self.batch
+        if self._mapped is not None:
+            self._mapped_check()
+            m = self._mapped
+            _lib.check(self.lib.omb_host_scatter(ptr(self._buf[self._state]), ptr(m["stash"]), b.ncompute,
+                                                 b.fstride, ptr(m["ptrs"]), stream_handle(None)), "omb_host_scatter")
+            torch.cuda.current_stream(self.dev).synchronize()
+            return
+        if self._pinned is None:
+            self._pinned = torch.zeros(6 * b.fstride, dtype=torch.float64).pin_memory()
         ptrs = b._leaf_ptrs(b.ncompute)
         if ptrs is not None:
             _lib.check(self.lib.omb_host_download(ptr(self._buf[self._state]), ptr(self._pinned), b.ncompute, 8,

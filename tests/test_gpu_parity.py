@@ -245,3 +245,39 @@ def test_synthetic_star_matches_oracle():
     # the atmosphere uses the dual-energy tau branch (pressure from tau**gamma): CUDA's pow is
     # not glibc's, so only the north_star tolerance is guaranteed here (bitwise elsewhere)
     assert rel_close(a, b, 1e-12) == 0
+
+
+def _ghosts(t):
+    out = []
+    for lf in t.sorted_leaves():
+        u = lf.subgrid.u.copy()
+        u[:, 3:11, 3:11, 3:11] = 0.0
+        out.append(u)
+    return np.stack(out)
+
+
+@pytest.mark.parametrize("xfer", ["mapped", "threads"])
+def test_host_transfer_paths(monkeypatch, xfer):
+    """Both host<->device transfer paths give the golden step, leave the host
+    ghost cells exactly as they were, and pick up leaf arrays a user replaced."""
+    monkeypatch.setenv("OMB_HOST_XFER", xfer)
+    t, g = case_tree("smooth_reflecting")
+    rng = np.random.default_rng(11)
+    for lf in t.sorted_leaves():  # distinctive host ghost values
+        u = lf.subgrid.u
+        keep = u[:, 3:11, 3:11, 3:11].copy()
+        u[...] = rng.standard_normal(u.shape)
+        u[:, 3:11, 3:11, 3:11] = keep
+    ghosts = _ghosts(t)
+    st = _stepper(t)
+    assert (st._mapped is not None) == (xfer == "mapped")
+    st.rk3_step(st.cfl_dt(0.4))
+    _check_state(t, g)
+    assert bitwise_mismatch(_ghosts(t), ghosts) == 0
+    for lf, a in zip(t.sorted_leaves(), g["init"]):  # new arrays holding the initial state
+        u = lf.subgrid.u.copy()
+        u[:, 3:11, 3:11, 3:11] = a
+        lf.subgrid._u = u
+    st.rk3_step(st.cfl_dt(0.4))
+    _check_state(t, g)
+    assert bitwise_mismatch(_ghosts(t), ghosts) == 0
