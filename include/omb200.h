@@ -143,6 +143,11 @@ int omb_host_upload(const double *const *leaf_u, int L, int n, long long fstride
                     int nchunks, void *stream);
 int omb_host_download(const double *dev, double *pinned, int L, int n, long long fstride, double *const *leaf_u,
                       int nchunks, void *stream);
+/* the download overlapped with the launch parts of the stage producing it: chunk c = leaves
+ * [bounds[c], bounds[c+1]) is copied on copy_stream after the cudaEvent_t ready[c] fires, then unpacked
+ * by the host threads; returns with the host arrays written */
+int omb_host_download_after(const double *dev, double *pinned, int n, long long fstride, double *const *leaf_u,
+                            int nchunks, const int *bounds, void *const *ready, void *copy_stream);
 /* zero-copy host transfers (n = 8): leaf_u is a DEVICE array of L pointers to padded (6, 14, 14, 14)
  * arrays in mapped pinned host memory (the stepper re-homes SubGrid.u into one pinned slab).  The GPU
  * reads / writes them over PCIe in whole-cache-line spans (rows y = 3..10, all z); the ghost z of those

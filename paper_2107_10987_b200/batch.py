@@ -264,6 +264,27 @@ class LeafBatch:
         self.run_leaf = np.array([i for r in runs for i in r], dtype=np.int32)
         self.nruns = len(runs)
 
+    def tail_parts(self, part_runs):
+        """Launch parts of a stage whose output is downloaded while it still runs:
+        the runs sorted by their last leaf, cut every ``part_runs`` runs.  Returns
+        (run_off, run_leaf, cuts, bounds): part k is runs [cuts[k], cuts[k+1]) of
+        the sorted table, and once parts 0..k are done every leaf below
+        bounds[k+1] is final (no later run writes it)."""
+        runs = self.runs
+        order = sorted(range(len(runs)), key=lambda r: max(runs[r]))
+        cuts = list(range(0, len(order), max(1, part_runs))) + [len(order)]
+        srt = [runs[r] for r in order]
+        run_off = np.zeros(len(srt) + 1, dtype=np.int32)
+        run_off[1:] = np.cumsum([len(r) for r in srt])
+        run_leaf = np.array([i for r in srt for i in r], dtype=np.int32)
+        # suffix minimum of the runs' first leaves
+        first = [min(r) for r in srt] + [self.ncompute]
+        suf = list(first)
+        for k in range(len(srt) - 1, -1, -1):
+            suf[k] = min(suf[k], suf[k + 1])
+        bounds = [0] + [suf[c] for c in cuts[1:]]
+        return run_off, run_leaf, cuts, bounds
+
     # -- host <-> packed state --------------------------------------------------
     def _leaf_ptrs(self, count):
         """Data pointers of the first ``count`` leaves' padded host arrays

@@ -1122,6 +1122,43 @@ int omb_host_scatter(const double* dev, const double* stash, int L, long long fs
   return 0;
 }
 
+/* The download overlapped with the stage that produces it: chunk c (leaves
+   [bounds[c], bounds[c+1])) is copied on copy_stream once `ready[c]` (an event
+   the caller recorded after the launch part that finishes those leaves) has
+   fired, and unpacked by the host threads as soon as its copy is done. */
+int omb_host_download_after(const double* dev, double* pinned, int n, long long fstride, double* const* leaf_u,
+                            int nchunks, const int* bounds, void* const* ready, void* copy_stream) {
+  if (int rc = lib_init()) return rc;
+  if (nchunks <= 0) return 0;
+  const int L = bounds[nchunks];
+  if (L <= 0) return 0;
+  const int nt = host_workers(L);
+  const long long n3 = (long long)n * n * n;
+  std::vector<cudaEvent_t> ev(nchunks);
+  for (int c = 0; c < nchunks; c++) {
+    CK(cudaEventCreateWithFlags(&ev[c], cudaEventDisableTiming), "omb_host_download_after event");
+    int lo = bounds[c], hi = bounds[c + 1];
+    CK(cudaStreamWaitEvent((cudaStream_t)copy_stream, (cudaEvent_t)ready[c], 0), "omb_host_download_after wait");
+    if (hi > lo)
+      CK(cudaMemcpy2DAsync(pinned + lo * n3, fstride * 8, dev + lo * n3, fstride * 8, (size_t)(hi - lo) * n3 * 8, 6,
+                           cudaMemcpyDeviceToHost, (cudaStream_t)copy_stream), "omb_host_download_after copy");
+    CK(cudaEventRecord(ev[c], (cudaStream_t)copy_stream), "omb_host_download_after record");
+  }
+  std::atomic<int> bad(0);
+  std::function<void(int)> work = [&](int t) {
+    for (int c = 0; c < nchunks; c++) {
+      if (cudaEventSynchronize(ev[c]) != cudaSuccess) { bad.store(1); return; }
+      int lo = bounds[c], hi = bounds[c + 1];
+      int a = lo + (int)((long long)(hi - lo) * t / nt), b = lo + (int)((long long)(hi - lo) * (t + 1) / nt);
+      for (int i = a; i < b; i++) copy_leaf(leaf_u[i], pinned, i, n, fstride, false);
+    }
+  };
+  host_pool().run(work, nt);
+  for (auto& e : ev) cudaEventDestroy(e);
+  if (bad.load()) return set_err("omb_host_download_after: copy failed");
+  return 0;
+}
+
 /* FP64 peak probe: launches blocks x 256 threads x 8 chains x iters DFMAs */
 int omb_fp64_peak(double* scratch, int blocks, int iters, void* stream) {
   k_dfma_peak<<<blocks, 256, 0, (cudaStream_t)stream>>>(scratch, iters);

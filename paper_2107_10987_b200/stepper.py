@@ -141,6 +141,21 @@ class B200HydroStepper:
             xfer = "mapped" if int(os.environ.get("LOCAL_WORLD_SIZE", "1")) > 1 else "threads"
         if host_sync and xfer == "mapped":
             self._rehome()
+        # threads path: the last stage is launched in parts of OMB_TAIL_WAVES waves of runs
+        # (runs sorted by leaf), and each part's leaves are copied back while the next part
+        # computes (omb_host_download_after); 0 = one launch, download afterwards
+        self._tail = None
+        waves = int(os.environ.get("OMB_TAIL_WAVES", "1"))
+        if (host_sync and self._mapped is None and waves > 0 and b.nvirtual == 0 and self._rleaf is None
+                and self._flux is None and not self._dev_gravity):
+            part_runs = (int(os.environ.get("OMB_TAIL_RUNS", "0"))  # (tests: small parts)
+                         or waves * torch.cuda.get_device_properties(dev).multi_processor_count)
+            if b.nruns > part_runs:
+                ro, rl, cuts, bounds = b.tail_parts(part_runs)
+                self._tail = {"run_off": T.from_numpy(ro).to(dev), "run_leaf": T.from_numpy(rl).to(dev),
+                              "cuts": cuts, "bounds": np.array(bounds, dtype=np.int32),
+                              "events": [torch.cuda.Event() for _ in range(len(cuts) - 1)],
+                              "stream": torch.cuda.Stream(dev)}
         self.dx_min = float(min(lf.subgrid.dx for lf in tree.leaves()))
         self.nglobal = partition.G if partition is not None else b.L
         if partition is not None:
@@ -254,6 +269,21 @@ class B200HydroStepper:
             return
         self._pinned.copy_(self._buf[self._state])
         b.unpack(self._pinned.numpy().reshape(6, b.L + b.nvirtual, 8, 8, 8))
+
+    def _download_tail(self):
+        b = self.batch
+        t = self._tail
+        ptrs = b._leaf_ptrs(b.ncompute)
+        if ptrs is None:
+            self.download()
+            return
+        if self._pinned is None:
+            self._pinned = torch.zeros(6 * b.fstride, dtype=torch.float64).pin_memory()
+        ev = (ctypes.c_void_p * len(t["events"]))(*[e.cuda_event for e in t["events"]])
+        _lib.check(self.lib.omb_host_download_after(ptr(self._buf[self._state]), ptr(self._pinned), 8, b.fstride,
+                                                    ptrs.ctypes.data, len(t["events"]), t["bounds"].ctypes.data,
+                                                    ev, ctypes.c_void_p(t["stream"].cuda_stream)),
+                   "omb_host_download_after")
 
     def state_tensor(self):
         return self._buf[self._state]
@@ -373,10 +403,12 @@ class B200HydroStepper:
             contact=int(self.mode.contact_detection), amax_bits=acc.data_ptr() + 8 * s,
             fallback=acc.data_ptr() + 8 * (3 + s), flux=ptr(self._flux))
 
-    def launch_step(self, dt=None, stream=None, events=None):
+    def launch_step(self, dt=None, stream=None, events=None, tail=False):
         """Enqueue the three stages (no host sync) and advance the device state.
-        dt=None uses the device dt written by the last cfl launch.  Returns
-        (buffer of the step-start state, [buffer of each stage's output])."""
+        dt=None uses the device dt written by the last cfl launch; tail=True
+        launches the last stage in the parts of ``self._tail`` (an event after
+        each).  Returns (buffer of the step-start state, [buffer of each stage's
+        output])."""
         if dt is not None:
             self._dt.fill_(float(dt))
         self._acc.zero_()
@@ -422,7 +454,17 @@ class B200HydroStepper:
                 d.nown = self.batch.ncompute
             if events is not None:
                 events[s][0].record()
-            _lib.check(self.lib.omb_stage(ctypes.byref(d), sh), "omb_stage")
+            if tail and s == 2:
+                t = self._tail
+                cuts = t["cuts"]
+                for k in range(len(cuts) - 1):
+                    d.run_off = ptr(t["run_off"]) + 4 * cuts[k]
+                    d.run_leaf = ptr(t["run_leaf"])
+                    d.nruns = cuts[k + 1] - cuts[k]
+                    _lib.check(self.lib.omb_stage(ctypes.byref(d), sh), "omb_stage")
+                    t["events"][k].record(stream)
+            else:
+                _lib.check(self.lib.omb_stage(ctypes.byref(d), sh), "omb_stage")
             if events is not None:
                 events[s][1].record()
             if getattr(self, "_fsend", None) is not None:
@@ -462,7 +504,10 @@ class B200HydroStepper:
         if self.host_sync and not self._fresh:
             self.upload()
         self._fresh = False
-        start, outs = self.launch_step(dt)
+        tail = self.host_sync and self._tail is not None
+        start, outs = self.launch_step(dt, tail=tail)
+        if tail:
+            self._download_tail()  # the result, copied back while its last stage runs
         self._reduce_stats()
         acc = self._acc.cpu().numpy()
         amax = acc[:3].view(np.float64)
@@ -484,6 +529,6 @@ class B200HydroStepper:
                     f"exceeds {self.abort_courant}")
             u_prev = outs[s]
         self.stats = stats
-        if self.host_sync:
+        if self.host_sync and not tail:
             self.download()
         return stats

@@ -281,3 +281,23 @@ def test_host_transfer_paths(monkeypatch, xfer):
     st.rk3_step(st.cfl_dt(0.4))
     _check_state(t, g)
     assert bitwise_mismatch(_ghosts(t), ghosts) == 0
+
+
+@pytest.mark.parametrize("part_runs", [1, 3, 7])
+def test_overlapped_download(monkeypatch, part_runs):
+    """The last stage launched in parts with each part's leaves copied back while
+    the next computes gives the golden step (and the CFL-abort rollback still holds)."""
+    monkeypatch.setenv("OMB_HOST_XFER", "threads")
+    monkeypatch.setenv("OMB_TAIL_RUNS", str(part_runs))
+    t, g = case_tree("sedov_c1")
+    st = _stepper(t)
+    assert st._tail is not None and len(st._tail["cuts"]) > 2
+    stats = st.rk3_step(st.cfl_dt(0.4))
+    _check_state(t, g)
+    assert stats.amax == float(g["amax"][0])
+    before = state_of(t).copy()
+    from paper_2107_10987_b200 import NumericsError
+
+    with pytest.raises(NumericsError):
+        st.rk3_step(dt=10.0)
+    assert bitwise_mismatch(state_of(t), before) == 0
