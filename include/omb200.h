@@ -202,6 +202,12 @@ int omb_fmm_upward(const long long *parents, int np, const long long *children, 
 int omb_fmm_m2l(const long long *off, const unsigned long long *contrib, const double *D,
                 const unsigned char *cellcell, const double *M, double *L, long long ntarget,
                 const long long *targets, const long long *subset /* NULL: all ntarget targets */, void *stream);
+/* one of the two M2L passes (part 0: L0..L3, part 1: L4..L19) over its own CSR lists; cellcell = NULL
+ * declares a list without cell-cell contributions (part 1 needs none of them: the solver passes it the
+ * subsequence of the other contributions, same order, so the result is unchanged bit for bit) */
+int omb_fmm_m2l_part(int part, const long long *off, const unsigned long long *contrib, const double *D,
+                     const unsigned char *cellcell, const double *M, double *L, long long ntarget,
+                     const long long *targets, const long long *subset, void *stream);
 int omb_fmm_downward(const long long *parents, int np, const long long *children, const double *center, double *L,
                      void *stream);
 int omb_fmm_fields(const double *L, const long long *cell_base, int nleaf, double *phi, double *gx, double *gy,

@@ -125,19 +125,25 @@ __global__ void __launch_bounds__(128, 4) k_fmm_m2l(const long long* off, const 
   long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   if (k >= ntarget) return;
   long long ti = subset ? subset[k] : k;  // a rank of a partitioned run solves only its targets
+  if (off[ti] == off[ti + 1]) return;  // nothing to add (the filtered PART 1 lists)
   long long x = targets[ti];
   constexpr int K0 = PART == 0 ? 0 : 4, KN = PART == 0 ? 4 : 16;
   double l[KN];
 #pragma unroll
   for (int k = 0; k < KN; k++) l[k] = L[x * NC + K0 + k];
-  for (long long q = off[ti]; q < off[ti + 1]; q++) {
-    unsigned long long w = __ldg(contrib + q);
+  // software pipeline over the (dependent-load) chain: the next contribution's
+  // word is loaded while this one is processed
+  const long long q1 = off[ti + 1];
+  unsigned long long wn = off[ti] < q1 ? __ldg(contrib + off[ti]) : 0ull;
+  for (long long q = off[ti]; q < q1; q++) {
+    unsigned long long w = wn;
+    if (q + 1 < q1) wn = __ldg(contrib + q + 1);
     long long src = (long long)(w & 0xFFFFFFFFFFull);
     long long g = (long long)((w >> 40) & 0x7FFFFFull);
     int flip = (int)(w >> 63);
     const double* Dg = D + (g * 2 + flip) * NC;
     const double* Ms = M + src * NC;
-    if (cellcell[g]) {
+    if (cellcell && cellcell[g]) {  // (null: a list without cell-cell contributions)
       // L[eb,0] += ma*D0; L[eb,c] += ma*D_c; L[ea,0] += mb*D0; L[ea,c] += mb*(-D_c)
       // (the flipped D holds -D_c: x*(-d) is the reference's mb*(-D1))
       if (PART == 0) {
@@ -507,6 +513,19 @@ int omb_fmm_m2l(const long long* off, const unsigned long long* contrib, const d
   k_fmm_m2l<1><<<nb, 128, 0, (cudaStream_t)stream>>>(off, contrib, D, cellcell, M, L, ntarget, targets, subset);
   cudaError_t e = cudaGetLastError();
   return e == cudaSuccess ? 0 : ferr("omb_fmm_m2l", e);
+}
+
+int omb_fmm_m2l_part(int part, const long long* off, const unsigned long long* contrib, const double* D,
+                     const unsigned char* cellcell, const double* M, double* L, long long ntarget,
+                     const long long* targets, const long long* subset, void* stream) {
+  if (ntarget <= 0) return 0;
+  unsigned nb = (unsigned)((ntarget + 127) / 128);
+  if (part == 0)
+    k_fmm_m2l<0><<<nb, 128, 0, (cudaStream_t)stream>>>(off, contrib, D, cellcell, M, L, ntarget, targets, subset);
+  else
+    k_fmm_m2l<1><<<nb, 128, 0, (cudaStream_t)stream>>>(off, contrib, D, cellcell, M, L, ntarget, targets, subset);
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? 0 : ferr("omb_fmm_m2l_part", e);
 }
 
 int omb_fmm_downward(const long long* parents, int np, const long long* children, const double* center, double* L,

@@ -242,6 +242,17 @@ class B200FmmSolver:
         self._cellcell = T.from_numpy((a_cell & b_cell).astype(np.uint8)).to(dev)
         self._off = T.from_numpy(off).to(dev)
         self._contrib = T.from_numpy(contrib.view(np.int64)).to(dev)
+        del contrib
+        # the L4..L19 pass needs no cell-cell contribution (90 % of them at theta 0.5): its
+        # lists are the subsequence of the others, same order, CSR over the same targets
+        g = (self._contrib >> 40) & 0x7FFFFF
+        keep = self._cellcell[g] == 0
+        del g
+        cs = T.cumsum(keep, 0)
+        self._off1 = T.cat([T.zeros(1, dtype=T.int64, device=dev), cs])[self._off]
+        del cs
+        self._contrib1 = self._contrib[keep]
+        del keep
         self._targets = T.from_numpy(targets.astype(np.int64)).to(dev)
         self._cell_base = T.from_numpy(t.cell_base).to(dev)
         lv = t.level
@@ -303,9 +314,11 @@ class B200FmmSolver:
                                           ptr(self._M), sh), "omb_fmm_upward")
         sub = getattr(self, "_subset", None)  # partitioned: this rank's targets only
         nt = int(sub.numel()) if sub is not None else int(self._targets.numel())
-        _lib.check(lib.omb_fmm_m2l(ptr(self._off), ptr(self._contrib), ptr(self._D), ptr(self._cellcell),
-                                   ptr(self._M), ptr(self._L), nt, ptr(self._targets),
-                                   ptr(sub) if sub is not None else None, sh), "omb_fmm_m2l")
+        for part, off, contrib, cc in ((0, self._off, self._contrib, ptr(self._cellcell)),
+                                       (1, self._off1, self._contrib1, None)):
+            _lib.check(lib.omb_fmm_m2l_part(part, ptr(off), ptr(contrib), ptr(self._D), cc, ptr(self._M),
+                                            ptr(self._L), nt, ptr(self._targets),
+                                            ptr(sub) if sub is not None else None, sh), "omb_fmm_m2l_part")
         for _, par in self._down:
             _lib.check(lib.omb_fmm_downward(ptr(par), int(par.numel()), ptr(self._children), ptr(self._center),
                                             ptr(self._L), sh), "omb_fmm_downward")
@@ -320,9 +333,9 @@ class B200FmmSolver:
         return o[:, :n]
 
     def launches_per_stage(self):
-        """Kernels of one stage_fields call: 2 solves x (masses, upward levels, M2L,
-        downward levels, fields) + the -div(momentum) source."""
-        per = 2 if self.theta == 0.0 else 3 + len(self._up) + len(self._down)
+        """Kernels of one stage_fields call: 2 solves x (masses, upward levels, the two
+        M2L passes, downward levels, fields) + the -div(momentum) source."""
+        per = 2 if self.theta == 0.0 else 4 + len(self._up) + len(self._down)
         return 2 * per + 1
 
     def stage_fields(self, U, fstride, info, bc, nleaf, grav, stream=None):
