@@ -207,7 +207,9 @@ int omb_fmm_m2l(const long long *off, const unsigned long long *contrib, const d
  * subsequence of the other contributions, same order, so the result is unchanged bit for bit) */
 int omb_fmm_m2l_part(int part, const long long *off, const unsigned long long *contrib, const double *D,
                      const unsigned char *cellcell, const double *M, double *L, long long ntarget,
-                     const long long *targets, const long long *subset, void *stream);
+                     const long long *targets, const long long *subset, double *m0 /* NULL, or nentities doubles:
+                     part 0 first copies the monopoles there and reads cell-cell masses from it */,
+                     long long nentities, void *stream);
 int omb_fmm_downward(const long long *parents, int np, const long long *children, const double *center, double *L,
                      void *stream);
 int omb_fmm_fields(const double *L, const long long *cell_base, int nleaf, double *phi, double *gx, double *gy,

@@ -67,7 +67,7 @@ def load():
     L.omb_fmm_direct.argtypes = [vp, vp, vp, vp, vp, i, vp, vp, vp, vp, vp]
     L.omb_fmm_upward.argtypes = [vp, i, vp, vp, vp, vp]
     L.omb_fmm_m2l.argtypes = [vp, vp, vp, vp, vp, vp, ll, vp, vp, vp]
-    L.omb_fmm_m2l_part.argtypes = [i, vp, vp, vp, vp, vp, vp, ll, vp, vp, vp]
+    L.omb_fmm_m2l_part.argtypes = [i, vp, vp, vp, vp, vp, vp, ll, vp, vp, vp, ll, vp]
     L.omb_fmm_downward.argtypes = [vp, i, vp, vp, vp, vp]
     L.omb_fmm_fields.argtypes = [vp, vp, i, vp, vp, vp, vp, vp]
     L.omb_fmm_rhodot.argtypes = [vp, ll, vp, i, i, vp, i, vp, vp]

@@ -121,7 +121,8 @@ template <int PART>
 __global__ void __launch_bounds__(128, 4) k_fmm_m2l(const long long* off, const unsigned long long* contrib,
                                                     const double* D /*[G][2][20]*/, const unsigned char* cellcell,
                                                     const double* M, double* L, long long ntarget,
-                                                    const long long* targets, const long long* subset) {
+                                                    const long long* targets, const long long* subset,
+                                                    const double* M0c = nullptr) {
   long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   if (k >= ntarget) return;
   long long ti = subset ? subset[k] : k;  // a rank of a partitioned run solves only its targets
@@ -147,7 +148,9 @@ __global__ void __launch_bounds__(128, 4) k_fmm_m2l(const long long* off, const 
       // L[eb,0] += ma*D0; L[eb,c] += ma*D_c; L[ea,0] += mb*D0; L[ea,c] += mb*(-D_c)
       // (the flipped D holds -D_c: x*(-d) is the reference's mb*(-D1))
       if (PART == 0) {
-        double m = __ldg(Ms);
+        // the monopole from the compact mass array when given (8 B per entity: L2-resident,
+        // where the 160 B moment records are not)
+        double m = M0c ? __ldg(M0c + src) : __ldg(Ms);
         l[0] += m * __ldg(Dg);
 #pragma unroll
         for (int c = 0; c < 3; c++) l[1 + c] += m * __ldg(Dg + 1 + c);
@@ -515,13 +518,24 @@ int omb_fmm_m2l(const long long* off, const unsigned long long* contrib, const d
   return e == cudaSuccess ? 0 : ferr("omb_fmm_m2l", e);
 }
 
+__global__ void k_fmm_m0(const double* __restrict__ M, long long n, double* __restrict__ M0c) {
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < n; e += (long long)gridDim.x * blockDim.x)
+    M0c[e] = M[e * NC];
+}
+
 int omb_fmm_m2l_part(int part, const long long* off, const unsigned long long* contrib, const double* D,
                      const unsigned char* cellcell, const double* M, double* L, long long ntarget,
-                     const long long* targets, const long long* subset, void* stream) {
+                     const long long* targets, const long long* subset, double* m0, long long nentities,
+                     void* stream) {
   if (ntarget <= 0) return 0;
   unsigned nb = (unsigned)((ntarget + 127) / 128);
+  if (part == 0 && m0 && nentities > 0) {
+    long long b = (nentities + 255) / 256;
+    k_fmm_m0<<<(unsigned)(b < 148 * 16 ? b : 148 * 16), 256, 0, (cudaStream_t)stream>>>(M, nentities, m0);
+  }
   if (part == 0)
-    k_fmm_m2l<0><<<nb, 128, 0, (cudaStream_t)stream>>>(off, contrib, D, cellcell, M, L, ntarget, targets, subset);
+    k_fmm_m2l<0><<<nb, 128, 0, (cudaStream_t)stream>>>(off, contrib, D, cellcell, M, L, ntarget, targets, subset,
+                                                       m0);
   else
     k_fmm_m2l<1><<<nb, 128, 0, (cudaStream_t)stream>>>(off, contrib, D, cellcell, M, L, ntarget, targets, subset);
   cudaError_t e = cudaGetLastError();

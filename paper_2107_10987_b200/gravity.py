@@ -261,6 +261,7 @@ class B200FmmSolver:
         self._down = [(L, T.from_numpy(parents[L]).to(dev)) for L in sorted(parents) if len(parents[L])]
         self._dx3_dev = T.tensor([lf.subgrid.dx ** 3 for lf in tree.sorted_leaves()], dtype=T.float64, device=dev)
         self._M = T.zeros(t.nentities * NCOMP, dtype=T.float64, device=dev)
+        self._M0c = T.zeros(t.nentities, dtype=T.float64, device=dev)  # compact monopoles (M2L pass 0)
         self._L = T.zeros_like(self._M)
         self._signature = sig
 
@@ -318,7 +319,8 @@ class B200FmmSolver:
                                        (1, self._off1, self._contrib1, None)):
             _lib.check(lib.omb_fmm_m2l_part(part, ptr(off), ptr(contrib), ptr(self._D), cc, ptr(self._M),
                                             ptr(self._L), nt, ptr(self._targets),
-                                            ptr(sub) if sub is not None else None, sh), "omb_fmm_m2l_part")
+                                            ptr(sub) if sub is not None else None, ptr(self._M0c),
+                                            self.table.nentities, sh), "omb_fmm_m2l_part")
         for _, par in self._down:
             _lib.check(lib.omb_fmm_downward(ptr(par), int(par.numel()), ptr(self._children), ptr(self._center),
                                             ptr(self._L), sh), "omb_fmm_downward")
@@ -333,9 +335,10 @@ class B200FmmSolver:
         return o[:, :n]
 
     def launches_per_stage(self):
-        """Kernels of one stage_fields call: 2 solves x (masses, upward levels, the two
-        M2L passes, downward levels, fields) + the -div(momentum) source."""
-        per = 2 if self.theta == 0.0 else 4 + len(self._up) + len(self._down)
+        """Kernels of one stage_fields call: 2 solves x (masses, upward levels, the
+        monopole copy and the two M2L passes, downward levels, fields) + the
+        -div(momentum) source."""
+        per = 2 if self.theta == 0.0 else 5 + len(self._up) + len(self._down)
         return 2 * per + 1
 
     def stage_fields(self, U, fstride, info, bc, nleaf, grav, stream=None):
