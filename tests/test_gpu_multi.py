@@ -36,7 +36,10 @@ def test_partitioned_steps_match_single_process(world, halo):
         port = s.getsockname()[1]
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nproc-per-node", str(world), "--master-addr",
            "127.0.0.1", "--master-port", str(port), os.path.join(HERE, "gpu_dist_check.py")]
-    env = dict(os.environ, OMB_HALO=halo)
+    # host transfers: the mapped pinned leaves with p2p; host threads + the last stage in small
+    # launch parts with its download overlapped (OMB_TAIL_RUNS) with nccl
+    xfer = {"OMB_HOST_XFER": "mapped"} if halo == "p2p" else {"OMB_HOST_XFER": "threads", "OMB_TAIL_RUNS": "2"}
+    env = dict(os.environ, OMB_HALO=halo, **xfer)
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=900, env=env)
     assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
     assert f"multi-GPU parity on {world} ranks: OK" in r.stdout + r.stderr
