@@ -47,7 +47,7 @@ typedef struct {
     long long fstride;    /* doubles between fields (>= nleaves*512) */
     const OmbLeafInfo *info;
     const int *run_off;   /* [nruns+1] offsets into run_leaf */
-    const int *run_leaf;  /* leaf indices of each run, consecutive along +x at one level */
+    const int *run_leaf;  /* leaf indices of each run (1..4 leaves), consecutive along +x at one level */
     int nruns;
     const double *dt;     /* device scalar */
     double a, b;          /* stage weights (SSP_RK3_STAGES) */
@@ -150,9 +150,9 @@ int omb_host_download_after(const double *dev, double *pinned, int n, long long 
                             int nchunks, const int *bounds, void *const *ready, void *copy_stream);
 /* zero-copy host transfers (n = 8): leaf_u is a DEVICE array of L pointers to padded (6, 14, 14, 14)
  * arrays in mapped pinned host memory (the stepper re-homes SubGrid.u into one pinned slab).  The GPU
- * reads / writes them over PCIe in whole-cache-line spans (rows y = 3..10, all z); the ghost z of those
- * rows go to / come from `stash` (L * 2304 doubles of device memory), so the host ghost cells are
- * written back unchanged.  Both are asynchronous on `stream`. */
+ * reads / writes them over PCIe in whole 64 B lines: per (field, x), rows y = 3..10 with all z, widened
+ * to the 15 lines they touch; the ghost z of those rows and the widening's edge doubles go to / come
+ * from `stash` (L * 2688 doubles of device memory), so the host ghost cells are written back unchanged.  Both are asynchronous on `stream`. */
 int omb_host_gather(const double *const *leaf_u, int L, long long fstride, double *dev, double *stash, void *stream);
 int omb_host_scatter(const double *dev, const double *stash, int L, long long fstride, double *const *leaf_u,
                      void *stream);

@@ -79,6 +79,9 @@ def neighbor_table(tree, leaves, allow_amr=False):
     return out
 
 
+MAX_RUN = 4  # leaves per run: the stage kernel's shared-memory LeafInfo slots (omb_stage.cuh Smem::LINFO)
+
+
 class LeafBatch:
     """Device batch of leaves.  The first ``ncompute`` leaves are advanced by
     the stage kernel; the rest (multi-GPU halo leaves owned by other ranks)
@@ -86,6 +89,9 @@ class LeafBatch:
     table in global indices with ``gids`` the global index of each leaf."""
 
     def __init__(self, tree, max_run=4, leaves=None, ncompute=None, gnbr=None, gids=None, extra_exporters=()):
+        if not 1 <= max_run <= MAX_RUN:
+            raise ValueError(f"max_run must be in [1, {MAX_RUN}] (the stage kernel stages at most "
+                             f"{MAX_RUN} leaf descriptors per run), got {max_run}")
         self.tree = tree
         self.n = tree.n
         if self.n != 8:

@@ -1056,29 +1056,46 @@ int omb_host_download(const double* dev, double* pinned, int L, int n, long long
    memory (the stepper re-homes SubGrid.u into one pinned slab), and these kernels
    read / write them over PCIe directly -- no host thread touches the data.  The unit
    is a (leaf, field, x) span: rows y = 3..10 of the padded array with all 14 z
-   (896 B; whole host cache lines but at its two ends).  Its interior z = 3..10 go
-   to / come from the device state, its ghost z to / from `stash`, so the download
-   writes whole spans (no partial-line read-modify-write on the host) and leaves the
-   host ghost cells exactly as they were.  Replaces the per-leaf interior copies of
-   octomini's host state of record (mesh/tree.py:58-61). */
-constexpr int SPAN = 8 * 14;          // doubles per span
+   (112 doubles), widened to the whole 64 B host lines it touches -- it starts 2 or 6
+   doubles into a line, so its hull is exactly 15 lines (120 doubles).  The span's
+   interior z = 3..10 go to / come from the device state; its ghost z and the hull's
+   edge doubles (neighbouring rows of the padded array) to / from `stash`, so the
+   download writes whole lines only (no partial-line read-modify-write on the host)
+   and leaves every host ghost cell exactly as it was.  Replaces the per-leaf
+   interior copies of octomini's host state of record (mesh/tree.py:58-61). */
+constexpr int HULL = 120;              // doubles per span hull (15 lines of 64 B)
 constexpr int SPANS_PER_LEAF = 6 * 8;  // (field, x)
-constexpr int STASH_PER_SPAN = 8 * 6;  // ghost z per span
+constexpr int STASH_PER_SPAN = 56;     // 8 rows x 6 ghost z + 8 edge doubles
 
 __device__ __forceinline__ int span_src(int f, int x) { return ((f * 14 + x + 3) * 14 + 3) * 14; }
+
+// hull position j of span (f, x): its offset in the leaf's padded array, and
+// either the interior cell (x, y, z - 3) (returns true) or the stash slot
+__device__ __forceinline__ bool hull_pos(int f, int x, int j, int& src, int& cell, int& slot) {
+  int s0 = span_src(f, x), r = s0 & 7;  // 2 or 6 (leaf arrays are 64 B aligned)
+  src = s0 - r + j;
+  int p = j - r;  // position inside the span
+  if (p < 0) { slot = j; return false; }
+  if (p >= 8 * 14) { slot = r + 48 + (p - 8 * 14); return false; }
+  int y = p / 14, z = p - y * 14;
+  if (z >= 3 && z <= 10) { cell = x * 64 + y * 8 + (z - 3); return true; }
+  slot = r + y * 6 + (z < 3 ? z : z - 8);
+  return false;
+}
 
 __global__ void __launch_bounds__(256) k_host_gather(const double* const* __restrict__ leaf_u, unsigned total,
                                                      long long fstride, double* __restrict__ dev,
                                                      double* __restrict__ stash) {
   for (unsigned i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
-    unsigned sp = i / SPAN, j = i - sp * SPAN;
+    unsigned sp = i / HULL, j = i - sp * HULL;
     unsigned leaf = sp / SPANS_PER_LEAF, fx = sp - leaf * SPANS_PER_LEAF;
-    int f = fx >> 3, x = fx & 7, y = j / 14, z = j - y * 14;
-    double v = __ldcs(leaf_u[leaf] + span_src(f, x) + j);
-    if (z >= 3 && z <= 10)
-      dev[f * fstride + leaf * 512LL + x * 64 + y * 8 + (z - 3)] = v;
+    int f = fx >> 3, x = fx & 7, src, cell, slot;
+    bool in = hull_pos(f, x, (int)j, src, cell, slot);
+    double v = __ldcs(leaf_u[leaf] + src);
+    if (in)
+      dev[f * fstride + leaf * 512LL + cell] = v;
     else
-      stash[sp * STASH_PER_SPAN + y * 6 + (z < 3 ? z : z - 8)] = v;
+      stash[sp * STASH_PER_SPAN + slot] = v;
   }
 }
 
@@ -1086,12 +1103,12 @@ __global__ void __launch_bounds__(256) k_host_scatter(const double* __restrict__
                                                       unsigned total, long long fstride,
                                                       double* const* __restrict__ leaf_u) {
   for (unsigned i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
-    unsigned sp = i / SPAN, j = i - sp * SPAN;
+    unsigned sp = i / HULL, j = i - sp * HULL;
     unsigned leaf = sp / SPANS_PER_LEAF, fx = sp - leaf * SPANS_PER_LEAF;
-    int f = fx >> 3, x = fx & 7, y = j / 14, z = j - y * 14;
-    double v = (z >= 3 && z <= 10) ? dev[f * fstride + leaf * 512LL + x * 64 + y * 8 + (z - 3)]
-                                   : stash[sp * STASH_PER_SPAN + y * 6 + (z < 3 ? z : z - 8)];
-    __stcs(leaf_u[leaf] + span_src(f, x) + j, v);
+    int f = fx >> 3, x = fx & 7, src, cell, slot;
+    bool in = hull_pos(f, x, (int)j, src, cell, slot);
+    double v = in ? dev[f * fstride + leaf * 512LL + cell] : stash[sp * STASH_PER_SPAN + slot];
+    __stcs(leaf_u[leaf] + src, v);
   }
 }
 
@@ -1104,8 +1121,8 @@ int omb_host_gather(const double* const* leaf_u, int L, long long fstride, doubl
                     void* stream) {
   if (int rc = lib_init()) return rc;
   if (L <= 0) return 0;
-  if ((long long)L * SPANS_PER_LEAF * SPAN >= (1LL << 32)) return set_err("omb_host_gather: too many leaves");
-  unsigned total = (unsigned)L * SPANS_PER_LEAF * SPAN;
+  if ((long long)L * SPANS_PER_LEAF * HULL >= (1LL << 32)) return set_err("omb_host_gather: too many leaves");
+  unsigned total = (unsigned)L * SPANS_PER_LEAF * HULL;
   k_host_gather<<<host_xfer_grid(total), 256, 0, (cudaStream_t)stream>>>(leaf_u, total, fstride, dev, stash);
   CK(cudaGetLastError(), "omb_host_gather launch");
   return 0;
@@ -1115,8 +1132,8 @@ int omb_host_scatter(const double* dev, const double* stash, int L, long long fs
                      void* stream) {
   if (int rc = lib_init()) return rc;
   if (L <= 0) return 0;
-  if ((long long)L * SPANS_PER_LEAF * SPAN >= (1LL << 32)) return set_err("omb_host_scatter: too many leaves");
-  unsigned total = (unsigned)L * SPANS_PER_LEAF * SPAN;
+  if ((long long)L * SPANS_PER_LEAF * HULL >= (1LL << 32)) return set_err("omb_host_scatter: too many leaves");
+  unsigned total = (unsigned)L * SPANS_PER_LEAF * HULL;
   k_host_scatter<<<host_xfer_grid(total), 256, 0, (cudaStream_t)stream>>>(dev, stash, total, fstride, leaf_u);
   CK(cudaGetLastError(), "omb_host_scatter launch");
   return 0;

@@ -141,13 +141,15 @@ class B200HydroStepper:
             xfer = "mapped" if int(os.environ.get("LOCAL_WORLD_SIZE", "1")) > 1 else "threads"
         if host_sync and xfer == "mapped":
             self._rehome()
-        # threads path: the last stage is launched in parts of OMB_TAIL_WAVES waves of runs
-        # (runs sorted by leaf), and each part's leaves are copied back while the next part
-        # computes (omb_host_download_after); 0 = one launch, download afterwards
+        # the last stage is launched in parts of OMB_TAIL_WAVES waves of runs (runs sorted by
+        # leaf), and each part's leaves are copied back while the next part computes: by the
+        # copy engine + host threads (omb_host_download_after), or, mapped, by a scatter kernel
+        # on a side stream (OMB_MAPPED_TAIL=0: one scatter after the stage); 0 = one launch
         self._tail = None
         waves = int(os.environ.get("OMB_TAIL_WAVES", "1"))
-        if (host_sync and self._mapped is None and waves > 0 and b.nvirtual == 0 and self._rleaf is None
-                and self._flux is None and not self._dev_gravity):
+        mapped_tail = os.environ.get("OMB_MAPPED_TAIL", "1") == "1"
+        if (host_sync and (self._mapped is None or mapped_tail) and waves > 0 and b.nvirtual == 0
+                and self._rleaf is None and self._flux is None and not self._dev_gravity):
             part_runs = (int(os.environ.get("OMB_TAIL_RUNS", "0"))  # (tests: small parts)
                          or waves * torch.cuda.get_device_properties(dev).multi_processor_count)
             if b.nruns > part_runs:
@@ -185,7 +187,7 @@ class B200HydroStepper:
     # -- host <-> device -------------------------------------------------------------
     TRANSFER_CHUNKS = 8
 
-    SPAN_STASH = 2304  # ghost z doubles per leaf of the zero-copy spans (omb_host_gather)
+    SPAN_STASH = 48 * 56  # ghost z + line-edge doubles per leaf of the zero-copy spans (omb_host_gather)
 
     def _rehome(self):
         """Move the owned leaves' padded arrays (SubGrid.u) into one pinned host slab,
@@ -273,6 +275,25 @@ class B200HydroStepper:
     def _download_tail(self):
         b = self.batch
         t = self._tail
+        if self._mapped is not None:
+            # each part's final leaves are written to the mapped host slab as soon as the
+            # part is done (its event), on the side stream, while later parts compute
+            m = self._mapped
+            side = t["stream"]
+            cur = self._buf[self._state]
+            st = self.SPAN_STASH
+            bnd = t["bounds"]
+            for k, ev in enumerate(t["events"]):
+                lo, hi = int(bnd[k]), int(bnd[k + 1])
+                if hi <= lo:
+                    continue
+                side.wait_event(ev)
+                _lib.check(self.lib.omb_host_scatter(ptr(cur) + 8 * 512 * lo, ptr(m["stash"]) + 8 * st * lo, hi - lo,
+                                                     b.fstride, ptr(m["ptrs"]) + 8 * lo,
+                                                     ctypes.c_void_p(side.cuda_stream)), "omb_host_scatter")
+            side.synchronize()
+            torch.cuda.current_stream(self.dev).synchronize()
+            return
         ptrs = b._leaf_ptrs(b.ncompute)
         if ptrs is None:
             self.download()

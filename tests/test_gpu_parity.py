@@ -256,11 +256,16 @@ def _ghosts(t):
     return np.stack(out)
 
 
-@pytest.mark.parametrize("xfer", ["mapped", "threads"])
+@pytest.mark.parametrize("xfer", ["mapped", "mapped-tail", "threads"])
 def test_host_transfer_paths(monkeypatch, xfer):
     """Both host<->device transfer paths give the golden step, leave the host
-    ghost cells exactly as they were, and pick up leaf arrays a user replaced."""
-    monkeypatch.setenv("OMB_HOST_XFER", xfer)
+    ghost cells exactly as they were (the mapped path writes whole 64 B lines,
+    restoring the neighbouring ghost doubles from its stash), and pick up leaf
+    arrays a user replaced.  mapped-tail: the last stage in one-run launch parts,
+    each part's leaves written to the host while the next computes."""
+    monkeypatch.setenv("OMB_HOST_XFER", xfer.split("-")[0])
+    if xfer == "mapped-tail":
+        monkeypatch.setenv("OMB_TAIL_RUNS", "1")
     t, g = case_tree("smooth_reflecting")
     rng = np.random.default_rng(11)
     for lf in t.sorted_leaves():  # distinctive host ghost values
@@ -270,7 +275,8 @@ def test_host_transfer_paths(monkeypatch, xfer):
         u[:, 3:11, 3:11, 3:11] = keep
     ghosts = _ghosts(t)
     st = _stepper(t)
-    assert (st._mapped is not None) == (xfer == "mapped")
+    assert (st._mapped is not None) == xfer.startswith("mapped")
+    assert (st._tail is not None) == (xfer == "mapped-tail")
     st.rk3_step(st.cfl_dt(0.4))
     _check_state(t, g)
     assert bitwise_mismatch(_ghosts(t), ghosts) == 0
@@ -283,11 +289,12 @@ def test_host_transfer_paths(monkeypatch, xfer):
     assert bitwise_mismatch(_ghosts(t), ghosts) == 0
 
 
+@pytest.mark.parametrize("xfer", ["threads", "mapped"])
 @pytest.mark.parametrize("part_runs", [1, 3, 7])
-def test_overlapped_download(monkeypatch, part_runs):
+def test_overlapped_download(monkeypatch, part_runs, xfer):
     """The last stage launched in parts with each part's leaves copied back while
     the next computes gives the golden step (and the CFL-abort rollback still holds)."""
-    monkeypatch.setenv("OMB_HOST_XFER", "threads")
+    monkeypatch.setenv("OMB_HOST_XFER", xfer)
     monkeypatch.setenv("OMB_TAIL_RUNS", str(part_runs))
     t, g = case_tree("sedov_c1")
     st = _stepper(t)

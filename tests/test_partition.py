@@ -36,6 +36,18 @@ def test_partition_invariants(bnd, world):
         assert sorted(b.run_leaf.tolist()) == list(range(p.nown))
 
 
+def test_runs_respect_the_kernel_run_cap():
+    from paper_2107_10987_b200.batch import MAX_RUN, LeafBatch
+
+    t = mesh.build_uniform_tree(2, 8, boundary="reflecting")
+    for m in range(1, MAX_RUN + 1):
+        b = LeafBatch(t, max_run=m)
+        assert np.diff(b.run_off).max() <= m and b.run_off[-1] == b.ncompute
+    for m in (0, MAX_RUN + 1, 8):
+        with pytest.raises(ValueError):
+            LeafBatch(t, max_run=m)
+
+
 def test_neighbor_table_fast_path_matches_generic():
     for bnd in ("reflecting", "periodic", "outflow"):
         t = mesh.build_uniform_tree(2, 8, boundary=bnd)
