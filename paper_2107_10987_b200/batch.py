@@ -270,6 +270,34 @@ class LeafBatch:
         self.run_leaf = np.array([i for r in runs for i in r], dtype=np.int32)
         self.nruns = len(runs)
 
+    def split_tail(self, counts):
+        """Shorten the CTAs of the stage kernel's last wave.  The runs are ordered
+        longest first (one CTA each, dispatched in order); then, for each k in
+        ``counts``, the last k runs of >= 2 leaves are split in halves and moved to
+        the end.  The final wave then holds short CTAs, so the SMs run out of work
+        closer together.  A k that is not below the run count (a batch of at most one
+        wave) is skipped.  Results are bitwise the same for any run layout."""
+        runs = list(self.runs)
+        for k in counts:
+            if k <= 0 or k >= len(runs):
+                continue
+            runs.sort(key=len, reverse=True)
+            head, tail = runs[:-k], runs[-k:]
+            short = []
+            for r in tail:
+                if len(r) >= 2:
+                    h = len(r) // 2
+                    short += [r[:h], r[h:]]
+                else:
+                    short.append(r)
+            runs = head + sorted(short, key=len, reverse=True)
+        assert sorted(i for r in runs for i in r) == list(range(self.ncompute))
+        self.runs = runs
+        self.run_off = np.zeros(len(runs) + 1, dtype=np.int32)
+        self.run_off[1:] = np.cumsum([len(r) for r in runs])
+        self.run_leaf = np.array([i for r in runs for i in r], dtype=np.int32)
+        self.nruns = len(runs)
+
     def tail_parts(self, part_runs):
         """Launch parts of a stage whose output is downloaded while it still runs:
         the runs sorted by their last leaf, cut every ``part_runs`` runs.  Returns

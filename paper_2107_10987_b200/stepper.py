@@ -77,6 +77,13 @@ class B200HydroStepper:
             self.dist = None
             self.batch = LeafBatch(tree, max_run=max_run, leaves=leaves)
         b = self.batch
+        # the stage kernel's last CTAs made of shorter runs (half an SM count of runs split in
+        # halves, twice: 4 -> 2 -> 1 leaves), so the SMs run dry closer together.  c2 Sedov:
+        # 4.56 -> 4.35 ms per stage; c5 star (about uniform cost per run): +0.9 %
+        # (profiles/r01_split_tail_ab.jsonl).  OMB_SPLIT_TAIL=k[,k2...] overrides, 0 = off.
+        split = os.environ.get("OMB_SPLIT_TAIL")
+        half = torch.cuda.get_device_properties(self.dev).multi_processor_count // 2
+        b.split_tail([int(v) for v in split.split(",")] if split else [half, half])
         T = torch
         dev = self.dev
         # multi-GPU halo: uniform partitions read neighbour leaves straight from their owners'

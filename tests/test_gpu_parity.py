@@ -101,6 +101,23 @@ def test_step_parity(name, max_run):
     assert stats.kernel_launches == 6 * len(t.sorted_leaves())
 
 
+@pytest.mark.parametrize("name", ["sedov_c1", "amr_sedov_small"])
+@pytest.mark.parametrize("split", ["4", "6,3", "100"])
+def test_step_parity_split_tail(monkeypatch, name, split):
+    """Runs of mixed lengths (the last k runs split in halves; "6,3" splits twice; "100"
+    is skipped for the 16-run c1 batch, not below its run count) give the golden step."""
+    monkeypatch.setenv("OMB_SPLIT_TAIL", split)
+    t, g = case_tree(name)
+    st = _stepper(t)
+    lens = np.diff(st.batch.run_off)
+    if split != "100" or st.batch.nruns > 100:
+        assert lens.min() < lens.max()
+    stats = st.rk3_step(st.cfl_dt(0.4))
+    _check_state(t, g)
+    assert stats.amax == float(g["amax"][0])
+    assert stats.fallback_count == int(g["fallback"][0])
+
+
 def test_old_scheme_two_steps():
     from paper_2107_10987_b200 import HydroMode
 

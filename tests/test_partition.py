@@ -48,6 +48,23 @@ def test_runs_respect_the_kernel_run_cap():
             LeafBatch(t, max_run=m)
 
 
+def test_split_tail_keeps_every_leaf_once():
+    from paper_2107_10987_b200.batch import LeafBatch
+
+    t = mesh.build_uniform_tree(3, 8, boundary="reflecting")  # 512 leaves, 128 runs of 4
+    b = LeafBatch(t)
+    b.split_tail([148])  # not below the run count: unchanged
+    assert b.nruns == 128
+    b.split_tail([20, 10])
+    lens = np.diff(b.run_off)
+    assert b.nruns == 128 + 20 + 10 and list(lens[:108]) == [4] * 108
+    assert list(lens[108:]) == [2] * 30 + [1] * 20
+    assert sorted(b.run_leaf.tolist()) == list(range(b.ncompute))
+    for r in b.runs:  # still consecutive along +x
+        for a, c in zip(r, r[1:]):
+            assert b.info[a]["nbr"][OFFS.index((1, 0, 0))] == c
+
+
 def test_neighbor_table_fast_path_matches_generic():
     for bnd in ("reflecting", "periodic", "outflow"):
         t = mesh.build_uniform_tree(2, 8, boundary=bnd)
