@@ -345,6 +345,7 @@ def gpu_arm(args, rank, world):
     ratio = dt_h.numpy() * amax / st.dx_min
     aborted = bool(np.any(ratio > 1.0))
     info = {"nglobal": st.nglobal, "nruns": st.batch.nruns, "L": st.batch.L, "ncompute": st.batch.ncompute,
+            "run_lengths": {int(k): int(v) for k, v in zip(*np.unique(np.diff(st.batch.run_off), return_counts=True))},
             "launches": st.native_launches_per_step()}
     fmm = None
     if level == "c5g":  # the per-stage FMM solve on its own (density + dphi/dt), CUDA events
@@ -465,7 +466,8 @@ def gpu_arm(args, rank, world):
                                "reflecting, cfl 0.4, scheme new",
                    "step": "cfl_dt + 3 fused RK stages, dt on device",
                    "l2": "working set (3 x 6 x cells x 8 B = %.0f MB) > 126 MB L2; no flush" % (3 * 48 * cells / 1e6),
-                   "runs": info["nruns"], "max_run": args.max_run, "parallelism": f"leaf-partitioned x{world}",
+                   "runs": info["nruns"], "max_run": args.max_run, "run_lengths": info["run_lengths"],
+                   "parallelism": f"leaf-partitioned x{world}",
                    "halo_leaves_per_rank": int(info["L"] - info["ncompute"])},
         "roofline": {"bound": "fp64", "achieved": achieved_tf, "peak": peak64, "unit": "TFLOP/s",
                      "frac": achieved_tf / peak64, "traffic": traffic,
