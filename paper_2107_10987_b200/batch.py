@@ -185,8 +185,8 @@ class LeafBatch:
                 tasks.append(t)
                 nbr[q] = t[4]
             self.info[i]["nbr"] = nbr
-            if len(tasks) and any(nbr[q] >= L for q in range(27)):
-                self.solo[i] = True
+            # a leaf whose ghost regions come from virtual leaves still joins a run: the gather
+            # reads them through its own LeafInfo (only flux exporters run alone, below)
         self.nvirtual = len(tasks)
         self.amr_tasks = np.array(tasks, dtype=np.int32).reshape(-1, AMR_TASK_INTS)
         # reflux relations across faces (the reference's _reflux loop order)
