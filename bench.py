@@ -52,8 +52,10 @@ def parse():
     p.add_argument("--e2e-steps", type=int, default=8)
     p.add_argument("--cpu-leaves", type=int, default=512)
     p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--efficiency-steps", type=int, default=10,
+                   help="N>1: steps of the whole workload on rank 0's GPU alone (0 = skip)")
     p.add_argument("--config", default=None, choices=["c2", "c3", "c4", "c5", "c5g"],
-                   help="c2: uniform 128^3 (N=1 default); c3: uniform 256^3 (N>1 default); c4: AMR Sedov, "
+                   help="c2: uniform 128^3; c3: uniform 256^3 (default at every N); c4: AMR Sedov, "
                         "levels 3-6; c5: rotating polytrope stand-in, fixed gravity, 128^3; c5g: the same star "
                         "self-gravitating (device FMM re-solved every stage, theta 0.5; --level sets the tree, "
                         "default 4 = 128^3)")
@@ -79,7 +81,8 @@ def resolve_level(args, world):
         return 5
     if args.config == "c2":
         return 4
-    return args.level if args.level is not None else (4 if world == 1 else 5)
+    # every N runs the same workload (strong scaling): config c3, 256^3, fits one B200
+    return args.level if args.level is not None else 5
 
 
 def workload_name(level, nleaves):
@@ -92,7 +95,8 @@ def workload_name(level, nleaves):
                 "dphi/dt, as HydroStepper + FmmSolver)")
     if level == "c4":
         return f"sedov_amr_L3-6_n8 (config c4): {nleaves} sub-grids of 8^3 on levels 3-6 (SURVEY.md 8d construction)"
-    return f"sedov_uniform_L{level}_n8"
+    tag = {4: " (config c2: 128^3)", 5: " (config c3: 256^3)"}.get(level, "")
+    return f"sedov_uniform_L{level}_n8{tag}"
 
 
 def peaks():
@@ -229,7 +233,7 @@ def reference_arm(args, rank, world):
     v, nthr, sample, per = cpu_run(level, nleaves, args.steps, args.warmup)
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": per * 1e3, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic (init_sedov, no RNG)",
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic (init_sedov, no RNG)",
             "config": {"workload": f"{workload_name(level, None)}, reflecting, cfl 0.4; CPU sample per step"},
             "cpu_baseline": {"value": v, "unit": UNIT, "cores": nthr, "kind": "port", "sample": sample},
             "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
@@ -262,6 +266,8 @@ def fp64_peak(lib, torch):
 
 
 def gpu_arm(args, rank, world):
+    import gc
+
     import torch
 
     from paper_2107_10987_b200 import EosConfig, HydroMode, _lib
@@ -365,11 +371,39 @@ def gpu_arm(args, rank, world):
                "entities": int(fs.table.nentities), "theta": fs.theta,
                "interactions_per_s": 2 * 2 * fs.stats["pairs"] / (fmm_ms / 1e3),
                "prepare_s_host": t_prep, "share_of_step": 3 * fmm_ms / (ms / K)}
+    # same-box single-GPU reference for the parallel efficiency: rank 0 steps the WHOLE
+    # workload alone (same warm-up and step count, same initial state -- the host tree is
+    # untouched by the host_sync=False run), the other ranks wait
+    single = None
+    if world > 1 and args.efficiency_steps != 0 and level in (4, 5, "c4", "c5"):
+        del st
+        gc.collect()
+        torch.cuda.empty_cache()
+        dist.barrier()
+        if rank == 0:
+            st1 = B200HydroStepper(tree, eos, HydroMode("new"), host_sync=False, max_run=args.max_run, **extra)
+            for _ in range(args.warmup):
+                st1._cfl_launch(0.4)
+                st1.launch_step(None)
+            torch.cuda.synchronize()
+            s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            s0.record()
+            for _ in range(K):
+                st1._cfl_launch(0.4)
+                st1.launch_step(None)
+            s1.record()
+            torch.cuda.synchronize()
+            ms1 = s0.elapsed_time(s1)
+            single = {"value": cells * K / (ms1 / 1e3), "ms_per_step": ms1 / K, "steps": K, "warmup": args.warmup,
+                      "what": "the same workload and step sequence on rank 0's GPU alone, same run"}
+            del st1
+            gc.collect()
+            torch.cuda.empty_cache()
+        dist.barrier()
+        st = None
     # free the host tree and device buffers before the e2e / non-flat trees (c3 at 8 ranks:
     # 4.3 GB of host leaves per rank per tree)
     del st, tree, part
-    import gc
-
     gc.collect()
     torch.cuda.empty_cache()
 
@@ -459,7 +493,10 @@ def gpu_arm(args, rank, world):
             traffic = json.load(f).get("bytes_per_launch")
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K, "warmup": args.warmup,
-        "ms_per_step": ms / K, "higher_is_better": True, "scaling": "weak" if world == 1 else "strong",
+        "ms_per_step": ms / K, "higher_is_better": True, "scaling": "strong",
+        "per_gpu": value / world,
+        "parallel_efficiency": (value / (world * single["value"])) if single else (1.0 if world == 1 else None),
+        "single_gpu": single,
         "vs_baseline": None,
         "dtype": "f64", "data": "synthetic (init_sedov Sedov-Taylor, no RNG)",
         "config": {"workload": f"{workload_name(level, info['nglobal'])}: {info['nglobal']} sub-grids of 8^3 = {cells} cells, "

@@ -170,6 +170,11 @@ int omb_fp64_peak(double *scratch, int blocks, int iters, void *stream);
 /* padded (6,14,14,14) conserved block of one leaf as the ghost fill would produce it */
 int omb_gather(const double *u, long long fstride, const OmbLeafInfo *info, int leaf, int bc,
                double *out, void *stream);
+/* the same for n consecutive leaves first..first+n-1 (n <= 65535), out [n][6][14][14][14]: the
+ * stage state with its ghosts filled, as HydroStepper._stage hands it to a host gravity solver
+ * (hydro/step.py:106-113, mesh/ghosts.py:115-157; AMR regions need omb_amr_ghosts first) */
+int omb_gather_leaves(const double *u, long long fstride, const OmbLeafInfo *info, int first, int n, int bc,
+                      double *out, void *stream);
 
 /* ---- FMM gravity (gravity/solver.py:50-164; _core.pyx:372-608; multipole.py) ----------------------
  * Order-3 Cartesian FMM over the entity table (octree nodes + each leaf's block hierarchy down to cells).

@@ -82,17 +82,12 @@ static void build_face_tables(FaceTable* ft) {
   }
 }
 
-static std::once_flag g_init_flag;
-static int g_init_rc = 0;
-static int lib_init() {
-  std::call_once(g_init_flag, [] {
-    FaceTable ft[3];
-    build_face_tables(ft);
-    if (cudaMemcpyToSymbol(c_ft, ft, sizeof(ft)) != cudaSuccess) g_init_rc = -1;
-  });
-  if (g_init_rc) return set_err("face table upload failed");
-  return 0;
-}
+// one-time setup PER DEVICE (face tables in that device's constant bank, the
+// stage/reflux kernels' shared-memory attributes): a bit per device, set under
+// a mutex, read lock-free afterwards -- entry points may be called from many
+// host threads and for several devices in one process (the reference calls its
+// kernels from scheduler threads, _core.pyx:60,239).  Defined after the kernels.
+static int lib_init();
 
 // ---------------------------------------------------------------------------
 // per-sub-grid shims (the reference's `kernels` module surface)
@@ -455,11 +450,16 @@ __global__ void k_cfl_reduce(int L, const double* ratio, const int* bad, double 
   }
 }
 
-__global__ void k_gather(const double* U, long long fstride, const LeafInfo* info, int leaf, int bc, double* out) {
+// padded (6,14,14,14) arrays of leaves first .. first+gridDim.y-1: interior + the
+// ghost shell exactly as mesh/ghosts.py fills it (AMR regions from the virtual
+// leaves k_amr_ghosts filled)
+__global__ void k_gather(const double* U, long long fstride, const LeafInfo* info, int first, int bc, double* out) {
+  const int leaf = first + blockIdx.y;
+  double* o = out + (long long)blockIdx.y * NF * M * M * M;
   for (int c = threadIdx.x + blockIdx.x * blockDim.x; c < M * M * M; c += blockDim.x * gridDim.x) {
     double u[NF];
     gather_cell(U, fstride, info[leaf], bc, c / (M * M), (c / M) % M, c % M, u);
-    for (int v = 0; v < NF; v++) out[v * M * M * M + c] = u[v];
+    for (int v = 0; v < NF; v++) o[v * M * M * M + c] = u[v];
   }
 }
 
@@ -623,6 +623,28 @@ __global__ void k_dfma_peak(double* out, int iters) {
 // ---------------------------------------------------------------------------
 // C ABI
 // ---------------------------------------------------------------------------
+static std::mutex g_init_mu;
+static std::atomic<unsigned long long> g_init_devs{0};
+static int lib_init() {
+  int dev = 0;
+  CK(cudaGetDevice(&dev), "cudaGetDevice");
+  if (dev < 0 || dev >= 64) return set_err("device index outside [0, 64)");
+  const unsigned long long bit = 1ull << dev;
+  if (g_init_devs.load(std::memory_order_acquire) & bit) return 0;
+  std::lock_guard<std::mutex> lk(g_init_mu);
+  if (g_init_devs.load(std::memory_order_relaxed) & bit) return 0;
+  FaceTable ft[3];
+  build_face_tables(ft);
+  CK(cudaMemcpyToSymbol(c_ft, ft, sizeof(ft)), "face table upload");
+  // 512 threads x 128 registers fills the register file; 256/384/576/640 were measured slower
+  CK(cudaFuncSetAttribute(k_stage<STAGE_THREADS>, cudaFuncAttributeMaxDynamicSharedMemorySize, Smem::BYTES),
+     "stage smem attribute");
+  CK(cudaFuncSetAttribute(k_reflux_update, cudaFuncAttributeMaxDynamicSharedMemorySize, FLUX_SLOT * 8),
+     "reflux smem attribute");
+  g_init_devs.fetch_or(bit, std::memory_order_release);
+  return 0;
+}
+
 extern "C" {
 
 int omb_abi_version(void) { return OMB_ABI_VERSION; }
@@ -750,12 +772,6 @@ int omb_amr_ghosts(const OmbAmrDesc* d, void* stream) {
 int omb_reflux_update(const OmbRefluxDesc* d, void* stream) {
   if (int rc = lib_init()) return rc;
   if (d->nleaves <= 0) return 0;
-  static bool attr = false;
-  if (!attr) {
-    CK(cudaFuncSetAttribute(k_reflux_update, cudaFuncAttributeMaxDynamicSharedMemorySize, FLUX_SLOT * 8),
-       "reflux smem attribute");
-    attr = true;
-  }
   StageArgs A = stage_args(&d->stage);
   k_reflux_update<<<d->nleaves, 256, FLUX_SLOT * 8, (cudaStream_t)stream>>>(A, d->leaf, d->off, d->tasks);
   CK(cudaGetLastError(), "omb_reflux_update launch");
@@ -766,13 +782,6 @@ int omb_stage(const OmbStageDesc* d, void* stream) {
   if (int rc = lib_init()) return rc;
   if (d->ucur == d->unext) return set_err("omb_stage: unext must not alias ucur");
   if (!div_range_ok(d->gm1)) return set_err("omb_stage: gamma - 1 outside [2^-100, 2^100]");
-  static bool attr_set = false;
-  if (!attr_set) {
-    // 512 threads x 128 registers fills the register file; 256/384/576/640 were measured slower
-    CK(cudaFuncSetAttribute(k_stage<STAGE_THREADS>, cudaFuncAttributeMaxDynamicSharedMemorySize, Smem::BYTES),
-       "smem attribute");
-    attr_set = true;
-  }
   StageArgs A = stage_args(d);
   if (d->nruns <= 0) return 0;
   k_stage<STAGE_THREADS><<<d->nruns, STAGE_THREADS, Smem::BYTES, (cudaStream_t)stream>>>(A);
@@ -1188,6 +1197,16 @@ int omb_gather(const double* u, long long fstride, const OmbLeafInfo* info, int 
   if (int rc = lib_init()) return rc;
   k_gather<<<11, 256, 0, (cudaStream_t)stream>>>(u, fstride, (const LeafInfo*)info, leaf, bc, out);
   CK(cudaGetLastError(), "omb_gather launch");
+  return 0;
+}
+
+int omb_gather_leaves(const double* u, long long fstride, const OmbLeafInfo* info, int first, int n, int bc,
+                      double* out, void* stream) {
+  if (int rc = lib_init()) return rc;
+  if (n <= 0) return 0;
+  if (n > 65535) return set_err("omb_gather_leaves: more than 65535 leaves per call");
+  k_gather<<<dim3(11, n), 256, 0, (cudaStream_t)stream>>>(u, fstride, (const LeafInfo*)info, first, bc, out);
+  CK(cudaGetLastError(), "omb_gather_leaves launch");
   return 0;
 }
 

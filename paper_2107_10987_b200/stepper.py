@@ -43,10 +43,34 @@ class _DeviceArray:
         self.__cuda_array_interface__ = {"shape": (n,), "typestr": "<f8", "data": (ptr, False), "version": 3}
 
 
+def _on_device(fn):
+    """Run a stepper method with its device current, so streams (stream_handle) and
+    the library's per-device setup resolve to ``self.dev`` even when the caller's
+    current device is another one."""
+    import functools
+
+    @functools.wraps(fn)
+    def wrapped(self, *a, **kw):
+        with torch.cuda.device(self.dev):
+            return fn(self, *a, **kw)
+
+    return wrapped
+
+
 class B200HydroStepper:
     def __init__(self, tree, eos, mode, executor=None, gravity=None, omega=0.0, floors=None, abort_courant=1.0,
                  buffers=None, profiler=None, lane_pool=None, *, host_sync=True, max_run=4, device=None,
                  leaves=None, partition=None, group=None):
+        dev = require_cuda(device)
+        if dev.index is None:
+            dev = torch.device("cuda", torch.cuda.current_device())
+        self.dev = dev
+        with torch.cuda.device(dev):  # allocations, library setup and streams on `device`
+            self._setup(tree, eos, mode, executor, gravity, omega, floors, abort_courant, buffers, profiler,
+                        lane_pool, host_sync, max_run, leaves, partition, group)
+
+    def _setup(self, tree, eos, mode, executor, gravity, omega, floors, abort_courant, buffers, profiler, lane_pool,
+               host_sync, max_run, leaves, partition, group):
         self.tree = tree
         self.eos = eos
         self.mode = mode
@@ -60,7 +84,6 @@ class B200HydroStepper:
         self.lane_pool = lane_pool
         self.stats = StepStats()
         self.host_sync = host_sync
-        self.dev = require_cuda(device)
         self.lib = _lib.load()
         self.part = partition
         self.group = group
@@ -228,6 +251,7 @@ class B200HydroStepper:
                     v[...] = sg._u
                 sg._u = v
 
+    @_on_device
     def upload(self):
         """Copy the host leaves' interiors into the device state.  Mapped slab: one
         kernel reads them over PCIe.  Otherwise pipelined: host threads pack chunk c
@@ -256,6 +280,7 @@ class B200HydroStepper:
             self._buf[self._state].copy_(self._pinned, non_blocking=True)
         self._up_ev.record()
 
+    @_on_device
     def download(self):
         """Copy the device state back into the host leaves (the owned ones).  Mapped
         slab: one kernel writes them over PCIe, then the stream is synchronised.
@@ -383,6 +408,7 @@ class B200HydroStepper:
                        "omb_scatter_rows")
 
     # -- timestep ---------------------------------------------------------------------
+    @_on_device
     def _cfl_launch(self, cfl, stream=None):
         b = self.batch
         g = self.eos.gamma
@@ -396,6 +422,7 @@ class B200HydroStepper:
             self.dist.all_reduce(self._cfl_out, op=self.dist.ReduceOp.MIN, group=self.group)
             self._dt.copy_(self._cfl_out[1:2])
 
+    @_on_device
     def cfl_dt(self, cfl):
         """dt = cfl * min over leaves of dx / max(max_axis|v| + c)  (step.py:81-92)."""
         if self.host_sync:
@@ -431,6 +458,7 @@ class B200HydroStepper:
             contact=int(self.mode.contact_detection), amax_bits=acc.data_ptr() + 8 * s,
             fallback=acc.data_ptr() + 8 * (3 + s), flux=ptr(self._flux))
 
+    @_on_device
     def launch_step(self, dt=None, stream=None, events=None, tail=False):
         """Enqueue the three stages (no host sync) and advance the device state.
         dt=None uses the device dt written by the last cfl launch; tail=True
@@ -445,16 +473,6 @@ class B200HydroStepper:
         others = [i for i in range(4) if i != self._state]
         for s, (a, bw) in enumerate(SSP_RK3_STAGES):
             nxt = others[s]
-            if self._dev_gravity:
-                pass  # solved on the device below, after the AMR ghost regions are filled
-            elif self.gravity is not None:
-                # the reference re-solves gravity every stage (step.py:111-113); a solver that
-                # returns the same field object again (fixed gravity) is uploaded only once
-                fields = self.gravity.solve(self.tree, need_derivative=True)
-                if fields is not getattr(self, "_grav_src", None):
-                    self._grav = torch.from_numpy(self.batch.pack_gravity(fields).reshape(-1)).to(self.dev)
-                    self._grav_src = fields
-            nxt = others[s]
             if self._p2p:
                 # every rank has finished the previous stage (its output = this stage's input)
                 # before anyone reads it; also no rank writes a buffer a peer still reads
@@ -466,6 +484,8 @@ class B200HydroStepper:
                 ad = OmbAmrDesc(u=ptr(self._buf[cur]), fstride=self.batch.fstride, tasks=ptr(self._amr_tasks),
                                 ntasks=self.batch.nvirtual)
                 _lib.check(self.lib.omb_amr_ghosts(ctypes.byref(ad), sh), "omb_amr_ghosts")
+            if self.gravity is not None and not self._dev_gravity:
+                self._host_gravity(cur, stream)
             if self._dev_gravity:
                 # device FMM on this stage's state (the reference's order: ghost fill, then
                 # gravity, then reconstruction -- step.py:106-113)
@@ -507,6 +527,36 @@ class B200HydroStepper:
         self._state = outs[2]
         return start, outs
 
+    def _host_gravity(self, cur, stream=None):
+        """A host gravity object, re-solved every stage like the reference (step.py:106-113):
+        the stage state with its ghosts filled (omb_gather_leaves -- the reference's
+        exchange_ghosts, AMR regions included) is written into every leaf's padded
+        ``SubGrid.u`` first, so solvers that read the state (e.g. octomini's FmmSolver:
+        density, and rho_dot from the momentum ghosts, gravity/solver.py:134-171) see
+        exactly what the reference hands them.  Objects marked ``state_independent``
+        (fixed fields) skip the copy.  A field set returned again (same object) is
+        uploaded only once."""
+        if not getattr(self.gravity, "state_independent", False):
+            if self.part is not None:
+                raise NotImplementedError("a state-dependent host gravity solver needs the whole tree on one rank; "
+                                          "use gravity.B200FmmSolver with a partition")
+            b = self.batch
+            sh = stream_handle(stream)
+            n = b.L
+            padded = torch.empty((n, 6, 14, 14, 14), dtype=torch.float64, device=self.dev)
+            for first in range(0, n, 65535):
+                k = min(65535, n - first)
+                _lib.check(self.lib.omb_gather_leaves(ptr(self._buf[cur]), b.fstride, ptr(self._info), first, k,
+                                                      b.bc, padded.data_ptr() + 8 * first * 6 * 14 ** 3, sh),
+                           "omb_gather_leaves")
+            host = padded.cpu().numpy()
+            for k, lf in enumerate(b.leaves[:n]):
+                lf.subgrid.u[...] = host[k]
+        fields = self.gravity.solve(self.tree, need_derivative=True)
+        if fields is not getattr(self, "_grav_src", None):
+            self._grav = torch.from_numpy(self.batch.pack_gravity(fields).reshape(-1)).to(self.dev)
+            self._grav_src = fields
+
     def native_launches_per_step(self):
         """Kernels of libomb200 one cfl launch + launch_step enqueue (k_cfl_leaf/reduce,
         then per stage: halo pack/unpack, AMR ghosts, k_stage, flux rows, reflux)."""
@@ -527,6 +577,7 @@ class B200HydroStepper:
             self.dist.all_reduce(self._acc[:3], op=self.dist.ReduceOp.MAX, group=self.group)
             self.dist.all_reduce(self._acc[3:], op=self.dist.ReduceOp.SUM, group=self.group)
 
+    @_on_device
     def rk3_step(self, dt):
         """One SSP-RK3 step (step.py:94-102) on the device."""
         if self.host_sync and not self._fresh:

@@ -59,6 +59,13 @@ def case_tree(name):
         t = mesh.build_uniform_tree(1, 8, boundary="reflecting")
     elif name == "sources":
         t = mesh.build_uniform_tree(1, 8, boundary="outflow")
+    elif name in ("contact_step", "override_10", "gravity_density_amr"):
+        t = mesh.build_uniform_tree(1, 8, boundary="periodic")
+        if name == "gravity_density_amr":
+            t.split(t.leaf_at(1, (0, 0, 0)))
+            t.reindex()
+    elif name == "gravity_density":
+        t = mesh.build_uniform_tree(1, 8, boundary="reflecting")
     else:
         raise KeyError(name)
     g = golden(name)
@@ -69,6 +76,8 @@ def case_tree(name):
 
 
 class FixedGravity:
+    state_independent = True
+
     def __init__(self, fields):
         self.fields = fields
 
@@ -102,3 +111,21 @@ def rel_close(x, ref, rtol=1e-12):
         scale = max(float(np.max(np.abs(rs))), 1e-300)
         bad += int(np.count_nonzero(np.abs(xs - rs) > rtol * np.maximum(np.abs(rs), scale)))
     return bad
+
+
+class DensityGravity:
+    """The state-dependent gravity stub of tests/golden/make_golden.py (same
+    expressions): g from centred density differences -- reads the ghost cells of
+    the stage state -- dphi/dt from the momentum, phi = -rho."""
+
+    def solve(self, tree, need_derivative=False):
+        out = {}
+        for lf in tree.leaves():
+            u = lf.subgrid.u
+            r = u[0]
+            gx = -0.05 * (r[4:12, 3:11, 3:11] - r[2:10, 3:11, 3:11])
+            gy = -0.05 * (r[3:11, 4:12, 3:11] - r[3:11, 2:10, 3:11])
+            gz = -0.05 * (r[3:11, 3:11, 4:12] - r[3:11, 3:11, 2:10])
+            dphi = 0.01 * (u[1, 4:12, 3:11, 3:11] - u[1, 2:10, 3:11, 3:11])
+            out[lf.path] = dict(phi=-r[3:11, 3:11, 3:11].copy(), gx=gx, gy=gy, gz=gz, dphi_dt=dphi)
+        return out

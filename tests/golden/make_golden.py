@@ -330,7 +330,86 @@ def gravity_step_case():
     step_case("gravity_step", tree, steps=2, gravity=FmmSolver(0.5), omega=0.3)
 
 
+class DensityGravity:
+    """State-dependent gravity stub (round-2 contract test): g from the centred
+    density difference (reads the ghost cells the stage's fill produced), dphi/dt
+    from the momentum, phi = -rho.  The reference calls solve() after the stage's
+    ghost fill (hydro/step.py:106-113)."""
+
+    def solve(self, tree, need_derivative=False):
+        out = {}
+        for lf in tree.leaves():
+            u = lf.subgrid.u
+            r = u[0]
+            gx = -0.05 * (r[4:12, 3:11, 3:11] - r[2:10, 3:11, 3:11])
+            gy = -0.05 * (r[3:11, 4:12, 3:11] - r[3:11, 2:10, 3:11])
+            gz = -0.05 * (r[3:11, 3:11, 4:12] - r[3:11, 3:11, 2:10])
+            dphi = 0.01 * (u[1, 4:12, 3:11, 3:11] - u[1, 2:10, 3:11, 3:11])
+            out[lf.path] = dict(phi=-r[3:11, 3:11, 3:11].copy(), gx=gx, gy=gy, gz=gz, dphi_dt=dphi)
+        return out
+
+
+def density_gravity_cases():
+    t = build_uniform_tree(1, 8, boundary="reflecting")
+    random_smooth(t, seed=13)
+    step_case("gravity_density", t, steps=2, gravity=DensityGravity(), omega=0.2)
+    t = build_uniform_tree(1, 8, boundary="periodic")
+    t.split(t.leaf_at(1, (0, 0, 0)))
+    t.reindex()
+    random_smooth(t, seed=14)
+    step_case("gravity_density_amr", t, steps=1, gravity=DensityGravity())
+
+
+def contact_tree(seed=12):
+    """Level-1 periodic tree with a density jump x4 at x = 0 (pressure and velocity
+    continuous: a contact) on the smooth field, so the steepener (_core.pyx:107-142) fires."""
+    t = build_uniform_tree(1, 8, boundary="periodic")
+    random_smooth(t, seed=seed)
+    for lf in t.leaves():
+        sg = lf.subgrid
+        x = sg.cell_centers(0)[:, None, None] + 0.0 * sg.cell_centers(1)[None, :, None] + \
+            0.0 * sg.cell_centers(2)[None, None, :]
+        rho = (1.0 + 0.2 * np.sin(np.pi * x)) * np.where(x < 0.0, 4.0, 1.0)
+        p = 1.0 + 0.1 * np.cos(np.pi * sg.cell_centers(2))[None, None, :] + 0.0 * x
+        sg.interior[:] = conserved_from_primitive(rho, (0.3 + 0.0 * x, 0.1 + 0.0 * x, -0.05 + 0.0 * x), p, EOS)
+    return t
+
+
+def mode_cases():
+    """HydroMode branches: contact steepening in a full step, and the
+    quadrature_override hook -- new+override == old bitwise over 10 steps at a
+    fixed dt (tests/test_hydro_step.py:151-164)."""
+    step_case("contact_step", contact_tree(), steps=2, mode=HydroMode("new", contact_detection=True))
+    # the same initial data without contact detection must differ (the branch is live)
+    t = contact_tree()
+    st = HydroStepper(t, EOS, HydroMode("new"))
+    st.rk3_step(st.cfl_dt(0.4))
+    off = state_of(t)
+    g = np.load(os.path.join(HERE, "contact_step.npz"))
+    assert not np.array_equal(off, g["state1"]), "contact steepening did not fire"
+
+    def run(mode):
+        tree = build_uniform_tree(1, 8, boundary="periodic")
+        random_smooth(tree, seed=8)
+        init = state_of(tree)
+        st = HydroStepper(tree, EOS, mode)
+        dt = st.cfl_dt(0.3)
+        for _ in range(10):
+            st.rk3_step(dt)
+        return init, dt, state_of(tree), st.stats
+
+    init, dt, old, _ = run(HydroMode("old"))
+    _, dt2, new, stats = run(HydroMode("new", quadrature_override=True))
+    assert dt == dt2 and np.array_equal(old, new), "reference: old != new+override"
+    save("override_10", init=init, dt=np.array(dt), final=new, final_sha=np.array(sha(new)),
+         amax_last=np.array(stats.amax), fallback_last=np.array(stats.fallback_count))
+
+
 def main():
+    if sys.argv[1:] == ["modes"]:
+        mode_cases()
+        density_gravity_cases()
+        return
     if sys.argv[1:] == ["fmm"]:
         fmm_case()
         gravity_step_case()
@@ -363,6 +442,8 @@ def main():
     sources_case()
     fmm_case()
     gravity_step_case()
+    mode_cases()
+    density_gravity_cases()
 
 
 if __name__ == "__main__":

@@ -114,3 +114,26 @@ def test_emulated_amr_sedov_small():
     em.rk3_step(float(g["dts"][0]))
     assert bitwise_mismatch(state_of(t), g["state1"]) == 0
     assert em.amax == float(g["amax"][0])
+
+
+@pytest.mark.parametrize("max_run", [1, 4])
+def test_emulated_contact_detection(max_run):
+    """contact_detection=True: the steepener inside the fused kernel's mono6 (P1/P3)."""
+    t, g = case_tree("contact_step")
+    em = EmuStepper(t, 1.4, contact=True, max_run=max_run)
+    em.rk3_step(float(g["dts"][0]))
+    assert bitwise_mismatch(state_of(t), g["state1"]) == 0
+    assert em.amax == float(g["amax"][0])
+    assert em.fallback == int(g["fallback"][0])
+
+
+@pytest.mark.parametrize("override", [True, False])
+def test_emulated_override_equals_old(override):
+    """new + quadrature_override and old: the reference's 10-step state bitwise
+    (tests/test_hydro_step.py:151-164 pins old == new+override)."""
+    t, g = case_tree("override_10")
+    em = EmuStepper(t, 1.4, new_mode=override, override=override)  # override=False: the old scheme
+    dt = float(g["dt"])
+    for _ in range(10):
+        em.rk3_step(dt)
+    assert bitwise_mismatch(state_of(t), g["final"]) == 0

@@ -5,7 +5,7 @@ All calls go through the C-ABI library libomb200.so."""
 import numpy as np
 import pytest
 
-from _cases import EOS, bitwise_mismatch, case_tree, golden, rel_close, sources_gravity, state_of
+from _cases import EOS, DensityGravity, bitwise_mismatch, case_tree, golden, rel_close, sources_gravity, state_of
 
 pytestmark = pytest.mark.gpu
 
@@ -325,3 +325,145 @@ def test_overlapped_download(monkeypatch, part_runs, xfer):
     with pytest.raises(NumericsError):
         st.rk3_step(dt=10.0)
     assert bitwise_mismatch(state_of(t), before) == 0
+
+
+@pytest.mark.parametrize("max_run", [1, 4])
+def test_contact_detection_steps(max_run):
+    """HydroMode('new', contact_detection=True) through the fused kernel (the
+    steepener of _core.pyx:107-142 inside k_stage), 2 steps vs the reference."""
+    from paper_2107_10987_b200 import HydroMode
+
+    t, g = case_tree("contact_step")
+    st = _stepper(t, mode=HydroMode("new", contact_detection=True), max_run=max_run)
+    for s in range(2):
+        dt = st.cfl_dt(0.4)
+        assert dt == float(g["dts"][s])
+        stats = st.rk3_step(dt)
+        if s == 0:
+            _check_state(t, g)
+        assert stats.amax == float(g["amax"][s])
+        assert stats.fallback_count == int(g["fallback"][s])
+    _check_state(t, g, "final")
+
+
+@pytest.mark.parametrize("mode", ["override", "old"])
+@pytest.mark.parametrize("max_run", [1, 4])
+def test_override_equals_old_ten_steps(mode, max_run):
+    """new + quadrature_override == old, bitwise over 10 steps at a fixed dt
+    (reference tests/test_hydro_step.py:151-164): both modes reproduce the
+    reference's 10-step state."""
+    from paper_2107_10987_b200 import HydroMode
+
+    t, g = case_tree("override_10")
+    m = HydroMode("new", quadrature_override=True) if mode == "override" else HydroMode("old")
+    st = _stepper(t, mode=m, max_run=max_run)
+    dt = st.cfl_dt(0.3)
+    assert dt == float(g["dt"])
+    for _ in range(10):
+        st.rk3_step(dt)
+    _check_state(t, g, "final")
+
+
+@pytest.mark.parametrize("name", ["gravity_density", "gravity_density_amr"])
+def test_state_dependent_host_gravity(name):
+    """A host gravity object that reads the stage state (g from density
+    differences across ghost cells, dphi/dt from momenta) is solved every stage on
+    the stage state with filled ghosts, as HydroStepper._stage does (step.py:106-113)."""
+    t, g = case_tree(name)
+    st = _stepper(t, gravity=DensityGravity(), omega=0.2 if name == "gravity_density" else 0.0)
+    for s in range(len(g["dts"])):
+        dt = st.cfl_dt(0.4)
+        assert dt == float(g["dts"][s])
+        stats = st.rk3_step(dt)
+        if s == 0:
+            _check_state(t, g)
+        assert stats.amax == float(g["amax"][s])
+    if "final" in g:
+        _check_state(t, g, "final")
+
+
+def test_gather_matches_amr_ghost_golden():
+    """omb_gather_leaves after omb_amr_ghosts = the reference's exchange_ghosts on an
+    AMR tree (coarse/fine prolongation + restriction regions included)."""
+    import ctypes
+    import json
+
+    import torch
+
+    from paper_2107_10987_b200 import _lib, mesh
+    from paper_2107_10987_b200._abi import OmbAmrDesc
+    from paper_2107_10987_b200.batch import LeafBatch
+
+    g = golden("ghosts")
+    L = _lib.load()
+    t = mesh.build_uniform_tree(1, 8, boundary="reflecting")
+    t.split(t.leaf_at(1, (0, 0, 0)))
+    t.reindex()
+    assert [json.loads(p) for p in g["amr_paths"]] == [list(lf.path) for lf in t.sorted_leaves()]
+    for lf, u in zip(t.sorted_leaves(), g["amr"]):
+        lf.subgrid.interior[:] = u[:, 3:11, 3:11, 3:11]
+    b = LeafBatch(t)
+    U = torch.from_numpy(np.ascontiguousarray(b.pack())).cuda()
+    info = torch.from_numpy(b.info.view(np.uint8).copy()).cuda()
+    tasks = torch.from_numpy(b.amr_tasks.reshape(-1).copy()).cuda()
+    sh = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+    ad = OmbAmrDesc(u=U.data_ptr(), fstride=b.fstride, tasks=tasks.data_ptr(), ntasks=b.nvirtual)
+    _lib.check(L.omb_amr_ghosts(ctypes.byref(ad), sh), "omb_amr_ghosts")
+    out = torch.empty((b.L, 6, 14, 14, 14), dtype=torch.float64, device="cuda")
+    _lib.check(L.omb_gather_leaves(U.data_ptr(), b.fstride, info.data_ptr(), 0, b.L, b.bc, out.data_ptr(), sh),
+               "omb_gather_leaves")
+    assert bitwise_mismatch(out.cpu().numpy(), g["amr"]) == 0
+
+
+def test_kernels_module_threads_and_devices():
+    """The C ABI's one-time setup is per device and thread-safe: the kernels shim
+    called from 8 host threads at once (the reference's scheduler threads call
+    kernels concurrently, _core.pyx:60,239), and on every visible device."""
+    import threading
+
+    import torch
+
+    from paper_2107_10987_b200 import kernels
+
+    K = golden("kernels")
+    u = K["s0_u"]
+    ref_fx = K["s0_new_nc_fx"]
+    errs = []
+
+    def work(dev):
+        try:
+            with torch.cuda.device(dev):
+                torch.cuda.set_device(dev)
+                prim = kernels.primitives(u, 1.4, 1e-3)
+                lo, hi, _ = kernels.reconstruct(prim, 8, True, False, 1.4)
+                fx, _, _, _ = kernels.fluxes(lo, hi, 8, 1.4, True, False)
+                if bitwise_mismatch(fx, ref_fx):
+                    errs.append(f"device {dev}: flux mismatch")
+        except Exception as e:  # noqa: BLE001
+            errs.append(f"device {dev}: {e!r}")
+
+    ndev = torch.cuda.device_count()
+    th = [threading.Thread(target=work, args=(k % ndev,)) for k in range(8)]
+    for x in th:
+        x.start()
+    for x in th:
+        x.join()
+    assert not errs, errs
+
+
+def test_stepper_on_second_device():
+    """B200HydroStepper(device='cuda:1') while cuda:0 is current: allocations,
+    library setup and launches all land on device 1 (one step == golden)."""
+    import torch
+
+    if torch.cuda.device_count() < 2:
+        pytest.skip("needs 2 GPUs")
+    torch.cuda.set_device(0)
+    t, g = case_tree("sedov_c1")
+    st = _stepper(t, device="cuda:1")
+    assert st.state_tensor().device.index == 1
+    dt = st.cfl_dt(0.4)
+    assert dt == float(g["dts"][0])
+    st.rk3_step(dt)
+    _check_state(t, g)
+    assert torch.cuda.current_device() == 0
