@@ -23,7 +23,7 @@
 extern "C" {
 #endif
 
-#define OMB_ABI_VERSION 4
+#define OMB_ABI_VERSION 5
 
 /* per-leaf topology / geometry record (device array, one per leaf) */
 typedef struct {
@@ -128,6 +128,10 @@ int omb_unpack_leaves(const double *in, int n, double *u, long long fstride, int
  * the straight-line KT form, div_nz) differ from IEEE; bad[1..5] = first mismatch (a, b, a/b, div_by, KT form)
  * as bit patterns, bad[7] = claimed flag.  bad must hold 8 zeroed counters. */
 int omb_selftest_div(unsigned long long seed, long long n, unsigned long long *bad, void *stream);
+/* self-check of the device pow (csrc/omb_pow.cuh, glibc's algorithm and tables): out[i] = pow(x[i], y[i]),
+ * to be compared bitwise with the host libm's pow -- the reference's tau goes through glibc pow
+ * (reference.py:39, hydro/eos.py:50-61) */
+int omb_selftest_pow(const double *x, const double *y, long long n, double *out, void *stream);
 /* host (CPU) packing between per-leaf padded arrays (6, n+6, n+6, n+6) -- SubGrid.u, tree.py:47-61 --
  * and the [6][L][n^3] device layout; multithreaded, used around H2D/D2H copies */
 int omb_host_pack(const double *const *leaf_u, int L, int n, long long fstride, double *out);

@@ -51,6 +51,7 @@ def lib():
                                     ctypes.c_int])
     L.orc_stage_fluxes.restype = ctypes.c_int
     L.orc_max_threads.restype = ctypes.c_int
+    L.orc_pow_batch.argtypes = [_dp, _dp, ctypes.c_long, _dp]
     # the face tables come from the geometry generator (reference geometry.py:51-123 semantics)
     from ._tables import flat_face_table
 
@@ -104,3 +105,12 @@ def leaf_speed(interior, gamma, eta):
 
 def max_threads():
     return int(lib().orc_max_threads())
+
+
+def pow_batch(x, y):
+    """libm pow element-wise (the host reference of the device pow self-check)."""
+    x = np.ascontiguousarray(x, dtype=np.float64)
+    y = np.ascontiguousarray(y, dtype=np.float64)
+    out = np.empty_like(x)
+    lib().orc_pow_batch(_p(x), _p(y), x.size, _p(out))
+    return out

@@ -450,3 +450,8 @@ int orc_stage_fluxes(int L, int n, const double *U, double gamma, double eta, in
 }
 
 int orc_max_threads(void) { return (int)sysconf(_SC_NPROCESSORS_ONLN); }
+
+/* libm pow element-wise: the host side of the device pow self-check (tests only) */
+void orc_pow_batch(const double *x, const double *y, long n, double *out) {
+  for (long i = 0; i < n; i++) out[i] = pow(x[i], y[i]);
+}

@@ -551,6 +551,13 @@ __global__ void k_unpack(const double* __restrict__ in, int n, double* __restric
 
 // self-test of div_by (Markstein quotient) against the IEEE division on
 // random operands spanning 2^[-60,60] with random signs, 1 in 8 numerators 0
+// pow_glibc element-wise (the self-check of omb_pow.cuh against the host's libm)
+__global__ void k_pow_batch(const double* __restrict__ x, const double* __restrict__ y, long long n,
+                            double* __restrict__ out) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+    out[i] = pow_glibc(x[i], y[i]);
+}
+
 __global__ void k_selftest_div(unsigned long long seed, long long n, unsigned long long* bad) {
   unsigned long long s = seed ^ (0x9E3779B97F4A7C15ull * (blockIdx.x * blockDim.x + threadIdx.x + 1));
   unsigned long long nb = 0;
@@ -856,6 +863,13 @@ int omb_unpack_leaves(const double* in, int n, double* U, long long fstride, int
 int omb_selftest_div(unsigned long long seed, long long n, unsigned long long* bad, void* stream) {
   k_selftest_div<<<148 * 8, 256, 0, (cudaStream_t)stream>>>(seed, n, bad);
   CK(cudaGetLastError(), "omb_selftest_div launch");
+  return 0;
+}
+
+int omb_selftest_pow(const double* x, const double* y, long long n, double* out, void* stream) {
+  if (n <= 0) return 0;
+  k_pow_batch<<<148 * 8, 256, 0, (cudaStream_t)stream>>>(x, y, n, out);
+  CK(cudaGetLastError(), "omb_selftest_pow launch");
   return 0;
 }
 

@@ -23,6 +23,8 @@
 #define OMB_HD inline
 #endif
 
+#include "omb_pow.cuh"  // glibc's pow, bit for bit (tau: reference.py:39, eos.py:50-61)
+
 namespace omb {
 
 constexpr int NF = 6;
@@ -263,7 +265,7 @@ OMB_HD void prim_cell(const double* u, double gamma, double gm1, double eta, dou
   double vx = u[1] * inv, vy = u[2] * inv, vz = u[3] * inv;
   double kin = 0.5 * ((u[1] * vx + u[2] * vy) + u[3] * vz);
   double e1 = u[4] - kin;
-  double eint = (e1 >= eta * u[4]) ? e1 : pow(u[5], gamma);
+  double eint = (e1 >= eta * u[4]) ? e1 : pow_glibc(u[5], gamma);
   w[0] = rho;
   w[1] = vx;
   w[2] = vy;
@@ -284,7 +286,7 @@ OMB_HD double speed_cell(const double* u, double gamma, double gm1, double eta) 
   double vm = nanmax(nanmax(div_nz(fabs(u[1]), rho), div_nz(fabs(u[2]), rho)), div_nz(fabs(u[3]), rho));
   double kin = div_nz(0.5 * ((u[1] * u[1] + u[2] * u[2]) + u[3] * u[3]), rho);
   double e1 = u[4] - kin;
-  double eint = (e1 >= eta * u[4]) ? e1 : pow(u[5], gamma);
+  double eint = (e1 >= eta * u[4]) ? e1 : pow_glibc(u[5], gamma);
   double p = gm1 * eint;
   return vm + sqrt(gamma * p / rho);
 }
@@ -339,7 +341,7 @@ OMB_HD void update_cell_fin(const UpdateParams& P, double* nw, double* out) {
   {  // dual_energy_sync
     double kin = div_nz(0.5 * ((nw[1] * nw[1] + nw[2] * nw[2]) + nw[3] * nw[3]), nw[0]);
     double e1 = nw[4] - kin;
-    if (e1 >= P.eta * nw[4]) nw[5] = pow(fabs(e1), P.inv_gamma);
+    if (e1 >= P.eta * nw[4]) nw[5] = pow_glibc(fabs(e1), P.inv_gamma);
   }
   if (P.floor_rho > 0.0 && nw[0] < P.floor_rho) nw[0] = P.floor_rho;
   if (P.floor_vmax > 0.0 && P.floor_rho > 0.0) {

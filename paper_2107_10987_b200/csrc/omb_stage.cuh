@@ -149,10 +149,20 @@ static_assert(Smem::RAW_SIZE >= 4 * NF * PL, "prologue staging of planes 0..3 us
 // 8-byte global -> shared asynchronous copy (cp.async / LDGSTS on the GPU,
 // an immediate copy in the host emulation), completed by async_wait_all()
 // followed by a barrier.
+// The host emulation (tests/native/emu_stage.cpp, OMB_EMU_ASYNC) defers each
+// copy to the simulated thread's matching wait, like the hardware, so a read
+// of staged data before its wait + barrier shows up as a parity failure.
+#if !defined(__CUDA_ARCH__) && defined(OMB_EMU_ASYNC)
+void omb_emu_async_copy(double* dst, const double* src);
+void omb_emu_async_commit();
+void omb_emu_async_wait(int keep);
+#endif
 OMB_HD void async_copy8(double* dst_smem, const double* src) {
 #ifdef __CUDA_ARCH__
   unsigned sa = (unsigned)__cvta_generic_to_shared(dst_smem);
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sa), "l"(src) : "memory");
+#elif defined(OMB_EMU_ASYNC)
+  omb_emu_async_copy(dst_smem, src);
 #else
   *dst_smem = *src;
 #endif
@@ -160,17 +170,23 @@ OMB_HD void async_copy8(double* dst_smem, const double* src) {
 OMB_HD void async_commit() {
 #ifdef __CUDA_ARCH__
   asm volatile("cp.async.commit_group;\n" ::: "memory");
+#elif defined(OMB_EMU_ASYNC)
+  omb_emu_async_commit();
 #endif
 }
 OMB_HD void async_wait_all() {
 #ifdef __CUDA_ARCH__
   asm volatile("cp.async.wait_all;\n" ::: "memory");
+#elif defined(OMB_EMU_ASYNC)
+  omb_emu_async_wait(0);
 #endif
 }
 // wait until at most the most recently committed group is still in flight
 OMB_HD void async_wait_prev() {
 #ifdef __CUDA_ARCH__
   asm volatile("cp.async.wait_group 1;\n" ::: "memory");
+#elif defined(OMB_EMU_ASYNC)
+  omb_emu_async_wait(1);
 #endif
 }
 

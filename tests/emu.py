@@ -30,6 +30,7 @@ def lib():
                            check=True)
         _lib = ctypes.CDLL(SO)
         _lib.emu_stage.argtypes = [ctypes.POINTER(OmbStageDesc), ctypes.c_int]
+        _lib.emu_set_order.argtypes = [ctypes.c_int]
         _lib.emu_gather.argtypes = [ctypes.c_void_p, ctypes.c_longlong, ctypes.c_void_p, ctypes.c_int, ctypes.c_int,
                                     ctypes.c_void_p]
         _lib.emu_amr_ghosts.argtypes = [ctypes.POINTER(OmbAmrDesc)]
@@ -82,7 +83,9 @@ class EmuStepper:
                              floor_vmax=self.floors[2], bc=b.bc, new_mode=self.flags[0],
                              override_center=self.flags[1], contact=self.flags[2], amax_bits=ptr(am),
                              fallback=ptr(fb), flux=ptr(flux))
-            lib().emu_stage(ctypes.byref(d), self.nthr)
+            rc = lib().emu_stage(ctypes.byref(d), self.nthr)
+            if rc != 0:
+                raise RuntimeError(f"emu_stage failed ({rc})")
             if len(rleaf):
                 lib().emu_reflux_update(ctypes.byref(OmbRefluxDesc(stage=d, leaf=ptr(rleaf), off=ptr(roff),
                                                                    tasks=ptr(rtasks), nleaves=len(rleaf))))
@@ -172,7 +175,9 @@ class EmuDistStepper:
                              gamma=self.gamma, gm1=self.gamma - 1.0, eta=1e-3, inv_gamma=1.0 / self.gamma,
                              omega=0.0, floor_rho=0.0, floor_tau=0.0, floor_vmax=0.0, bc=b.bc, new_mode=1,
                              override_center=0, contact=0, amax_bits=ptr(am), fallback=ptr(fb), flux=ptr(flux))
-            lib().emu_stage(ctypes.byref(d), self.nthr)
+            rc = lib().emu_stage(ctypes.byref(d), self.nthr)
+            if rc != 0:
+                raise RuntimeError(f"emu_stage failed ({rc})")
             if self.part.amr:
                 self._exchange_fluxes(flux)
             if len(rleaf):

@@ -8,10 +8,40 @@
 
 #include <vector>
 
+#define OMB_EMU_ASYNC  // cp.async copies land at the issuing thread's wait (see omb_stage.cuh)
 #include "../../include/omb200.h"
 #include "../../paper_2107_10987_b200/csrc/omb_stage.cuh"
 
 using namespace omb;
+
+// ---- simulated cp.async: per simulated thread, committed groups of pending copies
+struct Pending {
+  double* dst;
+  double val;  // global sources are read-only during a stage: the value at issue is the value copied
+};
+static int g_tid = 0;
+static std::vector<std::vector<Pending>> g_open;                 // [thread] uncommitted copies
+static std::vector<std::vector<std::vector<Pending>>> g_groups;  // [thread][group]
+void omb::omb_emu_async_copy(double* dst, const double* src) { g_open[g_tid].push_back({dst, *src}); }
+void omb::omb_emu_async_commit() {
+  g_groups[g_tid].push_back(std::move(g_open[g_tid]));
+  g_open[g_tid].clear();
+}
+// keep = 0: cp.async.wait_all (= commit + wait_group 0); keep = 1: wait_group 1
+void omb::omb_emu_async_wait(int keep) {
+  if (keep == 0) omb_emu_async_commit();
+  auto& G = g_groups[g_tid];
+  size_t done = G.size() > (size_t)keep ? G.size() - keep : 0;
+  for (size_t k = 0; k < done; k++)
+    for (const Pending& p : G[k]) *p.dst = p.val;
+  G.erase(G.begin(), G.begin() + done);
+}
+
+// order in which the simulated threads run inside one barrier interval:
+// 0 ascending, 1 descending, 2 a stride-97 permutation.  A result that depends
+// on the order is a shared-memory race between threads of one interval.
+static int g_order = 0;
+extern "C" void emu_set_order(int mode) { g_order = mode; }
 
 extern "C" int emu_stage(const OmbStageDesc* d, int nthr) {
   if (nthr < 2 * NFACEX) return -1;  // the phase layout needs >= 128 threads
@@ -23,6 +53,10 @@ extern "C" int emu_stage(const OmbStageDesc* d, int nthr) {
   A.bc = d->bc; A.new_mode = d->new_mode; A.quad = d->new_mode && !d->override_center; A.contact = d->contact;
   A.amax_bits = d->amax_bits; A.fallback = d->fallback; A.flux = d->flux; A.halo = d->halo; A.nown = d->nown;
   std::vector<double> S(Smem::TOTAL);
+  std::vector<int> order(nthr);
+  for (int k = 0; k < nthr; k++) order[k] = g_order == 0 ? k : (g_order == 1 ? nthr - 1 - k : (int)((97LL * k) % nthr));
+  g_open.assign(nthr, {});
+  g_groups.assign(nthr, {});
   for (int run = 0; run < d->nruns; run++) {
     std::fill(S.begin(), S.end(), NAN);  // catch reads of never-written shared memory
     std::vector<Stage> st(nthr);
@@ -34,11 +68,12 @@ extern "C" int emu_stage(const OmbStageDesc* d, int nthr) {
       st[t].amax = 0.0; st[t].fb = 0;
     }
     int R = st[0].R;
-#define ALL(stmt) for (int t = 0; t < nthr; t++) { Stage& s = st[t]; (void)s; stmt; }
+#define ALL(stmt) for (int k_ = 0; k_ < nthr; k_++) { int t = order[k_]; g_tid = t; Stage& s = st[t]; (void)s; stmt; }
     ALL(s.bind_run_info(); s.stage_run_info(t, nthr));
-    // the phase sequence of k_stage (omb_kernels.cu), one ALL() per barrier interval
-    for (int X = 0; X < 4; X++) ALL(s.prefetch_plane(X, t, nthr, Smem::RAW + X * NF * PL));
-    ALL(s.prefetch_plane(4, t, nthr));
+    // the phase sequence of k_stage (omb_kernels.cu), one ALL() per barrier interval,
+    // with its cp.async commits and waits at the same points
+    ALL(for (int X = 0; X < 4; X++) s.prefetch_plane(X, t, nthr, Smem::RAW + X * NF * PL);
+        s.prefetch_plane(4, t, nthr); async_commit(); async_wait_all());
     for (int X = 0; X < 4; X++) ALL(s.convert_plane(X, t, nthr, Smem::RAW + X * NF * PL));
     const int ngroups = A.new_mode ? 2 : 1;
     const int T6 = NF * NYF - (512 - PL);
@@ -46,21 +81,26 @@ extern "C" int emu_stage(const OmbStageDesc* d, int nthr) {
       ALL(s.set_plane(X));
       ALL(if (X + 2 < 8 * R + 6) s.convert_plane(X + 2, t, nthr);
           if (X - 1 >= 3) { s.set_plane(X - 1); s.faces_yz(t, nthr, PL); s.set_plane(X); }
-          if (s.interior(X - 2) && t >= T6 && t < T6 + NFACEX) s.prefetch_update(X - 2, t - T6, NFACEX));
-      ALL(if (X + 3 < 8 * R + 6) s.prefetch_plane(X + 3, t, nthr));
+          if (s.interior(X - 2) && t >= T6 && t < T6 + NFACEX) s.prefetch_update(X - 2, t - T6, NFACEX);
+          async_commit());
       const bool p6 = X >= 3 && st[0].interior(X - 2);
       for (int g = 0; g < ngroups; g++) {
-        ALL(s.boundary_lines(g, t, nthr, h[t]));
+        ALL(if (g == 0) { if (X + 3 < 8 * R + 6) s.prefetch_plane(X + 3, t, nthr); async_commit(); }
+            s.boundary_lines(g, t, nthr, h[t]);
+            if (g == 0) async_wait_prev());
         ALL(s.store_hi(h[t]);
             if (X >= 3) { if (g == 0) s.combine_A(t, nthr); else if (A.quad) s.combine_B(t, nthr); }
             if (g == 0 && p6 && t >= nthr - NFACEX) { s.set_plane(X - 1); s.update_plane_a(t - (nthr - NFACEX), NFACEX); s.set_plane(X); });
       }
       ALL(s.inplane_lines(t, nthr);
           if (p6 && t >= nthr - NFACEX) { s.set_plane(X - 1); s.update_plane_b(t - (nthr - NFACEX), NFACEX); s.set_plane(X); });
-      ALL(if (s.interior(X)) s.inplane_fluxes(t, nthr));
+      ALL(if (s.interior(X)) s.inplane_fluxes(t, nthr); async_wait_all());
     }
-    ALL(s.set_plane(8 * R + 3); s.faces_yz(t, nthr); if (t < NFACEX) s.prefetch_update(8 * R + 2, t, NFACEX));
+    ALL(s.set_plane(8 * R + 3); s.faces_yz(t, nthr); if (t < NFACEX) s.prefetch_update(8 * R + 2, t, NFACEX);
+        async_commit(); async_wait_all());
     ALL(s.set_plane(8 * R + 3); s.update_plane(t, nthr));
+    for (int t = 0; t < nthr; t++)
+      if (!g_open[t].empty() || !g_groups[t].empty()) return -3;  // a copy never waited for
     double m = 0.0;
     long long f = 0;
     for (int t = 0; t < nthr; t++) {

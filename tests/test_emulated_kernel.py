@@ -137,3 +137,24 @@ def test_emulated_override_equals_old(override):
     for _ in range(10):
         em.rk3_step(dt)
     assert bitwise_mismatch(state_of(t), g["final"]) == 0
+
+
+@pytest.mark.parametrize("order", [1, 2])
+@pytest.mark.parametrize("name", ["smooth_reflecting", "amr_sedov_small", "contact_step"])
+def test_emulated_race_check(order, name):
+    """Shared-memory race check of the fused kernel's phase code (compute-sanitizer
+    is unavailable on the GPU pool): the simulated threads of every barrier
+    interval run in descending / permuted order, and the cp.async staging lands
+    only at the issuing thread's wait.  A read of data another thread writes in
+    the same interval, or of a staged copy before its wait + barrier, changes the
+    result; the golden step must come out bitwise regardless."""
+    t, g = case_tree(name)
+    lib().emu_set_order(order)
+    try:
+        em = EmuStepper(t, 1.4, contact=(name == "contact_step"), max_run=4)
+        em.rk3_step(float(g["dts"][0]))
+    finally:
+        lib().emu_set_order(0)
+    assert bitwise_mismatch(state_of(t), g["state1"]) == 0
+    assert em.amax == float(g["amax"][0])
+    assert em.fallback == int(g["fallback"][0])

@@ -5,9 +5,9 @@ tests/test_oracle.py), on the same synthetic inputs bench.py times.
 
 The reference path matched: ``pkg/src/octomini/hydro/step.py:81-144``
 (cfl_dt + rk3_step); inputs are SURVEY.md §8(d)'s constructions.  Bar per cell
-after one step: rho, momenta, egas bitwise; tau bitwise where the device pow is
-glibc's (csrc/omb_pow.cuh) -- the north_star tolerance 1e-12 is asserted for every
-field regardless; dt, amax and fallback counts exactly equal.
+after one step: every field bitwise (tau too: the device pow is glibc's,
+csrc/omb_pow.cuh), the north_star tolerance 1e-12 asserted as well; dt, amax and
+fallback counts exactly equal.
 """
 
 import os
@@ -46,6 +46,7 @@ def _oracle(t, gamma=1.4, **kw):
 def _same(got, ref, where):
     assert bitwise_mismatch(got[:, :5], ref[:, :5]) == 0, f"{where}: rho/momenta/egas not bitwise"
     assert rel_close(got, ref, 1e-12) == 0, f"{where}: outside 1e-12"
+    assert bitwise_mismatch(got, ref) == 0, f"{where}: tau not bitwise"
 
 
 def _restore(t, arr):
@@ -140,10 +141,7 @@ def test_c5_standin_level4_vs_oracle():
     o.rk3_step(dt)
     a, b = state_of(tg), state_of(tc)
     assert rel_close(a, b, 1e-12) == 0
-    from paper_2107_10987_b200 import _lib
-
-    if getattr(_lib, "GLIBC_POW", False):  # device pow == glibc pow: every field bitwise
-        assert bitwise_mismatch(a, b) == 0
+    assert bitwise_mismatch(a, b) == 0  # tau branch in the atmosphere: glibc pow on the device
     assert st.amax == o.amax
     assert st.fallback_count == o.fallback
 

@@ -82,8 +82,9 @@ def _stepper(t, **kw):
 def _check_state(t, g, key="state1"):
     got = state_of(t)
     ref = g[key]
-    # rho, momenta, egas bitwise; tau via pow: bitwise vs glibc is not guaranteed by CUDA's pow
+    # every field bitwise, tau included (the device pow is glibc's, csrc/omb_pow.cuh)
     assert bitwise_mismatch(got[:, :5], ref[:, :5]) == 0
+    assert bitwise_mismatch(got, ref) == 0
     assert rel_close(got, ref, 1e-12) == 0
 
 
@@ -236,10 +237,7 @@ def test_amr_reflux_two_steps_gpu():
             _check_state(t, g)
         assert stats.amax == float(g["amax"][s])
     got = np.ascontiguousarray(state_of(t))
-    if hashlib.sha256(got.tobytes()).hexdigest() != str(g["final_sha"]):
-        # tau may differ by an ulp through CUDA's pow; everything else must be bitwise
-        assert rel_close(got, g["final"], 1e-12) == 0
-        assert bitwise_mismatch(got[:, :5], g["final"][:, :5]) == 0
+    assert hashlib.sha256(got.tobytes()).hexdigest() == str(g["final_sha"])
 
 
 def test_synthetic_star_matches_oracle():
@@ -259,9 +257,10 @@ def test_synthetic_star_matches_oracle():
         gpu.rk3_step(dt)
         ref.rk3_step(dt)
     a, b = state_of(tg), state_of(tc)
-    # the atmosphere uses the dual-energy tau branch (pressure from tau**gamma): CUDA's pow is
-    # not glibc's, so only the north_star tolerance is guaranteed here (bitwise elsewhere)
+    # the atmosphere uses the dual-energy tau branch (pressure from tau**gamma): with glibc's
+    # pow on the device every field is bitwise
     assert rel_close(a, b, 1e-12) == 0
+    assert bitwise_mismatch(a, b) == 0
 
 
 def _ghosts(t):
@@ -467,3 +466,36 @@ def test_stepper_on_second_device():
     st.rk3_step(dt)
     _check_state(t, g)
     assert torch.cuda.current_device() == 0
+
+
+def test_device_pow_is_glibc():
+    """pow_glibc on the device == the host libm's pow, bit for bit: 2^22 random
+    pairs over every exponent, the exponents the step uses, and edge cases."""
+    import ctypes
+
+    import torch
+
+    import oracle  # checker only
+    from paper_2107_10987_b200 import _lib
+
+    rng = np.random.default_rng(7)
+    n = 1 << 22
+    xb = rng.integers(0, 2 ** 63, n, dtype=np.uint64)
+    x = xb.view(np.float64).copy()
+    y = rng.integers(0, 2 ** 63, n, dtype=np.uint64).view(np.float64).copy()
+    y[::2] = rng.choice([1.4, 1 / 1.4, 5 / 3, 0.6], n // 2)
+    x[1::4] = np.exp(rng.uniform(-30, 30, len(x[1::4])))
+    x[3::8] = -x[3::8]
+    y[3::16] = 3.0
+    edge = np.array([0.0, -0.0, 1.0, -1.0, np.inf, -np.inf, np.nan, 5e-324, 2.2250738585072014e-308, 1e-300, 1e300])
+    ex, ey = np.meshgrid(edge, np.array([0.0, 1.0, -1.0, 2.0, 0.5, 1.4, -1.4, np.inf, -np.inf, np.nan, 1e300]))
+    x = np.concatenate([x, ex.ravel()])
+    y = np.concatenate([y, ey.ravel()])
+    ref = oracle.pow_batch(x, y)
+    dx, dy = torch.from_numpy(x).cuda(), torch.from_numpy(y).cuda()
+    out = torch.empty_like(dx)
+    L = _lib.load()
+    _lib.check(L.omb_selftest_pow(dx.data_ptr(), dy.data_ptr(), x.size, out.data_ptr(),
+                                  ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)), "omb_selftest_pow")
+    got = out.cpu().numpy()
+    assert bitwise_mismatch(got, ref) == 0
