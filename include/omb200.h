@@ -128,6 +128,17 @@ int omb_unpack_leaves(const double *in, int n, double *u, long long fstride, int
  * the straight-line KT form, div_nz) differ from IEEE; bad[1..5] = first mismatch (a, b, a/b, div_by, KT form)
  * as bit patterns, bad[7] = claimed flag.  bad must hold 8 zeroed counters. */
 int omb_selftest_div(unsigned long long seed, long long n, unsigned long long *bad, void *stream);
+/* scalar flux surface (hydro/flux.py:12-94; the reference's test oracle for the point flux):
+ * omb_kt_flux  <- flux.kt_flux(left, right, axis, eos) for n point pairs; states [n][7] =
+ *   (rho, vx, vy, vz, p, eint, tau) as PrimitiveState holds them; out [n][6].  A pair with a
+ *   non-finite rho/v/p gets NaNs and atomically lowers *bad (init n) to its index: the caller raises
+ *   NumericsError like flux.py:56-58.
+ * omb_face_flux <- flux.face_flux(point_fluxes, new_mode) for n faces; pts [n][9][6], out [n][6] */
+int omb_kt_flux(const double *left, const double *right, int n, int axis, double gamma, double *out, int *bad,
+                void *stream);
+/* omb_physical_flux <- flux.physical_flux(state, axis) (flux.py:40-47) for n states [n][7] */
+int omb_physical_flux(const double *states, int n, int axis, double *out, void *stream);
+int omb_face_flux(const double *pts, int n, int new_mode, double *out, void *stream);
 /* self-check of the device pow (csrc/omb_pow.cuh, glibc's algorithm and tables): out[i] = pow(x[i], y[i]),
  * to be compared bitwise with the host libm's pow -- the reference's tau goes through glibc pow
  * (reference.py:39, hydro/eos.py:50-61) */

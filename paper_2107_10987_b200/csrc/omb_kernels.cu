@@ -551,6 +551,82 @@ __global__ void k_unpack(const double* __restrict__ in, int n, double* __restric
 
 // self-test of div_by (Markstein quotient) against the IEEE division on
 // random operands spanning 2^[-60,60] with random signs, 1 in 8 numerators 0
+// ---------------------------------------------------------------------------
+// scalar flux surface (hydro/flux.py:12-94): kt_flux / physical_flux on point
+// states, face_flux on 9 point fluxes -- batched, one thread per point
+// ---------------------------------------------------------------------------
+// state s = (rho, vx, vy, vz, p, eint, tau): PrimitiveState.conserved (flux.py:32-37)
+OMB_HD void pt_conserved(const double* s, double* u) {
+  // Python float ** 2 is C pow(x, 2.0), i.e. glibc's pow
+  double kin = 0.5 * s[0] * ((pow_glibc(s[1], 2.0) + pow_glibc(s[2], 2.0)) + pow_glibc(s[3], 2.0));
+  u[0] = s[0];
+  u[1] = s[0] * s[1];
+  u[2] = s[0] * s[2];
+  u[3] = s[0] * s[3];
+  u[4] = s[0] * s[5] + kin;
+  u[5] = s[6];
+}
+// physical_flux (flux.py:40-47)
+OMB_HD void pt_physical(const double* s, int axis, double* f) {
+  double u[NF];
+  pt_conserved(s, u);
+  double vn = s[1 + axis];
+  for (int v = 0; v < NF; v++) f[v] = u[v] * vn;
+  f[1 + axis] += s[4];
+  f[4] += s[4] * vn;
+}
+__global__ void k_kt_points(const double* __restrict__ L, const double* __restrict__ R, int n, int axis, double gamma,
+                            double* __restrict__ out, int* __restrict__ bad) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const double* l = L + 7 * i;
+  const double* r = R + 7 * i;
+  double* o = out + NF * i;
+  for (int k = 0; k < 5; k++)  // flux.py:56-58: rho, v, p must be finite
+    if (!isfinite(l[k]) || !isfinite(r[k])) {
+      atomicMin(bad, i);
+      for (int v = 0; v < NF; v++) o[v] = NAN;
+      return;
+    }
+  double cl = sqrt(gamma * l[4] / l[0]), cr = sqrt(gamma * r[4] / r[0]);
+  double vl = l[1 + axis], vr = r[1 + axis];
+  // Python max(0.0, a, b) / min(...): the first extreme argument wins
+  double ap = 0.0, am = 0.0;
+  if (vl + cl > ap) ap = vl + cl;
+  if (vr + cr > ap) ap = vr + cr;
+  if (vl - cl < am) am = vl - cl;
+  if (vr - cr < am) am = vr - cr;
+  double fl[NF], fr[NF], ul[NF], ur[NF];
+  pt_physical(l, axis, fl);
+  if (ap - am <= 0.0) {
+    for (int v = 0; v < NF; v++) o[v] = fl[v];
+    return;
+  }
+  pt_physical(r, axis, fr);
+  pt_conserved(l, ul);
+  pt_conserved(r, ur);
+  for (int v = 0; v < NF; v++) o[v] = ((ap * fl[v] - am * fr[v]) + (ap * am) * (ur[v] - ul[v])) / (ap - am);
+}
+__global__ void k_physical_points(const double* __restrict__ S, int n, int axis, double* __restrict__ out) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) pt_physical(S + 7 * i, axis, out + NF * i);
+}
+// face_flux (flux.py:70-91): pts [n][9][6] (centre, 4 edges, 4 vertices) -> out [n][6]
+__global__ void k_face_points(const double* __restrict__ pts, int n, int new_mode, double* __restrict__ out) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n * NF) return;
+  int f = i / NF, v = i % NF;
+  const double* p = pts + (long long)f * 9 * NF;
+  double c = p[v];
+  if (!new_mode) {
+    out[i] = c;
+    return;
+  }
+  double edev = ((p[1 * NF + v] - c) + (p[2 * NF + v] - c)) + ((p[3 * NF + v] - c) + (p[4 * NF + v] - c));
+  double vdev = ((p[5 * NF + v] - c) + (p[6 * NF + v] - c)) + ((p[7 * NF + v] - c) + (p[8 * NF + v] - c));
+  out[i] = c + (4.0 * edev + vdev) / 36.0;
+}
+
 // pow_glibc element-wise (the self-check of omb_pow.cuh against the host's libm)
 __global__ void k_pow_batch(const double* __restrict__ x, const double* __restrict__ y, long long n,
                             double* __restrict__ out) {
@@ -863,6 +939,30 @@ int omb_unpack_leaves(const double* in, int n, double* U, long long fstride, int
 int omb_selftest_div(unsigned long long seed, long long n, unsigned long long* bad, void* stream) {
   k_selftest_div<<<148 * 8, 256, 0, (cudaStream_t)stream>>>(seed, n, bad);
   CK(cudaGetLastError(), "omb_selftest_div launch");
+  return 0;
+}
+
+int omb_kt_flux(const double* left, const double* right, int n, int axis, double gamma, double* out, int* bad,
+                void* stream) {
+  if (n <= 0) return 0;
+  if (axis < 0 || axis > 2) return set_err("omb_kt_flux: axis must be 0, 1 or 2");
+  k_kt_points<<<(n + 127) / 128, 128, 0, (cudaStream_t)stream>>>(left, right, n, axis, gamma, out, bad);
+  CK(cudaGetLastError(), "omb_kt_flux launch");
+  return 0;
+}
+
+int omb_physical_flux(const double* states, int n, int axis, double* out, void* stream) {
+  if (n <= 0) return 0;
+  if (axis < 0 || axis > 2) return set_err("omb_physical_flux: axis must be 0, 1 or 2");
+  k_physical_points<<<(n + 127) / 128, 128, 0, (cudaStream_t)stream>>>(states, n, axis, out);
+  CK(cudaGetLastError(), "omb_physical_flux launch");
+  return 0;
+}
+
+int omb_face_flux(const double* pts, int n, int new_mode, double* out, void* stream) {
+  if (n <= 0) return 0;
+  k_face_points<<<(n * NF + 127) / 128, 128, 0, (cudaStream_t)stream>>>(pts, n, new_mode, out);
+  CK(cudaGetLastError(), "omb_face_flux launch");
   return 0;
 }
 

@@ -405,10 +405,37 @@ def mode_cases():
          amax_last=np.array(stats.amax), fallback_last=np.array(stats.fallback_count))
 
 
+def flux_point_cases():
+    """The scalar flux surface (hydro/flux.py): kt_flux on random point pairs for
+    every axis, physical_flux, face_flux on random 9-point sets (both modes)."""
+    from octomini.hydro.flux import face_flux, physical_flux
+
+    rng = np.random.default_rng(21)
+    n = 64
+    rho = rng.uniform(0.1, 3.0, (2, n))
+    p = rng.uniform(0.1, 3.0, (2, n))
+    v = rng.normal(0, 1.5, (2, n, 3))
+    v[:, :8] *= 8.0  # some supersonic pairs (one-sided upwinding)
+    out = {}
+    st = [[PrimitiveState.from_fields(float(rho[k, i]), tuple(float(x) for x in v[k, i]), float(p[k, i]), EOS)
+           for i in range(n)] for k in range(2)]
+    out["states"] = np.array([[[s.rho, s.vx, s.vy, s.vz, s.p, s.eint, s.tau] for s in st[k]] for k in range(2)])
+    for ax in range(3):
+        out[f"kt_{ax}"] = np.array([kt_flux(st[0][i], st[1][i], ax, EOS) for i in range(n)])
+        out[f"phys_{ax}"] = np.array([physical_flux(st[0][i], ax) for i in range(n)])
+    pts = rng.normal(0, 1, (32, 9, 6))
+    pts[0] = pts[0, 0]  # all nine equal: returned bit for bit
+    out["face_pts"] = pts
+    out["face_new"] = np.array([face_flux(q, True) for q in pts])
+    out["face_old"] = np.array([face_flux(q, False) for q in pts])
+    save("flux_points", **out)
+
+
 def main():
     if sys.argv[1:] == ["modes"]:
         mode_cases()
         density_gravity_cases()
+        flux_point_cases()
         return
     if sys.argv[1:] == ["fmm"]:
         fmm_case()
@@ -444,6 +471,7 @@ def main():
     gravity_step_case()
     mode_cases()
     density_gravity_cases()
+    flux_point_cases()
 
 
 if __name__ == "__main__":
