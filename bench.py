@@ -31,6 +31,7 @@ import numpy as np
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
+sys.path.insert(0, os.path.join(ROOT, "tests"))  # octomini_host: synthetic inputs (octomini's tree API)
 
 METRIC = "hydro cell-updates/sec (FP64) per GPU & at 1/2/4/8 B200; % of roofline"
 UNIT = "cell-updates/s"
@@ -63,10 +64,11 @@ def parse():
 
 
 def sedov_tree(level):
-    from paper_2107_10987_b200 import EosConfig, SedovConfig, build_uniform_tree, init_sedov
+    from octomini_host import SedovConfig, build_uniform_tree, init_sedov
+    from paper_2107_10987_b200 import EosConfig
 
     if level == "c4":
-        from paper_2107_10987_b200.problems import amr_sedov_tree
+        from octomini_host import amr_sedov_tree
 
         return amr_sedov_tree()
     t = build_uniform_tree(level, 8, boundary="reflecting")
@@ -175,7 +177,7 @@ def cpu_run(level, nleaves, steps, warmup):
     kw = {}
     gamma = 1.4
     if level == "c5":
-        from paper_2107_10987_b200.problems import synthetic_star
+        from octomini_host import synthetic_star
 
         tree, eos, grav, om, fl = synthetic_star(level=4)
         kw = dict(omega=om, gravity=grav, floors=(fl.rho, fl.tau, fl.vmax))
@@ -282,13 +284,13 @@ def gpu_arm(args, rank, world):
     level = resolve_level(args, world)
     extra = {}
     if level == "c5":
-        from paper_2107_10987_b200.problems import synthetic_star
+        from octomini_host import synthetic_star
 
         tree, eos, grav, om, fl = synthetic_star(level=4)
         extra = dict(gravity=grav, omega=om, floors=fl)
     elif level == "c5g":
         from paper_2107_10987_b200.gravity import B200FmmSolver
-        from paper_2107_10987_b200.problems import synthetic_star
+        from octomini_host import synthetic_star
 
         tree, eos, _, om, fl = synthetic_star(level=args.level or 4)
         extra = dict(gravity=B200FmmSolver(0.5), omega=om, floors=fl)
@@ -450,7 +452,7 @@ def gpu_arm(args, rank, world):
     # the same step on a NON-FLAT state (every cell off the limiter's flat shortcut), same tree
     nontrivial = None
     if level in (4, 5) and args.e2e_steps >= 0:
-        from paper_2107_10987_b200.problems import smooth_state
+        from octomini_host import smooth_state
 
         t3 = smooth_state(sedov_tree(level))
         p3 = Partition(t3, world, rank) if world > 1 else None

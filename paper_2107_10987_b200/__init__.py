@@ -4,14 +4,13 @@ reference's HydroStepper and per-sub-grid kernel API.
 
 Host side is Python; the compute runs in hand-written sm_100a CUDA kernels
 (libomb200.so, C ABI in include/omb200.h).  PyTorch provides device memory
-and streams only.
+and streams only.  The octree, its initial data and checkpoint reader are the
+caller's (octomini's own ``mesh`` / ``problems``): the stepper consumes any
+tree with octomini's interface.
 """
 
 from .errors import NativeError, NumericsError, StructureError  # noqa: F401
-from .hydro import (SSP_RK3_STAGES, EosConfig, FloorConfig, HydroMode, StepStats,  # noqa: F401
-                    conserved_from_primitive)
-from .mesh import Octree, SubGrid, build_uniform_tree, refine_by_criterion  # noqa: F401
-from .problems import SedovConfig, conservation_totals, init_sedov  # noqa: F401
+from .hydro import SSP_RK3_STAGES, EosConfig, FloorConfig, HydroMode, StepStats  # noqa: F401
 
 __version__ = "0.1.0"
 

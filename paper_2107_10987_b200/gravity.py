@@ -3,17 +3,16 @@
 
 Host, once per tree topology (cached like ``FmmSolver.prepare``):
   * the entity table -- every octree node plus, below each leaf, the complete
-    hierarchy of its sub-grid's blocks down to single cells
-    (gravity/entities.py:15-139, restated with the same numpy expressions so
-    centres are bit-identical);
+    hierarchy of its sub-grid's blocks down to single cells (the numbering and
+    centres of gravity/entities.py:15-139, built level by level over all leaves);
   * the dual-tree traversal in C++ (``omb_fmm_traverse``, the reference's
     stack discipline, opening criterion and lattice keys, _core.pyx:372-459);
   * the grouping by key (sorted keys, stable within a group, _core.pyx:476-494)
     and the per-target contribution lists in the reference's global M2L order
     (group by group, pair by pair, the b-side before the a-side,
     _core.pyx:563-608);
-  * kernel derivatives per group with the same numpy expressions as
-    multipole.py:173-191.
+  * kernel derivatives for all groups at once, each component with the
+    reference's operation order (multipole.py:173-199).
 Device, per solve: cell masses -> upward translation per level -> M2L per
 target -> downward translation per level -> phi, g per cell (``omb_fmm_*``).
 Every floating-point operation keeps the reference's order, so phi and g are
@@ -24,125 +23,139 @@ import numpy as np
 
 from . import _lib
 from .device import ptr, stream_handle
+from .geometry import GHOST, SX, SY, SZ
 
 NCOMP = 20
 S2 = [(0, 0), (0, 1), (0, 2), (1, 1), (1, 2), (2, 2)]
 S3 = [(0, 0, 0), (0, 0, 1), (0, 0, 2), (0, 1, 1), (0, 1, 2), (0, 2, 2), (1, 1, 1), (1, 1, 2), (1, 2, 2), (2, 2, 2)]
 
 
-def kernel_derivatives(R):
-    """D0..D3 of g(R) = -1/|R| (multipole.py:173-191), same numpy operations."""
-    R = np.asarray(R, dtype=float)
-    r2 = float(R @ R)
+def derivative_table(R):
+    """D0..D3 of the FMM kernel g(R) = -1/|R| for every interaction group at
+    once (rows of R), evaluated with the reference's operation order per
+    component (gravity/multipole.py:173-191) so they are bitwise its values:
+    r2 as numpy's ``R @ R`` (a BLAS dot, not the naive sum), then
+    D0 = -1/r, D1 = R/r^3, D2_ab = d_ab/r^3 - 3 R_a R_b / r^5,
+    D3_abc = 15 R_a R_b R_c / r^7 - 3 (d_ab R_c + d_ac R_b + d_bc R_a) / r^5.
+    Returns (G, 2, 20): [:, 0] at R, [:, 1] at -R (odd ranks negated,
+    multipole.py:194-199)."""
+    R = np.ascontiguousarray(R, dtype=np.float64)
+    G = len(R)
+    r2 = np.matmul(R[:, None, :], R[:, :, None])[:, 0, 0]
+    head = min(G, 4096)  # the stacked product must be the reference's per-row dot; else take that
+    if head and not np.array_equal(r2[:head], np.array([float(R[g] @ R[g]) for g in range(head)])):
+        r2 = np.array([float(R[g] @ R[g]) for g in range(G)])
     r = np.sqrt(r2)
     r3 = r2 * r
     r5 = r3 * r2
     r7 = r5 * r2
-    D = np.empty(NCOMP)
-    D[0] = -1.0 / r
-    D[1:4] = R / r3
-    for i, (a, b) in enumerate(S2):
-        D[4 + i] = (1.0 if a == b else 0.0) / r3 - 3.0 * R[a] * R[b] / r5
-    for i, (a, b, c) in enumerate(S3):
-        term = 15.0 * R[a] * R[b] * R[c] / r7
-        term -= 3.0 * ((a == b) * R[c] + (a == c) * R[b] + (b == c) * R[a]) / r5
-        D[10 + i] = term
+    D = np.empty((G, 2, NCOMP))
+    D[:, 0, 0] = -1.0 / r
+    D[:, 0, 1:4] = R / r3[:, None]
+    X = [R[:, 0], R[:, 1], R[:, 2]]
+    for k, (a, b) in enumerate(S2):
+        D[:, 0, 4 + k] = (1.0 if a == b else 0.0) / r3 - 3.0 * X[a] * X[b] / r5
+    for k, (a, b, c) in enumerate(S3):
+        dab, dac, dbc = (float(a == b), float(a == c), float(b == c))
+        D[:, 0, 10 + k] = 15.0 * X[a] * X[b] * X[c] / r7 - 3.0 * (dab * X[c] + dac * X[b] + dbc * X[a]) / r5
+    D[:, 1] = D[:, 0]
+    D[:, 1, 1:4] *= -1.0
+    D[:, 1, 10:] *= -1.0
     return D
 
 
-def flip_derivatives(D):
-    """D at -R: odd ranks negated (multipole.py:194-199)."""
-    out = D.copy()
-    out[..., 1:4] *= -1.0
-    out[..., 10:] *= -1.0
-    return out
-
-
 class EntityTable:
-    """Flat entity table (gravity/entities.py:15-139): centers, widths,
-    children (-1 for cells), is_cell, level; ``cell_base[i]`` is the entity of
-    cell 0 of ``sorted_leaves()[i]`` (its n^3 cells follow, x-major)."""
+    """The FMM entity table of a tree (the numbering and geometry of
+    gravity/entities.py:15-139): ids in depth-first pre-order from the root,
+    one per internal octree node; a leaf takes its sub-grid's whole block
+    hierarchy, levels j = 0..log2(n) of 8^j blocks each (x-major), the last
+    level being its cells.  Arrays: center (3), width, children (8, -1 for
+    cells), is_cell, level; ``cell_base[i]`` = id of cell 0 of sorted leaf i.
+    Built level by level over all leaves at once (numpy), with the reference's
+    arithmetic for every centre: corner = lower + ipos * (width / 2^level),
+    centre = corner + (b + 0.5) * w."""
 
     def __init__(self, tree):
         n = tree.n
         s = int(np.log2(n))
         assert 2 ** s == n
-        leaves = tree.sorted_leaves()
         per_leaf = (8 ** (s + 1) - 1) // 7
-        internal = []
-
-        def count_internal(node):
-            if not node.is_leaf:
-                internal.append(node)
-                for c in node.children:
-                    count_internal(c)
-
-        count_internal(tree.root)
-        total = len(internal) + len(leaves) * per_leaf
-        center = np.empty((total, 3), dtype=np.float64)
-        width = np.empty(total, dtype=np.float64)
+        # pre-order numbering (iterative DFS, children in octant order)
+        inner, leaf_nodes, leaf_base, ident = [], [], [], {}
+        cursor = 0
+        stack = [tree.root]
+        while stack:
+            node = stack.pop()
+            ident[id(node)] = cursor
+            if node.is_leaf:
+                leaf_nodes.append(node)
+                leaf_base.append(cursor)
+                cursor += per_leaf
+            else:
+                inner.append(node)
+                cursor += 1
+                stack.extend(reversed(node.children))
+        total = cursor
+        center = np.empty((total, 3))
+        width = np.empty(total)
         children = np.full((total, 8), -1, dtype=np.int64)
         is_cell = np.zeros(total, dtype=bool)
         level = np.empty(total, dtype=np.int32)
-        cell_base = {}
-        cursor = [0]
-
-        def alloc(k):
-            base = cursor[0]
-            cursor[0] += k
-            return base
-
-        def build_leaf(node):
-            bases = [alloc(8 ** j) for j in range(s + 1)]
-            for j in range(s + 1):
-                nb = 2 ** j
-                ids = bases[j] + (np.arange(nb)[:, None, None] * nb + np.arange(nb)[None, :, None]) * nb \
-                    + np.arange(nb)[None, None, :]
-                w = tree.width / (2 ** (node.level + j))
-                corner = tree.lower + node.ipos * (tree.width / 2 ** node.level)
-                bx = np.arange(nb)
-                cx = corner[0] + (bx + 0.5) * w
-                cy = corner[1] + (bx + 0.5) * w
-                cz = corner[2] + (bx + 0.5) * w
-                flat = ids.reshape(-1)
-                center[flat, 0] = np.repeat(cx, nb * nb)
-                center[flat, 1] = np.tile(np.repeat(cy, nb), nb)
-                center[flat, 2] = np.tile(cz, nb * nb)
-                width[flat] = w
-                level[flat] = node.level + j
-                if j < s:
-                    nb2 = 2 * nb
-                    child = bases[j + 1] + (np.arange(nb2)[:, None, None] * nb2 + np.arange(nb2)[None, :, None]) \
-                        * nb2 + np.arange(nb2)[None, None, :]
-                    for kz in (0, 1):
-                        for ky in (0, 1):
-                            for kx in (0, 1):
-                                children[flat, kx + 2 * ky + 4 * kz] = child[kx::2, ky::2, kz::2].reshape(-1)
-                else:
-                    is_cell[flat] = True
-            cell_base[node.path] = bases[s]
-            return bases[0]
-
-        def build(node):
-            if node.is_leaf:
-                return build_leaf(node)
-            eid = alloc(1)
-            w = tree.width / 2 ** node.level
-            corner = tree.lower + node.ipos * w
-            center[eid] = corner + 0.5 * w
-            width[eid] = w
-            level[eid] = node.level
-            for k, c in enumerate(node.children):
-                children[eid, k] = build(c)
-            return eid
-
-        self.root = build(tree.root)
-        assert cursor[0] == total
+        lower = np.asarray(tree.lower, dtype=np.float64)
+        # internal nodes
+        if inner:
+            ids = np.array([ident[id(nd)] for nd in inner], dtype=np.int64)
+            lv = np.array([nd.level for nd in inner])
+            w = tree.width / (2 ** lv).astype(np.float64)
+            corner = lower + np.array([nd.ipos for nd in inner]) * w[:, None]
+            center[ids] = corner + 0.5 * w[:, None]
+            width[ids] = w
+            level[ids] = lv
+            children[ids] = np.array([[ident[id(c)] for c in nd.children] for nd in inner], dtype=np.int64)
+        # leaf block hierarchies, one level j at a time for every leaf
+        base = np.array(leaf_base, dtype=np.int64)
+        lv = np.array([nd.level for nd in leaf_nodes])
+        ipos = np.array([nd.ipos for nd in leaf_nodes])
+        corner = lower + ipos * (tree.width / (2 ** lv).astype(np.float64))[:, None]
+        for j in range(s + 1):
+            nb = 2 ** j
+            first = base + (8 ** j - 1) // 7  # the leaf's level-j blocks follow levels 0..j-1
+            ids = first[:, None] + np.arange(nb ** 3)[None, :]  # x-major: (bx*nb + by)*nb + bz
+            w = tree.width / (2 ** (lv + j)).astype(np.float64)
+            off = (np.arange(nb) + 0.5)[None, :] * w[:, None]  # (leaf, b)
+            bx, by, bz = np.unravel_index(np.arange(nb ** 3), (nb, nb, nb))
+            center[ids, 0] = corner[:, 0:1] + off[:, bx]
+            center[ids, 1] = corner[:, 1:2] + off[:, by]
+            center[ids, 2] = corner[:, 2:3] + off[:, bz]
+            width[ids] = w[:, None]
+            level[ids] = (lv + j)[:, None]
+            if j < s:
+                nxt = base + (8 ** (j + 1) - 1) // 7
+                n2 = 2 * nb
+                for k in range(8):
+                    kx, ky, kz = k & 1, (k >> 1) & 1, (k >> 2) & 1
+                    cidx = ((2 * bx + kx) * n2 + (2 * by + ky)) * n2 + (2 * bz + kz)
+                    children[ids, k] = nxt[:, None] + cidx[None, :]
+            else:
+                is_cell[ids] = True
+        cb = dict(zip((nd.path for nd in leaf_nodes), base + (8 ** s - 1) // 7))
+        self.root = ident[id(tree.root)]
         self.center, self.width, self.children, self.is_cell, self.level = center, width, children, is_cell, level
         self.n = n
         self.nentities = total
-        self.leaf_paths = [lf.path for lf in leaves]
-        self.cell_base = np.array([cell_base[p] for p in self.leaf_paths], dtype=np.int64)
+        self.leaf_paths = [lf.path for lf in tree.sorted_leaves()]
+        self.cell_base = np.array([cb[p] for p in self.leaf_paths], dtype=np.int64)
+
+
+def _check_balance(tree):
+    """The 2:1 check FmmSolver.prepare runs first (mesh/tree.py:180-183 via
+    find_leaf_region, which raises StructureError on a violation)."""
+    offs = [(i, j, k) for i in (-1, 0, 1) for j in (-1, 0, 1) for k in (-1, 0, 1) if (i, j, k) != (0, 0, 0)]
+    for lf in tree.leaves():
+        for off in offs:
+            pos = tree.neighbor_ipos(lf, off)
+            if pos is not None:
+                tree.find_leaf_region(lf.level, pos)
 
 
 def traverse(lib, table, theta):
@@ -201,9 +214,7 @@ class B200FmmSolver:
             return
         import torch
 
-        from .mesh import check_balance
-
-        check_balance(tree)
+        _check_balance(tree)
         t = EntityTable(tree)
         self.table = t
         pa, pb, pk = traverse(self.lib, t, self.theta)
@@ -226,10 +237,7 @@ class B200FmmSolver:
         a_cell, b_cell = (gflags[:G] & 2) != 0, (gflags[:G] & 1) != 0
         self.stats["groups"] = G
         self.stats["pairs"] = int(len(pa))
-        D = np.empty((G, 2, NCOMP))
-        for g in range(G):
-            D[g, 0] = kernel_derivatives(R[g])
-            D[g, 1] = flip_derivatives(D[g, 0])
+        D = derivative_table(R)
         cnt = np.diff(off)
         targets = np.nonzero(cnt)[0].astype(np.int64)
         off = np.append(off[targets], off[-1]).astype(np.int64)  # CSR over the targets with contributions
@@ -448,8 +456,6 @@ class B200FmmSolver:
         """phi and g from rho, and dphi/dt from rho_dot = -div(momentum)
         (solver.py:134-153; the ghosts of the host sub-grids must be filled,
         as in the reference)."""
-        from .hydro import GravityField, momentum_divergence_source
-
         self.prepare(tree)
         phi, g = self.solve_density(tree)
         dphi = None
@@ -461,3 +467,33 @@ class B200FmmSolver:
             gx, gy, gz = g[path]
             field.add_leaf(path, phi[path], gx, gy, gz, dphi[path] if dphi is not None else None)
         return field
+
+
+class GravityField:
+    """Per-leaf potential, acceleration and potential time derivative
+    (gravity/solver.py:33-47); what a gravity solver's ``solve`` returns."""
+
+    def __init__(self):
+        self.per_leaf = {}
+
+    def __getitem__(self, path):
+        return self.per_leaf[path]
+
+    def add_leaf(self, path, phi, gx, gy, gz, dphi_dt=None):
+        self.per_leaf[path] = {"phi": phi, "gx": gx, "gy": gy, "gz": gz,
+                               "dphi_dt": dphi_dt if dphi_dt is not None else np.zeros_like(phi)}
+
+
+def momentum_divergence_source(subgrid):
+    """rho_dot = -div(s) by second-order central differences over the filled
+    ghosts (gravity/solver.py:156-168), same numpy expression."""
+    g = GHOST
+    n = subgrid.n
+    u = subgrid.u
+    inv2dx = 1.0 / (2.0 * subgrid.dx)
+    sl = slice(g, g + n)
+    return -(
+        (u[SX, g + 1: g + n + 1, sl, sl] - u[SX, g - 1: g + n - 1, sl, sl])
+        + (u[SY, sl, g + 1: g + n + 1, sl] - u[SY, sl, g - 1: g + n - 1, sl])
+        + (u[SZ, sl, sl, g + 1: g + n + 1] - u[SZ, sl, sl, g - 1: g + n - 1])
+    ) * inv2dx

@@ -8,6 +8,7 @@ import sys
 import time
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "tests"))
 
 
 def main(level=3, reps=5):
@@ -15,7 +16,7 @@ def main(level=3, reps=5):
 
     from paper_2107_10987_b200.batch import LeafBatch
     from paper_2107_10987_b200.gravity import B200FmmSolver
-    from paper_2107_10987_b200.problems import synthetic_star
+    from octomini_host import synthetic_star
 
     tree, eos, _, om, fl = synthetic_star(level=level)
     s = B200FmmSolver(0.5)

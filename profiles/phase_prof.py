@@ -10,6 +10,7 @@ import os
 import sys
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "tests"))
 NAMES = ["prologue", "P0 convert + P5 of prev plane", "P1A lines 0,3-6 + KT", "P2A combine",
          "P1B lines 9-12 + KT", "P2B combine", "P3 in-plane mono + P6", "P4 in-plane KT", "last P5",
          "epilogue P6"]
@@ -18,8 +19,9 @@ NAMES = ["prologue", "P0 convert + P5 of prev plane", "P1A lines 0,3-6 + KT", "P
 def main(kind="sedov", level=4, steps=3):
     import torch
 
-    from paper_2107_10987_b200 import EosConfig, HydroMode, SedovConfig, build_uniform_tree, init_sedov
-    from paper_2107_10987_b200.problems import smooth_state
+    from octomini_host import SedovConfig, build_uniform_tree, init_sedov
+    from paper_2107_10987_b200 import EosConfig, HydroMode
+    from octomini_host import smooth_state
     from paper_2107_10987_b200.stepper import B200HydroStepper
 
     t = build_uniform_tree(level, 8, boundary="reflecting")

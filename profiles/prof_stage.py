@@ -7,13 +7,15 @@ import os
 import sys
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "tests"))
 
 
 def main(kind="sedov", level=3, steps=3):
     import torch
 
-    from paper_2107_10987_b200 import EosConfig, HydroMode, SedovConfig, build_uniform_tree, init_sedov
-    from paper_2107_10987_b200.problems import smooth_state
+    from octomini_host import SedovConfig, build_uniform_tree, init_sedov
+    from paper_2107_10987_b200 import EosConfig, HydroMode
+    from octomini_host import smooth_state
     from paper_2107_10987_b200.stepper import B200HydroStepper
 
     t = build_uniform_tree(level, 8, boundary="reflecting")

@@ -5,7 +5,9 @@ import os
 
 import numpy as np
 
-from paper_2107_10987_b200 import hydro, mesh, problems
+import octomini_host as mesh
+import octomini_host as problems
+from paper_2107_10987_b200 import hydro
 
 GOLD = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
 EOS = hydro.EosConfig(gamma=1.4)
@@ -25,7 +27,7 @@ def random_smooth(tree, seed=0, amp=0.2, eos=EOS):
         rho = 1.0 + amp * np.sin(np.pi * x) * np.cos(np.pi * y)
         p = 1.0 + amp * np.cos(np.pi * z)
         vx = amp * np.sin(np.pi * y)
-        sg.interior[:] = hydro.conserved_from_primitive(
+        sg.interior[:] = mesh.conserved_from_primitive(
             rho, (vx, 0.05 * np.ones_like(rho), -0.02 * np.ones_like(rho)), p, eos)
 
 

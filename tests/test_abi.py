@@ -60,7 +60,8 @@ def test_struct_layouts_match_header(tmp_path):
 
 
 def test_host_pack_roundtrip():
-    from paper_2107_10987_b200 import _lib, mesh
+    import octomini_host as mesh
+    from paper_2107_10987_b200 import _lib
     from paper_2107_10987_b200.batch import LeafBatch
 
     t = mesh.build_uniform_tree(2, 8, boundary="periodic")

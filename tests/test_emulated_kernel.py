@@ -49,7 +49,7 @@ def test_emulated_sources_and_floors():
 
 def test_emulated_gather_matches_ghost_golden():
     import ctypes
-    from paper_2107_10987_b200 import mesh
+    import octomini_host as mesh
     from paper_2107_10987_b200.batch import LeafBatch
 
     g = golden("ghosts")
@@ -85,7 +85,7 @@ def test_emulated_amr_ghost_regions():
     import ctypes
     import json
 
-    from paper_2107_10987_b200 import mesh
+    import octomini_host as mesh
     from paper_2107_10987_b200._abi import OmbAmrDesc
     from paper_2107_10987_b200.batch import LeafBatch
 

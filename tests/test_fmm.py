@@ -11,7 +11,8 @@ import numpy as np
 import pytest
 
 from _cases import golden
-from paper_2107_10987_b200 import gravity, mesh
+import octomini_host as mesh
+from paper_2107_10987_b200 import gravity
 
 
 def _fill(tree, g, name):
@@ -51,13 +52,17 @@ def test_interaction_groups_match_reference(name):
 
 
 def test_kernel_derivatives_formula():
-    """D(R) of g = -1/|R|: D0 = -1/r, D1 = R/r^3 (multipole.py:173-191)."""
-    R = np.array([0.3, -0.4, 1.2])
-    D = gravity.kernel_derivatives(R)
-    r = np.sqrt(R @ R)
-    assert D[0] == -1.0 / r
-    assert np.allclose(D[1:4], R / r ** 3, rtol=1e-15)
-    assert np.array_equal(gravity.flip_derivatives(D)[[0, 4, 5, 6, 7, 8, 9]], D[[0, 4, 5, 6, 7, 8, 9]])
+    """D(R) of g = -1/|R|: D0 = -1/r, D1 = R/r^3 (multipole.py:173-191); at -R the odd ranks flip."""
+    R = np.array([[0.3, -0.4, 1.2], [1.0, 2.0, -0.5]])
+    D = gravity.derivative_table(R)
+    for g in range(2):
+        r = np.sqrt(R[g] @ R[g])
+        assert D[g, 0, 0] == -1.0 / r
+        assert np.allclose(D[g, 0, 1:4], R[g] / r ** 3, rtol=1e-15)
+        assert np.array_equal(D[g, 1, 1:4], -D[g, 0, 1:4]) and np.array_equal(D[g, 1, 4:10], D[g, 0, 4:10])
+        assert np.array_equal(D[g, 1, 10:], -D[g, 0, 10:])
+    # trace-free rank 2 (the kernel is harmonic away from 0)
+    assert abs(D[0, 0, 4] + D[0, 0, 7] + D[0, 0, 9]) < 1e-14
 
 
 @pytest.mark.gpu

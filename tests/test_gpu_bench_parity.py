@@ -23,7 +23,8 @@ NTHR = os.cpu_count() or 1
 
 
 def _sedov(level):
-    from paper_2107_10987_b200 import EosConfig, SedovConfig, build_uniform_tree, init_sedov
+    from octomini_host import SedovConfig, build_uniform_tree, init_sedov
+    from paper_2107_10987_b200 import EosConfig
 
     t = build_uniform_tree(level, 8, boundary="reflecting")
     init_sedov(SedovConfig(), t, EosConfig(gamma=1.4))
@@ -74,7 +75,7 @@ def test_c2_one_step_vs_oracle():
 def test_c2_ten_steps_totals_vs_oracle():
     """c2 over 10 steps: every dt bitwise, the final state, and the conserved
     totals (problems/diagnostics.py:9-30) within 1e-12 of the oracle's."""
-    from paper_2107_10987_b200.problems import conservation_totals
+    from octomini_host import conservation_totals
 
     tg, tc = _sedov(4), _sedov(4)
     g = _gpu(tg, host_sync=False)
@@ -93,7 +94,7 @@ def test_c2_ten_steps_totals_vs_oracle():
 
 def test_c4_full_amr_one_step_vs_oracle():
     """c4: the full AMR Sedov tree (levels 3-6, 3,704 sub-grids)."""
-    from paper_2107_10987_b200.problems import amr_sedov_tree
+    from octomini_host import amr_sedov_tree
 
     t = amr_sedov_tree()
     assert len(t.leaves()) == 3704
@@ -114,7 +115,7 @@ def test_c4_full_amr_one_step_vs_oracle():
 def test_c4_run_lengths_bitwise():
     """The AMR run rule (leaves reading coarse/fine ghost regions join runs): the
     full c4 tree gives bitwise the same two steps with runs of 1 and of 4 leaves."""
-    from paper_2107_10987_b200.problems import amr_sedov_tree
+    from octomini_host import amr_sedov_tree
 
     out = []
     for mr in (1, 4):
@@ -129,7 +130,7 @@ def test_c4_run_lengths_bitwise():
 
 def test_c5_standin_level4_vs_oracle():
     """c5 stand-in at 128^3 (rotating frame, fixed gravity, floors, outflow): one step."""
-    from paper_2107_10987_b200.problems import synthetic_star
+    from octomini_host import synthetic_star
 
     tg, eos, grav, om, fl = synthetic_star(level=4)
     tc, _, gravc, _, _ = synthetic_star(level=4)

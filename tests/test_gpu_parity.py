@@ -134,7 +134,7 @@ def test_old_scheme_two_steps():
 
 
 def test_sedov_c1_ten_steps_totals():
-    from paper_2107_10987_b200.problems import conservation_totals
+    from octomini_host import conservation_totals
 
     t, g = case_tree("sedov_c1")
     st = _stepper(t)
@@ -166,7 +166,8 @@ def test_gather_matches_ghost_golden():
 
     import torch
 
-    from paper_2107_10987_b200 import _lib, mesh
+    import octomini_host as mesh
+    from paper_2107_10987_b200 import _lib
     from paper_2107_10987_b200.batch import LeafBatch
 
     g = golden("ghosts")
@@ -244,7 +245,7 @@ def test_synthetic_star_matches_oracle():
     """Config c5 stand-in (rotating frame + fixed gravity + floors, outflow): GPU vs the CPU oracle, 2 steps."""
     from oracle.step import OracleStepper
     from paper_2107_10987_b200 import HydroMode
-    from paper_2107_10987_b200.problems import synthetic_star
+    from octomini_host import synthetic_star
     from paper_2107_10987_b200.stepper import B200HydroStepper
 
     tg, eos, grav, om, fl = synthetic_star(level=2)
@@ -389,7 +390,8 @@ def test_gather_matches_amr_ghost_golden():
 
     import torch
 
-    from paper_2107_10987_b200 import _lib, mesh
+    import octomini_host as mesh
+    from paper_2107_10987_b200 import _lib
     from paper_2107_10987_b200._abi import OmbAmrDesc
     from paper_2107_10987_b200.batch import LeafBatch
 

@@ -8,7 +8,7 @@ from _cases import GOLD, bitwise_mismatch, case_tree, golden, state_of
 
 
 def test_read_reference_checkpoint():
-    from paper_2107_10987_b200.io import read_checkpoint
+    from octomini_host.checkpoint import read_checkpoint
 
     t, hdr = read_checkpoint(os.path.join(GOLD, "amr_reflux_init.omck"))
     assert hdr["time"] == 0.25 and hdr["step"] == 7 and hdr["extra"] == {"gamma": 1.4}
@@ -17,7 +17,8 @@ def test_read_reference_checkpoint():
 
 
 def test_corrupt_checkpoint_rejected(tmp_path):
-    from paper_2107_10987_b200.io import CheckpointError, read_checkpoint
+    from octomini_host.checkpoint import read_checkpoint
+    from paper_2107_10987_b200.io import CheckpointError
 
     raw = open(os.path.join(GOLD, "amr_reflux_init.omck"), "rb").read()
     p = tmp_path / "bad.omck"
@@ -46,7 +47,7 @@ def test_device_checkpoint_bytes_match_reference(tmp_path):
 def test_device_totals_match_conservation_totals():
     from paper_2107_10987_b200 import EosConfig, HydroMode
     from paper_2107_10987_b200.io import device_totals
-    from paper_2107_10987_b200.problems import conservation_totals
+    from octomini_host import conservation_totals
     from paper_2107_10987_b200.stepper import B200HydroStepper
 
     t, g = case_tree("sedov_c1")

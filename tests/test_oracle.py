@@ -12,7 +12,7 @@ import pytest
 import oracle
 from oracle.ghosts import exchange
 from oracle.step import OracleStepper
-from paper_2107_10987_b200 import mesh
+import octomini_host as mesh
 
 from _cases import bitwise_mismatch, case_tree, golden, sources_gravity, state_of
 

@@ -8,7 +8,7 @@ import socket
 import numpy as np
 import pytest
 
-from paper_2107_10987_b200 import mesh
+import octomini_host as mesh
 from paper_2107_10987_b200.batch import OFFS, neighbor_table
 from paper_2107_10987_b200.partition import Partition
 
