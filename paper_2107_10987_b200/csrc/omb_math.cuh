@@ -76,12 +76,24 @@ OMB_HD double div_fast(double a, double b, double y, unsigned& rare) {
 // single quotient by a divisor in [2^-100, 2^100] (caller's guarantee: the
 // EOS's gamma-1 -- checked on the host -- and the Simpson weight 36), with
 // its own rarely taken IEEE fallback
+// A zero numerator returns q0 = a*y (the signed zero) before the range test:
+// zero Simpson deviations are everywhere in the Sedov ambient, and the IEEE
+// division of the rare branch must not be reached (or speculated) for them --
+// CUDA routes 0/b through its out-of-line division subroutine (ncu: 1.4 M
+// warp-level calls per c2 launch, 5 % of k_stage's instructions, before this).
 OMB_HD double div_by(double a, double b, double y) {
   double q0 = a * y;
+  if (a == 0.0) return q0;
   double q1 = fma(fma(-b, q0, a), y, q0);
   double q2 = fma(fma(-b, q1, a), y, q1);
   double m = fabs(q1);
-  if (!(m > 0x1p-860 && m < 0x1p+1000)) q2 = (a == 0.0) ? q0 : a / b;
+  if (!(m > 0x1p-860 && m < 0x1p+1000)) {
+    double aa = a;
+#ifdef __CUDA_ARCH__
+    asm volatile("" : "+d"(aa));  // keep the IEEE division inside this rare branch
+#endif
+    q2 = aa / b;
+  }
   return q2;
 }
 

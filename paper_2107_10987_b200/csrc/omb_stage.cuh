@@ -66,6 +66,12 @@ OMB_HD int pos10(int y, int z) { return (y - 2) * 10 + (z - 2); }
 // last, so whole warps take the 2-field path.  shape: 0 = [3,10]^2 (line 0),
 // 1 = y in [2,11] x z in [3,10] (lines 1,3,4), 2 = y in [3,10] x z in [2,11]
 // (lines 2,5,6), 3 = all (diagonals 7..12).
+// Within that, the order is a table (omb_order.cuh, gen_position_order.py)
+// chosen so each half-warp's 8-byte shared-memory accesses -- through the
+// prim ring (row pitch 14) and the lo/hi / point-flux slots (pitch 10) -- hit
+// distinct banks, for the alignment a = 100k mod 16 at which the k-th line of
+// a phase starts (ncu: the row-major order cost 76 M excess wavefronts per c2
+// launch in the stencil loads alone).
 OMB_HD int line_shape(int l) {
   if (l == 0) return 0;
   if (l == 1 || l == 3 || l == 4) return 1;
@@ -73,27 +79,23 @@ OMB_HD int line_shape(int l) {
   return 3;
 }
 OMB_HD int shape_needed(int sh) { return sh == 0 ? 64 : (sh == 3 ? 100 : 80); }
-OMB_HD void shape_pos(int sh, int i, int& y, int& z) {
-  if (sh == 3) { y = 2 + i / 10; z = 2 + i % 10; return; }
-  if (sh == 0) {
-    if (i < 64) { y = 3 + i / 8; z = 3 + i % 8; return; }
-    int j = i - 64;
-    if (j < 10) { y = 2; z = 2 + j; return; }
-    if (j < 20) { y = 11; z = 2 + j - 10; return; }
-    int k = j - 20;
-    y = 3 + k / 2; z = (k & 1) ? 11 : 2;
-    return;
-  }
-  if (sh == 1) {
-    if (i < 80) { y = 2 + i / 8; z = 3 + i % 8; return; }
-    int j = i - 80;
-    y = 2 + j / 2; z = (j & 1) ? 11 : 2;
-    return;
-  }
-  if (i < 80) { y = 3 + i / 10; z = 2 + i % 10; return; }
-  int j = i - 80;
-  if (j < 10) { y = 2; z = 2 + j; return; }
-  y = 11; z = 2 + j - 10;
+}  // namespace omb
+#include "omb_order.cuh"
+namespace omb {
+#ifdef __CUDACC__
+static __device__ const unsigned char d_pos_order[11][100] = OMB_ORDER_TABLE;
+#endif
+static const unsigned char h_pos_order[11][100] = OMB_ORDER_TABLE;
+// i-th position of the line that is the k-th (k = 0..4) of its phase
+OMB_HD void shape_pos(int sh, int k, int i, int& y, int& z) {
+  int row = order_row(sh, (4 * k) & 15);
+#ifdef __CUDA_ARCH__
+  int p = __ldg(&d_pos_order[row][i]);
+#else
+  int p = h_pos_order[row][i];
+#endif
+  y = 2 + p / 10;
+  z = 2 + p % 10;
 }
 OMB_HD int yslot(int y, int z) { return (y - 2) * 8 + (z - 3); }
 OMB_HD int zslot(int y, int z) { return (y - 3) * 9 + (z - 2); }
@@ -470,7 +472,7 @@ struct Stage {
       int dl = dl0 + it / NP, i = it % NP;
       int l = dl_line(dl);
       int sh = line_shape(l), y, z;
-      shape_pos(sh, i, y, z);
+      shape_pos(sh, dl - dl0, i, y, z);
       int pos = pos10(y, z);
       double lo[NF], hi[NF];
       mono6(l, X, y, z, lo, hi, i < shape_needed(sh));
@@ -588,7 +590,7 @@ struct Stage {
     for (int it = tid; it < nip * NP; it += nthr) {
       int ip = it / NP, i = it % NP, l = ip_line(ip);
       int sh = line_shape(l), y, z;
-      shape_pos(sh, i, y, z);
+      shape_pos(sh, ip, i, y, z);
       int pos = pos10(y, z);
       double lo[NF], hi[NF];
       mono6(l, X, y, z, lo, hi, i < shape_needed(sh));
