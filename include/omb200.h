@@ -23,7 +23,7 @@
 extern "C" {
 #endif
 
-#define OMB_ABI_VERSION 5
+#define OMB_ABI_VERSION 6
 
 /* per-leaf topology / geometry record (device array, one per leaf) */
 typedef struct {
@@ -63,6 +63,13 @@ typedef struct {
      * stage-input buffer (CUDA IPC peer memory, same fstride on every rank); NULL: halo slots local */
     const double *const *halo;
     int nown;
+    /* passive-scalar pass (species; SURVEY.md 0.2 -- a scalar follows tau's path: PPM, KT flux,
+     * Simpson faces, RK update, no sources / dual energy / floors): scalar != 0 runs the stage on
+     * ucur = (rho, sx, sy, sz, p, X) built by omb_scalar_input, reads X's step-start state from
+     * s_u0 and writes only X's stage output to s_next ([fstride] each); unext is not written */
+    int scalar;
+    const double *s_u0;
+    double *s_next;
 } OmbStageDesc;
 
 /* AMR ghost regions: each task fills, in the interior of a VIRTUAL leaf (batch index >= number of real
@@ -139,6 +146,12 @@ int omb_kt_flux(const double *left, const double *right, int n, int axis, double
 /* omb_physical_flux <- flux.physical_flux(state, axis) (flux.py:40-47) for n states [n][7] */
 int omb_physical_flux(const double *states, int n, int axis, double *out, void *stream);
 int omb_face_flux(const double *pts, int n, int new_mode, double *out, void *stream);
+/* passive scalars: the input of a scalar pass, dst [6][fstride] = (rho, sx, sy, sz, p, X) from the stage
+ * input u (p as the stage's primitive conversion computes it, reference.py:30-45).  Leaves [0, n_all) get
+ * fields 0-4 (n_all counts the AMR virtual leaves, filled by omb_amr_ghosts before); leaves [0, n_x) get
+ * X from x (skip with x = NULL; run omb_amr_ghosts on dst, then this again with x = NULL, for AMR) */
+int omb_scalar_input(const double *u, long long fstride, int n_all, const double *x, int n_x, double gamma,
+                     double gm1, double eta, double *dst, void *stream);
 /* self-check of the device pow (csrc/omb_pow.cuh, glibc's algorithm and tables): out[i] = pow(x[i], y[i]),
  * to be compared bitwise with the host libm's pow -- the reference's tau goes through glibc pow
  * (reference.py:39, hydro/eos.py:50-61) */

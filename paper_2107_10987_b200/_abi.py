@@ -32,6 +32,7 @@ class OmbStageDesc(ctypes.Structure):
         ("bc", ctypes.c_int), ("new_mode", ctypes.c_int), ("override_center", ctypes.c_int),
         ("contact", ctypes.c_int), ("amax_bits", ctypes.c_void_p), ("fallback", ctypes.c_void_p),
         ("flux", ctypes.c_void_p), ("halo", ctypes.c_void_p), ("nown", ctypes.c_int),
+        ("scalar", ctypes.c_int), ("s_u0", ctypes.c_void_p), ("s_next", ctypes.c_void_p),
     ]
 
 

@@ -12,11 +12,11 @@ from .errors import NativeError
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 SO_PATH = os.environ.get("OMB_LIB_PATH") or os.path.join(_HERE, "libomb200.so")  # override: A/B experiments
-ABI_VERSION = 5
+ABI_VERSION = 6
 _lib = None
 
 EXPORTS = ("omb_abi_version", "omb_last_error", "omb_stage_smem_bytes", "omb_primitives", "omb_reconstruct",
-           "omb_fluxes", "omb_stage", "omb_cfl", "omb_gather", "omb_gather_leaves", "omb_fp64_peak", "omb_pack_leaves", "omb_unpack_leaves", "omb_selftest_div", "omb_selftest_pow", "omb_kt_flux", "omb_physical_flux", "omb_face_flux", "omb_host_pack", "omb_host_unpack", "omb_host_upload", "omb_host_download", "omb_host_download_after", "omb_host_gather", "omb_host_scatter", "omb_set_host_threads", "omb_amr_ghosts",
+           "omb_fluxes", "omb_stage", "omb_cfl", "omb_gather", "omb_gather_leaves", "omb_fp64_peak", "omb_pack_leaves", "omb_unpack_leaves", "omb_selftest_div", "omb_selftest_pow", "omb_kt_flux", "omb_physical_flux", "omb_face_flux", "omb_scalar_input", "omb_host_pack", "omb_host_unpack", "omb_host_upload", "omb_host_download", "omb_host_download_after", "omb_host_gather", "omb_host_scatter", "omb_set_host_threads", "omb_amr_ghosts",
            "omb_reflux_update", "omb_leaf_sums", "omb_disk_order",
            "omb_gather_rows", "omb_scatter_rows", "omb_enable_peer_access", "omb_ipc_alloc", "omb_ipc_open",
            "omb_fmm_traverse", "omb_fmm_build", "omb_fmm_build_direct", "omb_fmm_direct", "omb_fmm_masses", "omb_fmm_upward", "omb_fmm_m2l", "omb_fmm_m2l_part", "omb_fmm_downward",
@@ -49,6 +49,7 @@ def load():
     L.omb_kt_flux.argtypes = [vp, vp, i, i, d, vp, vp, vp]
     L.omb_face_flux.argtypes = [vp, i, i, vp, vp]
     L.omb_physical_flux.argtypes = [vp, i, i, vp, vp]
+    L.omb_scalar_input.argtypes = [vp, ll, i, vp, i, d, d, d, vp, vp]
     L.omb_host_pack.argtypes = [vp, i, i, ll, vp]
     L.omb_host_unpack.argtypes = [vp, i, i, ll, vp]
     L.omb_host_upload.argtypes = [vp, i, i, ll, vp, vp, i, vp]

@@ -267,7 +267,9 @@ __device__ unsigned long long g_phase_cycles[16];
   } while (0)
 #endif
 
-template <int NT>
+// SC: the passive-scalar pass (a separate instantiation, so the hydro stage
+// carries none of its branches: A.scalar is a compile-time constant below)
+template <int NT, int SC>
 __global__ void __launch_bounds__(NT, 1) k_stage(StageArgs A) {
   static_assert(NT >= 2 * NFACEX, "P6 runs on the last 64 threads of the last P1 group");
   extern __shared__ double S[];
@@ -275,6 +277,7 @@ __global__ void __launch_bounds__(NT, 1) k_stage(StageArgs A) {
   Stage st;
   st.S = S;
   st.A = A;
+  st.A.scalar = SC;
   st.run = blockIdx.x;
   int off = A.run_off[blockIdx.x];
   st.R = A.run_off[blockIdx.x + 1] - off;
@@ -627,6 +630,22 @@ __global__ void k_face_points(const double* __restrict__ pts, int n, int new_mod
   out[i] = c + (4.0 * edev + vdev) / 36.0;
 }
 
+// passive-scalar pass input: (rho, sx, sy, sz, p, X) per cell
+__global__ void k_scalar_input(const double* __restrict__ U, long long fstride, int n_all, const double* __restrict__ x,
+                               int n_x, double gamma, double gm1, double eta, double* __restrict__ dst) {
+  long long n = (long long)n_all * 512;
+  for (long long c = blockIdx.x * (long long)blockDim.x + threadIdx.x; c < n; c += (long long)gridDim.x * blockDim.x) {
+    double u[NF], w[NF];
+#pragma unroll
+    for (int v = 0; v < NF; v++) u[v] = U[v * fstride + c];
+    prim_cell(u, gamma, gm1, eta, w);
+#pragma unroll
+    for (int v = 0; v < 4; v++) dst[v * fstride + c] = u[v];
+    dst[4 * fstride + c] = w[4];
+    if (x != nullptr && c < (long long)n_x * 512) dst[5 * fstride + c] = x[c];
+  }
+}
+
 // pow_glibc element-wise (the self-check of omb_pow.cuh against the host's libm)
 __global__ void k_pow_batch(const double* __restrict__ x, const double* __restrict__ y, long long n,
                             double* __restrict__ out) {
@@ -720,8 +739,10 @@ static int lib_init() {
   build_face_tables(ft);
   CK(cudaMemcpyToSymbol(c_ft, ft, sizeof(ft)), "face table upload");
   // 512 threads x 128 registers fills the register file; 256/384/576/640 were measured slower
-  CK(cudaFuncSetAttribute(k_stage<STAGE_THREADS>, cudaFuncAttributeMaxDynamicSharedMemorySize, Smem::BYTES),
+  CK(cudaFuncSetAttribute(k_stage<STAGE_THREADS, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, Smem::BYTES),
      "stage smem attribute");
+  CK(cudaFuncSetAttribute(k_stage<STAGE_THREADS, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, Smem::BYTES),
+     "scalar stage smem attribute");
   CK(cudaFuncSetAttribute(k_reflux_update, cudaFuncAttributeMaxDynamicSharedMemorySize, FLUX_SLOT * 8),
      "reflux smem attribute");
   g_init_devs.fetch_or(bit, std::memory_order_release);
@@ -841,6 +862,9 @@ static StageArgs stage_args(const OmbStageDesc* d) {
   A.flux = d->flux;
   A.halo = d->halo;
   A.nown = d->nown;
+  A.scalar = d->scalar;
+  A.s_u0 = d->s_u0;
+  A.s_next = d->s_next;
   return A;
 }
 
@@ -867,7 +891,10 @@ int omb_stage(const OmbStageDesc* d, void* stream) {
   if (!div_range_ok(d->gm1)) return set_err("omb_stage: gamma - 1 outside [2^-100, 2^100]");
   StageArgs A = stage_args(d);
   if (d->nruns <= 0) return 0;
-  k_stage<STAGE_THREADS><<<d->nruns, STAGE_THREADS, Smem::BYTES, (cudaStream_t)stream>>>(A);
+  if (d->scalar)
+    k_stage<STAGE_THREADS, 1><<<d->nruns, STAGE_THREADS, Smem::BYTES, (cudaStream_t)stream>>>(A);
+  else
+    k_stage<STAGE_THREADS, 0><<<d->nruns, STAGE_THREADS, Smem::BYTES, (cudaStream_t)stream>>>(A);
   CK(cudaGetLastError(), "omb_stage launch");
   return 0;
 }
@@ -963,6 +990,17 @@ int omb_face_flux(const double* pts, int n, int new_mode, double* out, void* str
   if (n <= 0) return 0;
   k_face_points<<<(n * NF + 127) / 128, 128, 0, (cudaStream_t)stream>>>(pts, n, new_mode, out);
   CK(cudaGetLastError(), "omb_face_flux launch");
+  return 0;
+}
+
+int omb_scalar_input(const double* u, long long fstride, int n_all, const double* x, int n_x, double gamma,
+                     double gm1, double eta, double* dst, void* stream) {
+  if (n_all <= 0) return 0;
+  long long n = (long long)n_all * 512;
+  int blocks = (int)((n + 255) / 256);
+  k_scalar_input<<<blocks < 148 * 16 ? blocks : 148 * 16, 256, 0, (cudaStream_t)stream>>>(u, fstride, n_all, x, n_x,
+                                                                                           gamma, gm1, eta, dst);
+  CK(cudaGetLastError(), "omb_scalar_input launch");
   return 0;
 }
 

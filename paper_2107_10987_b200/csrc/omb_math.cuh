@@ -286,6 +286,18 @@ OMB_HD void prim_cell(const double* u, double gamma, double gm1, double eta, dou
   w[5] = u[5];
 }
 
+// passive-scalar pass (omb_scalar_input built u = (rho, sx, sy, sz, p, X)): the
+// velocities exactly as prim_cell forms them, the pressure and the scalar as given
+OMB_HD void prim_cell_scalar(const double* u, double* w) {
+  double inv = 1.0 / u[0];
+  w[0] = u[0];
+  w[1] = u[1] * inv;
+  w[2] = u[2] * inv;
+  w[3] = u[3] * inv;
+  w[4] = u[4];
+  w[5] = u[5];
+}
+
 // ---------------------------------------------------------------------------
 // CFL wave speed of one cell (step.py:86-88 via eos.py:28-44); NaN-propagating
 // ---------------------------------------------------------------------------

@@ -225,6 +225,9 @@ struct StageArgs {
   double* flux;                   // face-flux export slots (AMR), or null
   const double* const* halo;      // multi-GPU: halo slot k's block in its owner's buffer, or null
   int nown;                       // first halo slot
+  int scalar;                     // passive-scalar pass: ucur = (rho, s, p, X); X alone is updated
+  const double* s_u0;             // scalar pass: X at the step start
+  double* s_next;                 // scalar pass: X's stage output
 };
 
 // conserved state of padded cell c (local coords in [0,14)^3) of a leaf, as
@@ -337,7 +340,8 @@ struct Stage {
     for (int it = tid; it < PL; it += nthr) {
       double u[NF], w[NF];
       gather_cell(A.ucur, A.fstride, LI, A.bc, lx, it / M, it % M, u);
-      prim_cell(u, A.gamma, A.gm1, A.eta, w);
+      if (A.scalar) prim_cell_scalar(u, w);
+      else prim_cell(u, A.gamma, A.gm1, A.eta, w);
 #pragma unroll
       for (int v = 0; v < NF; v++) prp(X, v)[it] = w[v];
     }
@@ -376,7 +380,8 @@ struct Stage {
 #pragma unroll
       for (int a = 0; a < 3; a++)
         if ((fm >> a) & 1) u[1 + a] = -u[1 + a];
-      prim_cell(u, A.gamma, A.gm1, A.eta, w);
+      if (A.scalar) prim_cell_scalar(u, w);
+      else prim_cell(u, A.gamma, A.gm1, A.eta, w);
 #pragma unroll
       for (int v = 0; v < NF; v++) prp(Xn, v)[it] = w[v];
     }
@@ -392,7 +397,8 @@ struct Stage {
 #pragma unroll
       for (int v = 0; v < NF; v++) {
         async_copy8(S + Smem::SG6 + v * NFACEX + it, A.ucur + v * A.fstride + cell);
-        async_copy8(S + Smem::SG6 + (NF + v) * NFACEX + it, A.u0 + v * A.fstride + cell);
+        const double* u0 = (A.scalar && v == NF - 1) ? A.s_u0 + cell : A.u0 + v * A.fstride + cell;
+        async_copy8(S + Smem::SG6 + (NF + v) * NFACEX + it, u0);
       }
       if (grav)
 #pragma unroll
@@ -756,6 +762,10 @@ struct Stage {
       double nw[NF], out[NF];
 #pragma unroll
       for (int v = 0; v < NF; v++) nw[v] = S[Smem::SG6 + v * NFACEX + it];
+      if (A.scalar) {  // the passive scalar: no dual energy, no floors
+        A.s_next[cell] = nw[NF - 1];
+        continue;
+      }
       update_cell_fin(P, nw, out);
 #pragma unroll
       for (int v = 0; v < NF; v++) A.unext[v * A.fstride + cell] = out[v];
@@ -798,6 +808,11 @@ struct Stage {
         for (int k = 0; k < 4; k++) g[k] = S[Smem::SG6 + (2 * NF + k) * NFACEX + it];
       double xc = LI.ox + LI.dx * (double)lx;
       double yc = LI.oy + LI.dx * (double)(y - 3);
+      if (A.scalar) {
+        update_cell_rk(P, u, u0, rr, xc, yc, g, out);
+        A.s_next[cell] = out[NF - 1];
+        continue;
+      }
       update_cell(P, u, u0, rr, xc, yc, g, out);
 #pragma unroll
       for (int v = 0; v < NF; v++) A.unext[v * A.fstride + cell] = out[v];
@@ -906,7 +921,7 @@ OMB_HD void update_leaf(const StageArgs& A, int leaf, const double* F, int tid, 
 #pragma unroll
     for (int v = 0; v < NF; v++) {
       u[v] = A.ucur[v * A.fstride + cell];
-      u0[v] = A.u0[v * A.fstride + cell];
+      u0[v] = (A.scalar && v == NF - 1) ? A.s_u0[cell] : A.u0[v * A.fstride + cell];
       double dfx = F[flux_index(0, v, x + 1, y, z)] - F[flux_index(0, v, x, y, z)];
       double dfy = F[flux_index(1, v, y + 1, x, z)] - F[flux_index(1, v, y, x, z)];
       double dfz = F[flux_index(2, v, z + 1, x, y)] - F[flux_index(2, v, z, x, y)];
@@ -920,6 +935,11 @@ OMB_HD void update_leaf(const StageArgs& A, int leaf, const double* F, int tid, 
       for (int q = 0; q < 4; q++) g[q] = A.grav[q * A.fstride + cell];
     double xc = LI.ox + LI.dx * (double)x;
     double yc = LI.oy + LI.dx * (double)y;
+    if (A.scalar) {
+      update_cell_rk(P, u, u0, rr, xc, yc, g, out);
+      A.s_next[cell] = out[NF - 1];
+      continue;
+    }
     update_cell(P, u, u0, rr, xc, yc, g, out);
 #pragma unroll
     for (int v = 0; v < NF; v++) A.unext[v * A.fstride + cell] = out[v];

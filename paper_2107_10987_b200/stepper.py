@@ -60,7 +60,9 @@ def _on_device(fn):
 class B200HydroStepper:
     def __init__(self, tree, eos, mode, executor=None, gravity=None, omega=0.0, floors=None, abort_courant=1.0,
                  buffers=None, profiler=None, lane_pool=None, *, host_sync=True, max_run=4, device=None,
-                 leaves=None, partition=None, group=None):
+                 leaves=None, partition=None, group=None, scalars=0):
+        if scalars and partition is not None:
+            raise NotImplementedError("passive scalars on a partitioned tree")
         dev = require_cuda(device)
         if dev.index is None:
             dev = torch.device("cuda", torch.cuda.current_device())
@@ -68,6 +70,7 @@ class B200HydroStepper:
         with torch.cuda.device(dev):  # allocations, library setup and streams on `device`
             self._setup(tree, eos, mode, executor, gravity, omega, floors, abort_courant, buffers, profiler,
                         lane_pool, host_sync, max_run, leaves, partition, group)
+            self._setup_scalars(int(scalars))
 
     def _setup(self, tree, eos, mode, executor, gravity, omega, floors, abort_courant, buffers, profiler, lane_pool,
                host_sync, max_run, leaves, partition, group):
@@ -213,6 +216,73 @@ class B200HydroStepper:
                 self._frecvbuf = T.empty(max(1, sum(partition.flux_recv_counts)) * FLUX_SLOT_DOUBLES,
                                          dtype=T.float64, device=dev)
         self.upload()
+
+    # -- passive scalars (species) ------------------------------------------------------
+    def _setup_scalars(self, ns):
+        """``scalars=NS`` passive scalars X_k (species densities; north_star / SURVEY.md §0.2):
+        each follows tau's path -- PPM reconstruction, the KT flux with the hydro state's
+        signal speeds, the Simpson faces, reflux, the RK update -- with no source, dual-energy
+        resync or floor.  One extra pass of the fused stage kernel per scalar and stage
+        (k_stage<.., 1>, on (rho, s, p, X) from omb_scalar_input).  The reference has no
+        species, so the check is structural: X = rho evolves bitwise like rho
+        (tests/test_gpu_scalars.py).  Device-resident: set_scalars / get_scalars."""
+        self.nscalars = ns
+        if ns == 0:
+            return
+        b = self.batch
+        self._sbuf = [[torch.zeros(b.fstride, dtype=torch.float64, device=self.dev) for _ in range(4)]
+                      for _ in range(ns)]
+        self._sin = torch.empty(6 * b.fstride, dtype=torch.float64, device=self.dev)
+        self._sacc = torch.zeros(2, dtype=torch.int64, device=self.dev)  # the scalar passes' amax / fallback: unused
+
+    @_on_device
+    def set_scalars(self, values):
+        """values: (NS, L, n, n, n) in sorted_leaves() order, or {leaf.path: (NS, n, n, n)}."""
+        b = self.batch
+        if isinstance(values, dict):
+            values = np.stack([np.asarray(values[lf.path]) for lf in b.leaves[:b.L]], axis=1)
+        values = np.ascontiguousarray(values, dtype=np.float64)
+        if values.shape != (self.nscalars, b.L, 8, 8, 8):
+            raise ValueError(f"scalars must have shape {(self.nscalars, b.L, 8, 8, 8)}")
+        for k in range(self.nscalars):
+            self._sbuf[k][self._state][:b.L * 512].copy_(torch.from_numpy(values[k].reshape(-1)))
+
+    @_on_device
+    def get_scalars(self):
+        b = self.batch
+        return np.stack([self._sbuf[k][self._state][:b.L * 512].cpu().numpy().reshape(b.L, 8, 8, 8)
+                         for k in range(self.nscalars)])
+
+    def _scalar_passes(self, d, cur, nxt, stream=None):
+        """After the hydro stage described by ``d`` (input buffer index cur): every scalar's
+        stage cur -> nxt, with the same stage weights, dt and signal speeds."""
+        b = self.batch
+        sh = stream_handle(stream)
+        g = self.eos.gamma
+        n_all = b.L + b.nvirtual
+        for k in range(self.nscalars):
+            X = self._sbuf[k]
+            _lib.check(self.lib.omb_scalar_input(ptr(self._buf[cur]), b.fstride, n_all, ptr(X[cur]), b.L, g, g - 1.0,
+                                                 self.eos.dual_energy_eta, ptr(self._sin), sh), "omb_scalar_input")
+            if self._amr_tasks is not None:  # X's coarse/fine ghost regions; fields 0-4 redone from the state's
+                ad = OmbAmrDesc(u=ptr(self._sin), fstride=b.fstride, tasks=ptr(self._amr_tasks), ntasks=b.nvirtual)
+                _lib.check(self.lib.omb_amr_ghosts(ctypes.byref(ad), sh), "omb_amr_ghosts")
+                _lib.check(self.lib.omb_scalar_input(ptr(self._buf[cur]), b.fstride, n_all, None, 0, g, g - 1.0,
+                                                     self.eos.dual_energy_eta, ptr(self._sin), sh), "omb_scalar_input")
+            ds = OmbStageDesc.from_buffer_copy(d)
+            ds.run_off, ds.run_leaf, ds.nruns = ptr(self._run_off), ptr(self._run_leaf), b.nruns  # (not a tail part)
+            ds.ucur = ptr(self._sin)
+            ds.scalar = 1
+            ds.s_u0 = ptr(X[self._state])
+            ds.s_next = ptr(X[nxt])
+            ds.amax_bits = self._sacc.data_ptr()
+            ds.fallback = self._sacc.data_ptr() + 8
+            ds.halo = None
+            _lib.check(self.lib.omb_stage(ctypes.byref(ds), sh), "omb_stage (scalar)")
+            if self._rleaf is not None:
+                rd = OmbRefluxDesc(stage=ds, leaf=ptr(self._rleaf), off=ptr(self._roff), tasks=ptr(self._rtasks),
+                                   nleaves=len(b.reflux_leaf))
+                _lib.check(self.lib.omb_reflux_update(ctypes.byref(rd), sh), "omb_reflux_update (scalar)")
 
     # -- host <-> device -------------------------------------------------------------
     TRANSFER_CHUNKS = 8
@@ -521,6 +591,8 @@ class B200HydroStepper:
                 rd = OmbRefluxDesc(stage=d, leaf=ptr(self._rleaf), off=ptr(self._roff), tasks=ptr(self._rtasks),
                                    nleaves=len(self.batch.reflux_leaf))
                 _lib.check(self.lib.omb_reflux_update(ctypes.byref(rd), sh), "omb_reflux_update")
+            if self.nscalars:
+                self._scalar_passes(d, cur, nxt, stream)
             outs.append(nxt)
             cur = nxt
         start = self._state

@@ -38,7 +38,7 @@ def sass_lines(so, func):
 
 def main(rep, so="paper_2107_10987_b200/libomb200.so", top=40):
     so = os.path.abspath(so)
-    func = "_Z7k_stageILi512EEvN3omb9StageArgsE"
+    func = "_Z7k_stageILi512ELi0EEvN3omb9StageArgsE"
     raw = subprocess.run(["ncu", "-i", os.path.abspath(rep), "--page", "source", "--csv", "--print-source=sass"],
                          capture_output=True, text=True, cwd="/tmp").stdout
     rows = list(csv.reader(io.StringIO(raw)))
@@ -80,7 +80,7 @@ if __name__ == "__main__":
 def opcode_lines(rep, so, opcode, top=25):
     """Source lines executing the most instructions of one opcode (prefix match)."""
     so = os.path.abspath(so)
-    func = "_Z7k_stageILi512EEvN3omb9StageArgsE"
+    func = "_Z7k_stageILi512ELi0EEvN3omb9StageArgsE"
     raw = subprocess.run(["ncu", "-i", os.path.abspath(rep), "--page", "source", "--csv", "--print-source=sass"],
                          capture_output=True, text=True, cwd="/tmp").stdout
     rows = list(csv.reader(io.StringIO(raw)))
@@ -107,7 +107,7 @@ def stall_lines(rep, so, reasons=("stall_barrier", "stall_wait", "stall_short_sb
                                   "stall_no_inst", "stall_math"), top=12):
     """Per stall reason: the source lines holding most of its samples."""
     so = os.path.abspath(so)
-    func = "_Z7k_stageILi512EEvN3omb9StageArgsE"
+    func = "_Z7k_stageILi512ELi0EEvN3omb9StageArgsE"
     raw = subprocess.run(["ncu", "-i", os.path.abspath(rep), "--page", "source", "--csv", "--print-source=sass"],
                          capture_output=True, text=True, cwd="/tmp").stdout
     rows = list(csv.reader(io.StringIO(raw)))
@@ -131,7 +131,7 @@ def stall_lines(rep, so, reasons=("stall_barrier", "stall_wait", "stall_short_sb
 def calls(rep, so):
     """Executed CALL instructions (out-of-line subroutines: IEEE division/sqrt slow paths) per source line."""
     so = os.path.abspath(so)
-    func = "_Z7k_stageILi512EEvN3omb9StageArgsE"
+    func = "_Z7k_stageILi512ELi0EEvN3omb9StageArgsE"
     raw = subprocess.run(["ncu", "-i", os.path.abspath(rep), "--page", "source", "--csv", "--print-source=sass"],
                          capture_output=True, text=True, cwd="/tmp").stdout
     rows = list(csv.reader(io.StringIO(raw)))

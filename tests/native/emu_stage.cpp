@@ -52,6 +52,7 @@ extern "C" int emu_stage(const OmbStageDesc* d, int nthr) {
   A.omega = d->omega; A.floor_rho = d->floor_rho; A.floor_tau = d->floor_tau; A.floor_vmax = d->floor_vmax;
   A.bc = d->bc; A.new_mode = d->new_mode; A.quad = d->new_mode && !d->override_center; A.contact = d->contact;
   A.amax_bits = d->amax_bits; A.fallback = d->fallback; A.flux = d->flux; A.halo = d->halo; A.nown = d->nown;
+  A.scalar = d->scalar; A.s_u0 = d->s_u0; A.s_next = d->s_next;
   std::vector<double> S(Smem::TOTAL);
   std::vector<int> order(nthr);
   for (int k = 0; k < nthr; k++) order[k] = g_order == 0 ? k : (g_order == 1 ? nthr - 1 - k : (int)((97LL * k) % nthr));
@@ -150,6 +151,7 @@ extern "C" int emu_reflux_update(const OmbRefluxDesc* r) {
   A.info = (const LeafInfo*)d->info; A.dt = d->dt; A.a = d->a; A.b = d->b; A.gamma = d->gamma; A.gm1 = d->gm1;
   A.inv_gm1 = 1.0 / d->gm1; A.eta = d->eta; A.inv_gamma = d->inv_gamma; A.omega = d->omega;
   A.floor_rho = d->floor_rho; A.floor_tau = d->floor_tau; A.floor_vmax = d->floor_vmax; A.flux = d->flux; A.halo = d->halo; A.nown = d->nown;
+  A.scalar = d->scalar; A.s_u0 = d->s_u0; A.s_next = d->s_next;
   std::vector<double> F(FLUX_SLOT);
   for (int i = 0; i < r->nleaves; i++) {
     int leaf = r->leaf[i];
