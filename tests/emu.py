@@ -33,6 +33,9 @@ def lib():
         _lib = ctypes.CDLL(SO)
         _lib.emu_stage.argtypes = [ctypes.POINTER(OmbStageDesc), ctypes.c_int]
         _lib.emu_set_order.argtypes = [ctypes.c_int]
+        _lib.emu_scalar_input.argtypes = [ctypes.c_void_p, ctypes.c_longlong, ctypes.c_int, ctypes.c_void_p,
+                                          ctypes.c_int, ctypes.c_double, ctypes.c_double, ctypes.c_double,
+                                          ctypes.c_void_p]
         _lib.emu_gather.argtypes = [ctypes.c_void_p, ctypes.c_longlong, ctypes.c_void_p, ctypes.c_int, ctypes.c_int,
                                     ctypes.c_void_p]
         _lib.emu_amr_ghosts.argtypes = [ctypes.POINTER(OmbAmrDesc)]
@@ -58,9 +61,16 @@ class EmuStepper:
         self.amax = 0.0
         self.fallback = 0
 
+    scalars = None  # (NS, L*512): passive scalars, stepped by the scalar pass after each stage
+
     def rk3_step(self, dt):
         b = self.b
         U0 = np.ascontiguousarray(b.pack())
+        X = None if self.scalars is None else [[np.ascontiguousarray(x.reshape(-1).copy()), np.zeros(b.fstride),
+                                                np.zeros(b.fstride), np.zeros(b.fstride)] for x in self.scalars]
+        if X is not None:
+            for xs in X:  # stage buffers sized like a field (virtual leaves included)
+                xs[0] = np.concatenate([xs[0], np.zeros(b.fstride - xs[0].size)])
         bufs = [U0, np.empty_like(U0), np.empty_like(U0), np.empty_like(U0)]
         dtv = np.array([dt])
         G = None if self.grav is None else np.ascontiguousarray(b.pack_gravity(self.grav))
@@ -91,10 +101,30 @@ class EmuStepper:
             if len(rleaf):
                 lib().emu_reflux_update(ctypes.byref(OmbRefluxDesc(stage=d, leaf=ptr(rleaf), off=ptr(roff),
                                                                    tasks=ptr(rtasks), nleaves=len(rleaf))))
+            for xs in X or []:  # the scalar pass, as B200HydroStepper._scalar_passes
+                sin = np.zeros(6 * b.fstride)
+                args = (ptr(bufs[cur]), b.fstride, b.L + b.nvirtual)
+                lib().emu_scalar_input(*args, ptr(xs[cur]), b.L, self.gamma, self.gamma - 1.0, self.eta, ptr(sin))
+                if b.nvirtual:
+                    lib().emu_amr_ghosts(ctypes.byref(OmbAmrDesc(u=ptr(sin), fstride=b.fstride, tasks=ptr(tasks),
+                                                                  ntasks=b.nvirtual)))
+                    lib().emu_scalar_input(*args, None, 0, self.gamma, self.gamma - 1.0, self.eta, ptr(sin))
+                ds = OmbStageDesc.from_buffer_copy(d)
+                dummy = np.zeros(2, dtype=np.uint64)
+                ds.ucur, ds.scalar, ds.s_u0, ds.s_next = ptr(sin), 1, ptr(xs[0]), ptr(xs[nxt])
+                ds.amax_bits, ds.fallback = ptr(dummy), ptr(dummy[1:])
+                rc = lib().emu_stage(ctypes.byref(ds), self.nthr)
+                if rc != 0:
+                    raise RuntimeError(f"emu_stage (scalar) failed ({rc})")
+                if len(rleaf):
+                    lib().emu_reflux_update(ctypes.byref(OmbRefluxDesc(stage=ds, leaf=ptr(rleaf), off=ptr(roff),
+                                                                       tasks=ptr(rtasks), nleaves=len(rleaf))))
             self.amax = max(self.amax, float(am.view(np.float64)[0]))
             self.fallback += int(fb[0])
             cur = nxt
         b.unpack(bufs[cur])
+        if X is not None:
+            self.scalars = np.stack([xs[cur][:b.L * 512].reshape(b.L, 8, 8, 8) for xs in X])
 
 
 class EmuDistStepper:
@@ -152,9 +182,16 @@ class EmuDistStepper:
                                     [c * row for c in p.flux_recv_counts], [c * row for c in p.flux_send_counts])
         fl[p.flux_recv_slots] = recv[:nr * row].reshape(nr, row)
 
+    scalars = None  # (NS, L*512): passive scalars, stepped by the scalar pass after each stage
+
     def rk3_step(self, dt):
         b = self.b
         U0 = np.ascontiguousarray(b.pack())
+        X = None if self.scalars is None else [[np.ascontiguousarray(x.reshape(-1).copy()), np.zeros(b.fstride),
+                                                np.zeros(b.fstride), np.zeros(b.fstride)] for x in self.scalars]
+        if X is not None:
+            for xs in X:  # stage buffers sized like a field (virtual leaves included)
+                xs[0] = np.concatenate([xs[0], np.zeros(b.fstride - xs[0].size)])
         bufs = [U0, np.empty_like(U0), np.empty_like(U0), np.empty_like(U0)]
         dtv = np.array([dt])
         flux = np.zeros(max(1, b.flux_slots) * FLUX_SLOT_DOUBLES)
@@ -185,6 +222,24 @@ class EmuDistStepper:
             if len(rleaf):
                 lib().emu_reflux_update(ctypes.byref(OmbRefluxDesc(stage=d, leaf=ptr(rleaf), off=ptr(roff),
                                                                    tasks=ptr(rtasks), nleaves=len(rleaf))))
+            for xs in X or []:  # the scalar pass, as B200HydroStepper._scalar_passes
+                sin = np.zeros(6 * b.fstride)
+                args = (ptr(bufs[cur]), b.fstride, b.L + b.nvirtual)
+                lib().emu_scalar_input(*args, ptr(xs[cur]), b.L, self.gamma, self.gamma - 1.0, self.eta, ptr(sin))
+                if b.nvirtual:
+                    lib().emu_amr_ghosts(ctypes.byref(OmbAmrDesc(u=ptr(sin), fstride=b.fstride, tasks=ptr(tasks),
+                                                                  ntasks=b.nvirtual)))
+                    lib().emu_scalar_input(*args, None, 0, self.gamma, self.gamma - 1.0, self.eta, ptr(sin))
+                ds = OmbStageDesc.from_buffer_copy(d)
+                dummy = np.zeros(2, dtype=np.uint64)
+                ds.ucur, ds.scalar, ds.s_u0, ds.s_next = ptr(sin), 1, ptr(xs[0]), ptr(xs[nxt])
+                ds.amax_bits, ds.fallback = ptr(dummy), ptr(dummy[1:])
+                rc = lib().emu_stage(ctypes.byref(ds), self.nthr)
+                if rc != 0:
+                    raise RuntimeError(f"emu_stage (scalar) failed ({rc})")
+                if len(rleaf):
+                    lib().emu_reflux_update(ctypes.byref(OmbRefluxDesc(stage=ds, leaf=ptr(rleaf), off=ptr(roff),
+                                                                       tasks=ptr(rtasks), nleaves=len(rleaf))))
             self.amax = max(self.amax, float(am.view(np.float64)[0]))
             cur = nxt
         b.unpack(bufs[cur])

@@ -162,3 +162,17 @@ extern "C" int emu_reflux_update(const OmbRefluxDesc* r) {
   }
   return 0;
 }
+
+// passive-scalar pass input (omb_scalar_input): (rho, sx, sy, sz, p, X)
+extern "C" int emu_scalar_input(const double* U, long long fstride, int n_all, const double* x, int n_x, double gamma,
+                                double gm1, double eta, double* dst) {
+  for (long long c = 0; c < (long long)n_all * 512; c++) {
+    double u[NF], w[NF];
+    for (int v = 0; v < NF; v++) u[v] = U[v * fstride + c];
+    prim_cell(u, gamma, gm1, eta, w);
+    for (int v = 0; v < 4; v++) dst[v * fstride + c] = u[v];
+    dst[4 * fstride + c] = w[4];
+    if (x != nullptr && c < (long long)n_x * 512) dst[5 * fstride + c] = x[c];
+  }
+  return 0;
+}

@@ -158,3 +158,17 @@ def test_emulated_race_check(order, name):
     assert bitwise_mismatch(state_of(t), g["state1"]) == 0
     assert em.amax == float(g["amax"][0])
     assert em.fallback == int(g["fallback"][0])
+
+
+@pytest.mark.parametrize("name", ["sedov_c1", "amr_reflux"])
+def test_emulated_scalar_tracks_rho(name):
+    """The passive-scalar pass of the fused kernel (host emulation): X = rho stays
+    bitwise rho, X = 2 rho stays 2 X (uniform and AMR with reflux)."""
+    t, g = case_tree(name)
+    em = EmuStepper(t, 1.4, max_run=4)
+    rho = state_of(t)[:, 0]
+    em.scalars = np.stack([rho, 2.0 * rho])
+    em.rk3_step(float(g["dts"][0]))
+    assert bitwise_mismatch(state_of(t), g["state1"]) == 0
+    assert np.array_equal(em.scalars[0], state_of(t)[:, 0])
+    assert np.array_equal(em.scalars[1], 2.0 * em.scalars[0])
