@@ -176,6 +176,13 @@ class LeafBatch:
                         octa = int(pos[a]) & 1
                         c0 = octa * (n // 2) + fr[0] // 2
                         c1 = octa * (n // 2) + (fr[1] - 1) // 2 + 1
+                        # the reference prolongs the coarse sub-block clipped to [c0-1, c1+1) (ghosts.py:62-85);
+                        # its one-sided edge slopes (transfer.py _edge_padded) then fall on the margin
+                        # rows, never on the cells the region samples.  That invariant is also what lets a
+                        # leaf reading virtual regions join a run: inside a run, A's +x diagonal ghosts come
+                        # from B's face region instead of A's own -- the same coarse cells with the same
+                        # interior-slope values (c4 tree: runs of 1 and 4 bitwise equal,
+                        # tests/test_gpu_bench_parity.py::test_c4_run_lengths_bitwise)
                         m0, m1 = max(c0 - 1, 0), min(c1 + 1, n)
                         t[6 + a], t[9 + a], t[12 + a] = m0, m1, fr[0] + octa * n - 2 * m0
                 else:

@@ -13,7 +13,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 SO = os.path.join(HERE, "libomb200.so")
 SOURCES = ["omb_kernels.cu", "omb_fmm.cu"]
-HEADERS = ["omb_math.cuh", "omb_stage.cuh", "omb_pow.cuh", "omb_pow_tables.cuh", "omb_order.cuh"]
+HEADERS = ["omb_math.cuh", "omb_stage.cuh", "omb_pow.cuh", "omb_pow_tables.cuh", "omb_items.cuh"]
 NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-fmad=false", "-std=c++17",
               "-Xptxas", "-v", "-shared", "-Xcompiler", "-fPIC"]
 

@@ -49,53 +49,30 @@ OMB_HD int dl_line(int dl) { return dl < 5 ? (dl == 0 ? 0 : dl + 2) : dl + 4; }
 // in-plane lines 1, 2, 7, 8
 OMB_HD int ip_line(int ip) { return ip < 2 ? ip + 1 : ip + 5; }
 
-// inclusive P ranges (y, z) of the interfaces each line contributes to faces
-// of interior cells (derived from the face tables, geometry.py:51-97)
-OMB_HD void used_range(int l, int& ylo, int& yhi, int& zlo, int& zhi) {
-  ylo = (l == 3 || l == 9 || l == 10) ? 2 : 3;
-  yhi = (l == 4 || l == 11 || l == 12) ? 11 : 10;
-  zlo = (l == 5 || l == 9 || l == 11) ? 2 : 3;
-  zhi = (l == 6 || l == 10 || l == 12) ? 11 : 10;
-}
-
 OMB_HD int pos10(int y, int z) { return (y - 2) * 10 + (z - 2); }
 
-// Item order of the 100 lo/hi positions of a plane for one line: positions
-// whose lo or hi feeds a flux come first (a rectangle), the rest -- needed
-// only for the reference's positivity-fallback count, i.e. only rho and p --
-// last, so whole warps take the 2-field path.  shape: 0 = [3,10]^2 (line 0),
-// 1 = y in [2,11] x z in [3,10] (lines 1,3,4), 2 = y in [3,10] x z in [2,11]
-// (lines 2,5,6), 3 = all (diagonals 7..12).
-// Within that, the order is a table (omb_order.cuh, gen_position_order.py)
-// chosen so each half-warp's 8-byte shared-memory accesses -- through the
-// prim ring (row pitch 14) and the lo/hi / point-flux slots (pitch 10) -- hit
-// distinct banks, for the alignment a = 100k mod 16 at which the k-th line of
-// a phase starts (ncu: the row-major order cost 76 M excess wavefronts per c2
-// launch in the stencil loads alone).
-OMB_HD int line_shape(int l) {
-  if (l == 0) return 0;
-  if (l == 1 || l == 3 || l == 4) return 1;
-  if (l == 2 || l == 5 || l == 6) return 2;
-  return 3;
-}
-OMB_HD int shape_needed(int sh) { return sh == 0 ? 64 : (sh == 3 ? 100 : 80); }
+// The items of the reconstruction phases -- (line, position) of a plane --
+// come from tables (omb_items.cuh, gen_phase_items.py): ordered by cost (KT
+// with 3, 2, 1 axes, then reconstruction only, then the rho/p-only positions
+// whose lo/hi feed no flux but count in the reference's positivity fallback),
+// then half-warp by half-warp so the 8-byte shared-memory accesses through
+// the prim ring (row pitch 14) and the lo/hi / point-flux slots (pitch 10) hit
+// distinct banks.  Entry: bits 0-6 pos10, 7-10 the line's index in the phase,
+// 11 FULL (all six fields; else rho and p only), 12 KT (the interface from
+// the previous plane into this position feeds a face).
 }  // namespace omb
-#include "omb_order.cuh"
+#include "omb_items.cuh"
 namespace omb {
 #ifdef __CUDACC__
-static __device__ const unsigned char d_pos_order[11][100] = OMB_ORDER_TABLE;
+static __device__ const unsigned short d_items[OMB_ITEMS_TOTAL] = OMB_ITEMS_ALL;
 #endif
-static const unsigned char h_pos_order[11][100] = OMB_ORDER_TABLE;
-// i-th position of the line that is the k-th (k = 0..4) of its phase
-OMB_HD void shape_pos(int sh, int k, int i, int& y, int& z) {
-  int row = order_row(sh, (4 * k) & 15);
+static const unsigned short h_items[OMB_ITEMS_TOTAL] = OMB_ITEMS_ALL;
+OMB_HD unsigned item_entry(int off, int it) {
 #ifdef __CUDA_ARCH__
-  int p = __ldg(&d_pos_order[row][i]);
+  return __ldg(&d_items[off + it]);
 #else
-  int p = h_pos_order[row][i];
+  return h_items[off + it];
 #endif
-  y = 2 + p / 10;
-  z = 2 + p % 10;
 }
 OMB_HD int yslot(int y, int z) { return (y - 2) * 8 + (z - 3); }
 OMB_HD int zslot(int y, int z) { return (y - 3) * 9 + (z - 2); }
@@ -468,20 +445,20 @@ struct Stage {
 
   // ---- P1: boundary lines (d.x = 1) of group g on plane X ----------------
   OMB_HD void boundary_lines(int g, int tid, int nthr, Hold& h) {
-    int dl0 = g == 0 ? 0 : 5, ndl = g == 0 ? (A.new_mode ? 5 : 1) : 4;
-    int nitems = ndl * NP;
+    int dl0 = g == 0 ? 0 : 5;
+    int toff = g == 0 ? (A.new_mode ? OMB_ITEMS_P1A_NEW_OFF : OMB_ITEMS_P1A_OLD_OFF) : OMB_ITEMS_P1B_NEW_OFF;
+    int nitems = g == 0 ? (A.new_mode ? OMB_ITEMS_P1A_NEW_N : OMB_ITEMS_P1A_OLD_N) : OMB_ITEMS_P1B_NEW_N;
     h.s0 = h.s1 = -1;
 #pragma unroll 1
     for (int k = 0; k < 2; k++) {
       int it = tid + k * nthr;
       if (it >= nitems) break;
-      int dl = dl0 + it / NP, i = it % NP;
+      unsigned e = item_entry(toff, it);
+      int pos = e & 127, dl = dl0 + ((e >> 7) & 15);
       int l = dl_line(dl);
-      int sh = line_shape(l), y, z;
-      shape_pos(sh, dl - dl0, i, y, z);
-      int pos = pos10(y, z);
+      int y = 2 + pos / 10, z = 2 + pos % 10;
       double lo[NF], hi[NF];
-      mono6(l, X, y, z, lo, hi, i < shape_needed(sh));
+      mono6(l, X, y, z, lo, hi, (e >> 11) & 1);
       if (k == 0) {
 #pragma unroll
         for (int v = 0; v < NF; v++) h.h0[v] = hi[v];
@@ -491,13 +468,10 @@ struct Stage {
         for (int v = 0; v < NF; v++) h.h1[v] = hi[v];
         h.s1 = dl * NF * NP + pos;
       }
-      bool kt = X >= 3 && (A.quad || l == 0);
+      // the interface (X-1, P) -> (X, pos), P = pos - d, feeds a face of an interior cell
+      bool kt = X >= 3 && (A.quad || l == 0) && ((e >> 12) & 1);
       if (!kt) continue;
-      int py = y - ldy(l), pz = z - ldz(l);
-      int ylo, yhi, zlo, zhi;
-      used_range(l, ylo, yhi, zlo, zhi);
-      if (py < ylo || py > yhi || pz < zlo || pz > zhi) continue;
-      int pp = pos10(py, pz);
+      int pp = pos - ldy(l) * 10 - ldz(l);
       double hp[NF];
 #pragma unroll
       for (int v = 0; v < NF; v++) hp[v] = S[Smem::HI + (dl * NF + v) * NP + pp];
@@ -592,14 +566,14 @@ struct Stage {
 
   // ---- P3: in-plane lines 1, 2, 7, 8 on plane X --------------------------
   OMB_HD void inplane_lines(int tid, int nthr) {
-    int nip = A.new_mode ? 4 : 2;
-    for (int it = tid; it < nip * NP; it += nthr) {
-      int ip = it / NP, i = it % NP, l = ip_line(ip);
-      int sh = line_shape(l), y, z;
-      shape_pos(sh, ip, i, y, z);
-      int pos = pos10(y, z);
+    int toff = A.new_mode ? OMB_ITEMS_P3_NEW_OFF : OMB_ITEMS_P3_OLD_OFF;
+    int nitems = A.new_mode ? OMB_ITEMS_P3_NEW_N : OMB_ITEMS_P3_OLD_N;
+    for (int it = tid; it < nitems; it += nthr) {
+      unsigned e = item_entry(toff, it);
+      int pos = e & 127, ip = (e >> 7) & 15, l = ip_line(ip);
+      int y = 2 + pos / 10, z = 2 + pos % 10;
       double lo[NF], hi[NF];
-      mono6(l, X, y, z, lo, hi, i < shape_needed(sh));
+      mono6(l, X, y, z, lo, hi, (e >> 11) & 1);
 #pragma unroll
       for (int v = 0; v < NF; v++) {
         S[Smem::LHI + ((ip * 2 + 0) * NF + v) * NP + pos] = lo[v];

@@ -24,7 +24,7 @@ def lib():
         srcs = [os.path.join(HERE, "native", "emu_stage.cpp"),
                 os.path.join(ROOT, "paper_2107_10987_b200", "csrc", "omb_stage.cuh"),
                 os.path.join(ROOT, "paper_2107_10987_b200", "csrc", "omb_math.cuh"),
-                os.path.join(ROOT, "paper_2107_10987_b200", "csrc", "omb_order.cuh"),
+                os.path.join(ROOT, "paper_2107_10987_b200", "csrc", "omb_items.cuh"),
                 os.path.join(ROOT, "paper_2107_10987_b200", "csrc", "omb_pow.cuh")]
         if not os.path.exists(SO) or os.path.getmtime(SO) < max(os.path.getmtime(s) for s in srcs):
             os.makedirs(os.path.dirname(SO), exist_ok=True)
