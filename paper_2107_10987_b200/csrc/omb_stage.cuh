@@ -265,18 +265,6 @@ struct Stage {
   // thread-carried reductions
   double amax;
   long long fb;
-  // this thread's first item of P1A / P1B / P3 (the same every plane), loaded once
-  unsigned item_p1a, item_p1b, item_p3;
-
-  OMB_HD void load_items(int tid) {
-    int na = A.new_mode ? OMB_ITEMS_P1A_NEW_N : OMB_ITEMS_P1A_OLD_N;
-    int oa = A.new_mode ? OMB_ITEMS_P1A_NEW_OFF : OMB_ITEMS_P1A_OLD_OFF;
-    int n3 = A.new_mode ? OMB_ITEMS_P3_NEW_N : OMB_ITEMS_P3_OLD_N;
-    int o3 = A.new_mode ? OMB_ITEMS_P3_NEW_OFF : OMB_ITEMS_P3_OLD_OFF;
-    item_p1a = tid < na ? item_entry(oa, tid) : 0u;
-    item_p1b = tid < OMB_ITEMS_P1B_NEW_N ? item_entry(OMB_ITEMS_P1B_NEW_OFF, tid) : 0u;
-    item_p3 = tid < n3 ? item_entry(o3, tid) : 0u;
-  }
 
   OMB_HD double& sm(int off) { return S[off]; }
   OMB_HD double* prp(int x, int v) { return S + Smem::PR + ((x % 5) * NF + v) * PL; }
@@ -465,7 +453,7 @@ struct Stage {
     for (int k = 0; k < 2; k++) {
       int it = tid + k * nthr;
       if (it >= nitems) break;
-      unsigned e = k == 0 ? (g == 0 ? item_p1a : item_p1b) : item_entry(toff, it);
+      unsigned e = item_entry(toff, it);
       int pos = e & 127, dl = dl0 + ((e >> 7) & 15);
       int l = dl_line(dl);
       int y = 2 + pos / 10, z = 2 + pos % 10;
@@ -581,7 +569,7 @@ struct Stage {
     int toff = A.new_mode ? OMB_ITEMS_P3_NEW_OFF : OMB_ITEMS_P3_OLD_OFF;
     int nitems = A.new_mode ? OMB_ITEMS_P3_NEW_N : OMB_ITEMS_P3_OLD_N;
     for (int it = tid; it < nitems; it += nthr) {
-      unsigned e = it == tid ? item_p3 : item_entry(toff, it);
+      unsigned e = item_entry(toff, it);
       int pos = e & 127, ip = (e >> 7) & 15, l = ip_line(ip);
       int y = 2 + pos / 10, z = 2 + pos % 10;
       double lo[NF], hi[NF];
