@@ -31,7 +31,9 @@ typedef struct {
     int offmask;   /* bit 2a: the -a face is a physical wall; bit 2a+1: the +a face */
     double ox, oy, oz;  /* first interior cell centre (SubGrid.origin) */
     double dx, inv_dx;  /* cell width and the host-computed 1.0/dx */
-    int flags;     /* bit 0: export face fluxes to flux[slot]; bit 1: update deferred to omb_reflux_update */
+    int flags;     /* bit 0: export face fluxes to flux[slot]; bit 1: update deferred to omb_reflux_update;
+                    * 8^3 blocks of a 16^3/32^3 leaf: bit 2+2a / 3+2a: the positivity-fallback count on axis a
+                    * starts at 3 / ends at 10 (not 2 / 11); bits 8+5a: the block's cell offset in its leaf */
     int slot;      /* flux export slot (OMB_FLUX_SLOT doubles: FX (6,9,8,8), FY (6,8,9,8), FZ (6,8,8,9)) */
 } OmbLeafInfo;
 

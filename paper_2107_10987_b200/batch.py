@@ -92,10 +92,18 @@ class LeafBatch:
         if not 1 <= max_run <= MAX_RUN:
             raise ValueError(f"max_run must be in [1, {MAX_RUN}] (the stage kernel stages at most "
                              f"{MAX_RUN} leaf descriptors per run), got {max_run}")
+        self.blocks = None
+        if tree.n != 8:  # 16^3 / 32^3 leaves run as 8^3 blocks (blocks.py)
+            if tree.n not in (16, 32) or leaves is not None or gnbr is not None:
+                raise UnsupportedTree(f"{tree.n}^3 sub-grids: uniform single-GPU trees of n = 16 or 32 only")
+            from .blocks import BlockTree
+
+            try:
+                tree = self.blocks = BlockTree(tree)
+            except NotImplementedError as e:
+                raise UnsupportedTree(str(e)) from None
         self.tree = tree
         self.n = tree.n
-        if self.n != 8:
-            raise UnsupportedTree("the fused stage kernel is built for 8^3 sub-grids")
         if tree.boundary not in BC_CODES:
             raise ValueError(f"unknown boundary {tree.boundary!r}")
         self.bc = BC_CODES[tree.boundary]
@@ -126,7 +134,12 @@ class LeafBatch:
                 rec["nbr"] = [local[int(g)] if g >= 0 else g for g in row]
             else:
                 rec["nbr"] = -1
-            rec["ox"], rec["oy"], rec["oz"] = (float(x) for x in sg.origin)
+            # cell centres origin + dx * i (blocks: the leaf's origin, offsets in flags)
+            rec["ox"], rec["oy"], rec["oz"] = (float(x) for x in getattr(sg, "leaf_origin", sg.origin))
+            if self.blocks is not None:
+                from .blocks import block_flags
+
+                rec["flags"] |= block_flags(lf.b, self.blocks.nb)
             rec["dx"] = sg.dx
             rec["inv_dx"] = 1.0 / sg.dx
             self.dx[i] = sg.dx
@@ -333,6 +346,8 @@ class LeafBatch:
         array.  Cached: rebuilt only when a leaf's array object changed (the
         cache holds the arrays, so their memory cannot be reused meanwhile)."""
         arrs = [lf.subgrid.u for lf in self.leaves[:count]]
+        if any(u is None for u in arrs):  # 16^3 / 32^3 blocks: interior views only
+            return None
         cache = getattr(self, "_ptr_cache", {}).get(count)
         if cache is not None and all(map(operator.is_, arrs, cache[0])):
             return cache[1]
@@ -370,7 +385,12 @@ class LeafBatch:
     def pack_gravity(self, fields):
         G = np.zeros((4, self.L + self.nvirtual, 8, 8, 8))
         for i, lf in enumerate(self.leaves):
-            f = fields[lf.path]
+            if self.blocks is None:
+                f, sl = fields[lf.path], (slice(None),) * 3
+            else:  # a block of a 16^3 / 32^3 leaf: its part of the leaf's fields
+                f = fields[lf.leaf.path]
+                sl = tuple(slice(8 * b, 8 * b + 8) for b in lf.b)
+            n = self.blocks.nb * 8 if self.blocks is not None else 8
             for k, name in enumerate(("gx", "gy", "gz", "dphi_dt")):
-                G[k, i] = np.broadcast_to(f[name], (8, 8, 8))
+                G[k, i] = np.broadcast_to(f[name], (n, n, n))[sl]
         return G

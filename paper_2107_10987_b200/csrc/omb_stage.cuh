@@ -173,7 +173,8 @@ struct LeafInfo {
   int nbr[27];    // batch index of the same-level (or virtual AMR) neighbour per offset, -1 none
   int offmask;    // bit 2a: -a side is a physical wall, bit 2a+1: +a side
   double ox, oy, oz, dx, inv_dx;
-  int flags;      // bit 0: export face fluxes to flux[slot]; bit 1: update deferred (reflux)
+  int flags;      // bit 0: export face fluxes to flux[slot]; bit 1: update deferred (reflux);
+                  // 16^3/32^3 blocks (blocks.py): bits 2-7 fallback-count range, 8-22 cell offsets
   int slot;
 };
 constexpr int FLUX_SLOT = 3 * NF * 9 * 8 * 8;  // FX (6,9,8,8) | FY (6,8,9,8) | FZ (6,8,8,9)
@@ -295,10 +296,24 @@ struct Stage {
     return (LI.flags & 1) ? A.flux + (long long)LI.slot * FLUX_SLOT : nullptr;
   }
 
-  OMB_HD int mult(int X) const {  // how many leaves of the run count plane X in [2,12)
+  // how many leaves of the run count position (X, y, z) in the reference's positivity-fallback
+  // count: [2,12)^3 per leaf (_core.pyx:143-155); a block of a 16^3 / 32^3 leaf (blocks.py) counts
+  // only its share of its leaf's range (flags bits 2-7: the range starts at 3 / ends at 10)
+#ifdef __CUDA_ARCH__
+  __device__ __noinline__  // only the rare fallback branch calls it: keep its registers out of mono6
+#else
+  inline
+#endif
+  int mult(int X, int c0) const {  // c0 = y * M + z (recovered from the stencil address)
+    int y = c0 / M, z = c0 % M;
     int c = 0;
-    for (int r = 0; r < R; r++)
-      if (X >= 8 * r + 2 && X <= 8 * r + 11) c++;
+    for (int r = 0; r < R; r++) {
+      int f = LIs[r].flags;
+      bool in = X >= 8 * r + 2 + ((f >> 2) & 1) && X <= 8 * r + 11 - ((f >> 3) & 1) &&
+                y >= 2 + ((f >> 4) & 1) && y <= 11 - ((f >> 5) & 1) && z >= 2 + ((f >> 6) & 1) &&
+                z <= 11 - ((f >> 7) & 1);
+      c += in;
+    }
     return c;
   }
   OMB_HD bool interior(int X) const { return X >= 3 && X < 8 * R + 3; }
@@ -423,12 +438,12 @@ struct Stage {
     }
     if (A.contact) contact_steepen(rr, pm1, pp1, A.gamma, lo[0], hi[0]);
     if (lo[0] <= 0.0 || lo[4] <= 0.0) {
-      fb += mult(X);
+      fb += mult(X, ad[2] - ring[2]);
 #pragma unroll
       for (int v = 0; v < NF; v++) lo[v] = S[ad[2] + v * PL];
     }
     if (hi[0] <= 0.0 || hi[4] <= 0.0) {
-      fb += mult(X);
+      fb += mult(X, ad[2] - ring[2]);
 #pragma unroll
       for (int v = 0; v < NF; v++) hi[v] = S[ad[2] + v * PL];
     }
@@ -717,8 +732,8 @@ struct Stage {
       if (P.has_grav)
 #pragma unroll
         for (int k = 0; k < 4; k++) g[k] = S[Smem::SG6 + (2 * NF + k) * NFACEX + it];
-      double xc = LI.ox + LI.dx * (double)lx;
-      double yc = LI.oy + LI.dx * (double)(y - 3);
+      double xc = LI.ox + LI.dx * (double)(lx + ((LI.flags >> 8) & 31));  // origin + dx * i of the leaf
+      double yc = LI.oy + LI.dx * (double)(y - 3 + ((LI.flags >> 13) & 31));
       update_cell_rk(P, u, u0, rr, xc, yc, g, nw);
 #pragma unroll
       for (int v = 0; v < NF; v++) S[Smem::SG6 + v * NFACEX + it] = nw[v];
@@ -780,8 +795,8 @@ struct Stage {
       if (P.has_grav)
 #pragma unroll
         for (int k = 0; k < 4; k++) g[k] = S[Smem::SG6 + (2 * NF + k) * NFACEX + it];
-      double xc = LI.ox + LI.dx * (double)lx;
-      double yc = LI.oy + LI.dx * (double)(y - 3);
+      double xc = LI.ox + LI.dx * (double)(lx + ((LI.flags >> 8) & 31));  // origin + dx * i of the leaf
+      double yc = LI.oy + LI.dx * (double)(y - 3 + ((LI.flags >> 13) & 31));
       if (A.scalar) {
         update_cell_rk(P, u, u0, rr, xc, yc, g, out);
         A.s_next[cell] = out[NF - 1];
@@ -907,8 +922,8 @@ OMB_HD void update_leaf(const StageArgs& A, int leaf, const double* F, int tid, 
     if (P.has_grav)
 #pragma unroll
       for (int q = 0; q < 4; q++) g[q] = A.grav[q * A.fstride + cell];
-    double xc = LI.ox + LI.dx * (double)x;
-    double yc = LI.oy + LI.dx * (double)y;
+    double xc = LI.ox + LI.dx * (double)(x + ((LI.flags >> 8) & 31));
+    double yc = LI.oy + LI.dx * (double)(y + ((LI.flags >> 13) & 31));
     if (A.scalar) {
       update_cell_rk(P, u, u0, rr, xc, yc, g, out);
       A.s_next[cell] = out[NF - 1];

@@ -156,6 +156,9 @@ class B200HydroStepper:
 
         # a device FMM (gravity.B200FmmSolver) is solved on the device every stage, in place
         self._dev_gravity = isinstance(gravity, B200FmmSolver)
+        if b.blocks is not None and (self._dev_gravity or (gravity is not None and
+                                                            not getattr(gravity, "state_independent", False))):
+            raise NotImplementedError("16^3 / 32^3 sub-grids with a state-dependent gravity solver")
         if self._dev_gravity:
             gravity.prepare(tree)
             if partition is not None:
@@ -230,6 +233,8 @@ class B200HydroStepper:
         if ns == 0:
             return
         b = self.batch
+        if b.blocks is not None:
+            raise NotImplementedError("passive scalars with 16^3 / 32^3 sub-grids")
         self._sbuf = [[torch.zeros(b.fstride, dtype=torch.float64, device=self.dev) for _ in range(4)]
                       for _ in range(ns)]
         self._sin = torch.empty(6 * b.fstride, dtype=torch.float64, device=self.dev)
@@ -509,7 +514,8 @@ class B200HydroStepper:
             if g < big:
                 raise NumericsError(f"non-finite wave speed on leaf {self.tree.sorted_leaves()[g].path}")
         elif bad >= 0:
-            raise NumericsError(f"non-finite wave speed on leaf {self.batch.leaves[bad].path}")
+            lf = self.batch.leaves[bad]
+            raise NumericsError(f"non-finite wave speed on leaf {getattr(lf, 'leaf', lf).path}")
         return cfl * float(out[0])
 
     # -- one step -----------------------------------------------------------------------
@@ -663,7 +669,8 @@ class B200HydroStepper:
         acc = self._acc.cpu().numpy()
         amax = acc[:3].view(np.float64)
         fb = acc[3:]
-        L = self.nglobal
+        # the reference's logical count is per leaf of ITS tree (16^3 / 32^3 leaves run as 8^3 blocks)
+        L = len(self.tree.leaves()) if self.batch.blocks is not None else self.nglobal
         stats = StepStats()
         u_prev = start
         for s in range(3):

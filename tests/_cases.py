@@ -68,6 +68,12 @@ def case_tree(name):
             t.reindex()
     elif name == "gravity_density":
         t = mesh.build_uniform_tree(1, 8, boundary="reflecting")
+    elif name == "sedov_n16":
+        t = mesh.build_uniform_tree(1, 16, boundary="reflecting")
+    elif name == "sedov_n32":
+        t = mesh.build_uniform_tree(0, 32, boundary="reflecting")
+    elif name in ("smooth_n16", "fallback_n16"):
+        t = mesh.build_uniform_tree(1, 16, boundary="periodic")
     else:
         raise KeyError(name)
     g = golden(name)

@@ -431,7 +431,31 @@ def flux_point_cases():
     save("flux_points", **out)
 
 
+def subgrid_size_cases():
+    """16^3 and 32^3 sub-grids (tree.py:13 VALID_N): Sedov at 32^3 cells as 8 leaves of 16^3 and as
+    one leaf of 32^3 (reflecting, 2 steps), a smooth periodic 16^3 tree (1 step), and a 16^3 tree
+    with density spikes so the positivity fallback fires (per-leaf counts)."""
+    t = build_uniform_tree(1, 16, boundary="reflecting")
+    init_sedov(SedovConfig(), t, EOS)
+    step_case("sedov_n16", t, steps=2)
+    t = build_uniform_tree(0, 32, boundary="reflecting")
+    init_sedov(SedovConfig(), t, EOS)
+    step_case("sedov_n32", t, steps=2)
+    t = build_uniform_tree(1, 16, boundary="periodic")
+    random_smooth(t, seed=15)
+    step_case("smooth_n16", t, steps=1)
+    t = build_uniform_tree(1, 16, boundary="periodic")
+    random_smooth(t, seed=16)
+    for lf in t.leaves():  # zero-pressure cells (egas = tau = 0, at rest): the fallback fires around them
+        for c in ((7, 7, 7), (8, 3, 12), (0, 15, 3), (15, 0, 8), (3, 8, 0)):  # incl. cells on leaf / block edges
+            lf.subgrid.interior[1:6][(slice(None),) + c] = 0.0
+    step_case("fallback_n16", t, steps=1, cfl=0.1)
+
+
 def main():
+    if sys.argv[1:] == ["n16"]:
+        subgrid_size_cases()
+        return
     if sys.argv[1:] == ["modes"]:
         mode_cases()
         density_gravity_cases()
@@ -472,6 +496,7 @@ def main():
     mode_cases()
     density_gravity_cases()
     flux_point_cases()
+    subgrid_size_cases()
 
 
 if __name__ == "__main__":

@@ -172,3 +172,15 @@ def test_emulated_scalar_tracks_rho(name):
     assert bitwise_mismatch(state_of(t), g["state1"]) == 0
     assert np.array_equal(em.scalars[0], state_of(t)[:, 0])
     assert np.array_equal(em.scalars[1], 2.0 * em.scalars[0])
+
+
+@pytest.mark.parametrize("name", ["sedov_n16", "sedov_n32", "smooth_n16", "fallback_n16"])
+def test_emulated_subgrid_sizes(name):
+    """16^3 and 32^3 sub-grids run as 8^3 blocks (paper_2107_10987_b200/blocks.py): the
+    reference's step bitwise, and its per-leaf positivity-fallback count exactly."""
+    t, g = case_tree(name)
+    em = EmuStepper(t, 1.4)
+    em.rk3_step(float(g["dts"][0]))
+    assert bitwise_mismatch(state_of(t), g["state1"]) == 0
+    assert em.amax == float(g["amax"][0])
+    assert em.fallback == int(g["fallback"][0])

@@ -501,3 +501,22 @@ def test_device_pow_is_glibc():
                                   ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)), "omb_selftest_pow")
     got = out.cpu().numpy()
     assert bitwise_mismatch(got, ref) == 0
+
+
+@pytest.mark.parametrize("name", ["sedov_n16", "sedov_n32", "smooth_n16", "fallback_n16"])
+def test_subgrid_sizes_16_32(name):
+    """octomini's 16^3 and 32^3 sub-grids (tree.py:13) through B200HydroStepper: every step
+    bitwise, the per-leaf fallback count exact, kernel_launches counted per leaf of the tree."""
+    t, g = case_tree(name)
+    st = _stepper(t)
+    for s in range(len(g["dts"])):
+        dt = st.cfl_dt(0.1 if name == "fallback_n16" else 0.4)
+        assert dt == float(g["dts"][s])
+        stats = st.rk3_step(dt)
+        if s == 0:
+            _check_state(t, g)
+        assert stats.amax == float(g["amax"][s])
+        assert stats.fallback_count == int(g["fallback"][s])
+        assert stats.kernel_launches == 6 * len(t.leaves())
+    if "final" in g:
+        _check_state(t, g, "final")
