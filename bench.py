@@ -53,6 +53,8 @@ def parse():
     p.add_argument("--e2e-steps", type=int, default=8)
     p.add_argument("--cpu-leaves", type=int, default=512)
     p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--subgrid", type=int, default=8, choices=[8, 16, 32],
+                   help="sub-grid edge of the uniform Sedov trees (16/32: single GPU; run as 8^3 blocks)")
     p.add_argument("--efficiency-steps", type=int, default=10,
                    help="N>1: steps of the whole workload on rank 0's GPU alone (0 = skip)")
     p.add_argument("--config", default=None, choices=["c2", "c3", "c4", "c5", "c5g"],
@@ -63,6 +65,9 @@ def parse():
     return p.parse_args()
 
 
+SUBGRID_N = 8  # --subgrid: sub-grid edge of the uniform Sedov trees (8, 16 or 32; same cells)
+
+
 def sedov_tree(level):
     from octomini_host import SedovConfig, build_uniform_tree, init_sedov
     from paper_2107_10987_b200 import EosConfig
@@ -71,7 +76,8 @@ def sedov_tree(level):
         from octomini_host import amr_sedov_tree
 
         return amr_sedov_tree()
-    t = build_uniform_tree(level, 8, boundary="reflecting")
+    # the same 8*2^level cells per edge as SUBGRID_N^3 leaves (c2 may also read 512 x 16^3)
+    t = build_uniform_tree(level - {8: 0, 16: 1, 32: 2}[SUBGRID_N], SUBGRID_N, boundary="reflecting")
     init_sedov(SedovConfig(), t, EosConfig(gamma=1.4))
     return t
 
@@ -98,7 +104,8 @@ def workload_name(level, nleaves):
     if level == "c4":
         return f"sedov_amr_L3-6_n8 (config c4): {nleaves} sub-grids of 8^3 on levels 3-6 (SURVEY.md 8d construction)"
     tag = {4: " (config c2: 128^3)", 5: " (config c3: 256^3)"}.get(level, "")
-    return f"sedov_uniform_L{level}_n8{tag}"
+    lv = level - {8: 0, 16: 1, 32: 2}[SUBGRID_N]
+    return f"sedov_uniform_L{lv}_n{SUBGRID_N}{tag}"
 
 
 def peaks():
@@ -501,7 +508,10 @@ def gpu_arm(args, rank, world):
         "single_gpu": single,
         "vs_baseline": None,
         "dtype": "f64", "data": "synthetic (init_sedov Sedov-Taylor, no RNG)",
-        "config": {"workload": f"{workload_name(level, info['nglobal'])}: {info['nglobal']} sub-grids of 8^3 = {cells} cells, "
+        "config": {"workload": f"{workload_name(level, info['nglobal'])}: " + (
+                       f"{info['nglobal']} sub-grids of 8^3" if SUBGRID_N == 8 else
+                       f"{info['nglobal'] // (SUBGRID_N // 8) ** 3} sub-grids of {SUBGRID_N}^3 (run as "
+                       f"{info['nglobal']} 8^3 blocks)") + f" = {cells} cells, "
                                "reflecting, cfl 0.4, scheme new",
                    "step": "cfl_dt + 3 fused RK stages, dt on device",
                    "l2": "working set (3 x 6 x cells x 8 B = %.0f MB) > 126 MB L2; no flush" % (3 * 48 * cells / 1e6),
@@ -547,6 +557,8 @@ def main():
     _JSON_OUT = os.fdopen(os.dup(1), "w")
     os.dup2(2, 1)
     args = parse()
+    global SUBGRID_N
+    SUBGRID_N = args.subgrid
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     if args.impl == "reference":  # CPU only, rank 0 alone; no collectives needed
