@@ -12,9 +12,12 @@ Order, the point of the tables:
      rho/p-only -- so warps are uniformly heavy or light and the heavy ones spread
      over fewer warps (the barrier after P1 held 60 % of the kernel's barrier
      stalls with the per-line order: every warp carried a heavy lane);
-  2. within a class, line by line, positions chosen half-warp by half-warp so
-     the 8-byte shared-memory accesses hit distinct banks through both pitches
-     the items use (prim ring rows: 14 doubles; lo/hi and point-flux slots: 10).
+  2. within a class, each line's 8 x 8 block first as half-warps of (8 z of
+     row y, the same z of row y + 4): the 8-byte shared-memory accesses then hit
+     distinct banks through both pitches the items use (prim ring rows: 14
+     doubles; lo/hi and point-flux slots: 10 -- both put rows 4 apart 8 doubles
+     apart mod 16); the rest greedily, then a local search (swaps inside a class)
+     on the exact per-half-warp bank cost of every access site.
 
     python paper_2107_10987_b200/csrc/gen_phase_items.py
 """
@@ -60,6 +63,22 @@ def banks(p):
     return (p[0] * 14 + p[1]) % 16, (p[0] * 10 + p[1]) % 16
 
 
+def paired_rows(cells):
+    """Up to 64 cells of a rectangle in half-warps of (8 z of row y, the same z of row y + 4): both
+    pitches (14, 10) put rows y and y + 4 eight doubles apart mod 16, so each half-warp hits 16
+    distinct bank pairs.  Returns (ordered, leftover)."""
+    have = set(cells)
+    for y0 in sorted({y for y, _ in cells}):
+        for z0 in sorted({z for _, z in cells}):
+            out = []
+            for q in range(4):
+                for h in (0, 4):
+                    out += [(y0 + q + h, z0 + j) for j in range(8)]
+            if set(out) <= have:  # the first 8 x 8 square inside the set
+                return out, [c for c in cells if c not in set(out)]
+    return [], list(cells)
+
+
 def table(lines, with_kt, seed):
     rng = random.Random(seed)
     groups = []  # (class rank, line index, positions)
@@ -73,18 +92,92 @@ def table(lines, with_kt, seed):
             rng.shuffle(ps)
             groups.append((c, k, ps))
     groups.sort(key=lambda g: (g[0], g[1]))
+    # KT classes: each line's paired-row block of 64 (aligned half-warps, conflict-free), the rest after
     items = []
-    for c, k, ps in groups:
-        pool = list(ps)
-        while pool:
-            w = len(items) // 16  # half-warp of the next item
-            used = [banks(items_pos) for (kk, items_pos, _, _) in items[16 * w:] if kk == k]
-            u14, u10 = {b[0] for b in used}, {b[1] for b in used}
-            j = min(range(len(pool)), key=lambda i: (banks(pool[i])[0] in u14) + (banks(pool[i])[1] in u10))
-            p = pool.pop(j)
-            l = lines[k]
-            items.append((k, p, p in needed(l), with_kt and p in kt_set(l)))
+    for c in sorted({g[0] for g in groups}):
+        if c <= 3:  # KT with 3, 2, 1 axes; reconstruction only
+            rest = []
+            for cc, k, ps in groups:
+                if cc != c:
+                    continue
+                blk, left = paired_rows(ps)
+                l = lines[k]
+                items += [(k, p, p in needed(l), with_kt and p in kt_set(l)) for p in blk]
+                rest.append((cc, k, left))
+            todo = rest
+        else:
+            todo = [g for g in groups if g[0] == c]
+        for _, k, ps in todo:
+            pool = list(ps)
+            while pool:
+                w = len(items) // 16
+                used = [banks(ip) for (kk, ip, _, _) in items[16 * w:] if kk == k]
+                u14, u10 = {b[0] for b in used}, {b[1] for b in used}
+                j = min(range(len(pool)), key=lambda i: (banks(pool[i])[0] in u14) + (banks(pool[i])[1] in u10))
+                p = pool.pop(j)
+                l = lines[k]
+                items.append((k, p, p in needed(l), with_kt and p in kt_set(l)))
     return items
+
+
+
+PL, NP, RING = 196, 100, 6 * 196  # omb_stage.cuh: ring plane pitch, lo/hi slots per line, ring slot stride
+
+
+def accesses(item, phase_kt):
+    """The shared-memory double addresses one item touches, per access site (site -> address):
+    the 5 stencil loads of mono6 (ring rows of pitch 14; planes k for lines with d.x = 1), the
+    hi store / lo-hi stores (slots of pitch 10), and for P1 KT items the previous-plane hi load
+    and the point-flux store at P = pos - d."""
+    k_line, (y, z), full, kt, l = item
+    d = DIRS[l]
+    c0, dd = y * 14 + z, d[1] * 14 + d[2]
+    out = {}
+    for k in range(5):
+        out[("ring", k)] = ((k if d[0] else 2) * RING) + c0 + (k - 2) * dd
+    pos = (y - 2) * 10 + (z - 2)
+    out["slot"] = k_line * 6 * NP + pos
+    if kt:
+        out["hp"] = k_line * 6 * NP + pos - 10 * d[1] - d[2]
+        out["raw"] = (l % 4) * 6 * NP + pos - 10 * d[1] - d[2]
+    return out
+
+
+def window_cost(items, phase_kt):
+    """Excess wavefronts of one half-warp: per access site, max lanes on one bank pair minus 1."""
+    sites = {}
+    for it in items:
+        for key, a in accesses(it, phase_kt).items():
+            sites.setdefault(key, {}).setdefault(a % 16, set()).add(a)
+    return sum(max(len(v) for v in banks.values()) - 1 for banks in sites.values())
+
+
+def anneal(items, lines, phase_kt, iters, seed):
+    """Swap items of the same cost class (the class order stays) while the half-warp bank
+    cost does not grow."""
+    rng = random.Random(seed)
+    full = [(k, p, f, t, lines[k]) for (k, p, f, t) in items]
+    cls = [(3 - nax(lines[k])) if t else (3 if f else 4) for (k, p, f, t) in items]
+    by_cls = {}
+    for i, c in enumerate(cls):
+        by_cls.setdefault(c, []).append(i)
+    win = lambda i: i // 16
+    cost = {w: window_cost(full[16 * w:16 * w + 16], phase_kt) for w in range((len(full) + 15) // 16)}
+    for _ in range(iters):
+        c = rng.choice(list(by_cls))
+        a, b = rng.sample(by_cls[c], 2) if len(by_cls[c]) > 1 else (None, None)
+        if a is None or win(a) == win(b):
+            continue
+        wa, wb = win(a), win(b)
+        before = cost[wa] + cost[wb]
+        full[a], full[b] = full[b], full[a]
+        ca = window_cost(full[16 * wa:16 * wa + 16], phase_kt)
+        cb = window_cost(full[16 * wb:16 * wb + 16], phase_kt)
+        if ca + cb <= before:
+            cost[wa], cost[wb] = ca, cb
+        else:
+            full[a], full[b] = full[b], full[a]
+    return [(k, p, f, t) for (k, p, f, t, _) in full], sum(cost.values())
 
 
 def excess(items):
@@ -116,9 +209,11 @@ def main():
     allv, off = [], 0
     for name, lines, kt in PHASES:
         best = min((table(lines, kt, s) for s in range(40)), key=excess)
+        best, cost = anneal(best, lines, kt, 60000, 7)
+        print(name, "half-warp bank cost", cost)
         assert sorted((k, p) for k, p, _, _ in best) == sorted((k, p) for k in range(len(lines)) for p in ALL)
         enc = encode(best)
-        L.append(f"// {name}: lines {lines}, {len(enc)} items, excess bank conflicts {excess(best)}")
+        L.append(f"// {name}: lines {lines}, {len(enc)} items, excess wavefronts per plane {cost}")
         L.append(f"#define OMB_ITEMS_{name}_OFF {off}")
         L.append(f"#define OMB_ITEMS_{name}_N {len(enc)}")
         allv += enc
