@@ -380,6 +380,16 @@ def gpu_arm(args, rank, world):
                "entities": int(fs.table.nentities), "theta": fs.theta,
                "interactions_per_s": 2 * 2 * fs.stats["pairs"] / (fmm_ms / 1e3),
                "prepare_s_host": t_prep, "share_of_step": 3 * fmm_ms / (ms / K)}
+        # roofline of the M2L passes (k_fmm_m2l, omb_fmm.cu): algorithmic FP64 flops per contribution
+        # = 8 for a cell-cell monopole (L0..L3 += m D), 202 for a full order-3 one (L0 56, L1 78,
+        # L2 48, L3 20), each pair contributing to both ends; 2 solves per stage
+        if "contrib_general" in fs.stats:
+            fl = 2 * (8.0 * fs.stats["contrib_cellcell"] + 202.0 * fs.stats["contrib_general"])
+            fmm["roofline"] = {"bound": "fp64", "kernel": "k_fmm_m2l (+ upward/downward passes in the time)",
+                               "flops_per_stage": fl, "achieved": fl / (fmm_ms / 1e3) / 1e12, "peak": peak64,
+                               "unit": "TFLOP/s", "frac": fl / (fmm_ms / 1e3) / 1e12 / peak64,
+                               "contrib_cellcell": fs.stats["contrib_cellcell"],
+                               "contrib_general": fs.stats["contrib_general"]}
     # same-box single-GPU reference for the parallel efficiency: rank 0 steps the WHOLE
     # workload alone (same warm-up and step count, same initial state -- the host tree is
     # untouched by the host_sync=False run), the other ranks wait

@@ -261,6 +261,9 @@ class B200FmmSolver:
         del cs
         self._contrib1 = self._contrib[keep]
         del keep
+        # M2L work per solve (bench roofline): cell-cell monopole contributions vs full order-3 ones
+        self.stats["contrib_general"] = int(self._contrib1.numel())
+        self.stats["contrib_cellcell"] = int(self._contrib.numel()) - self.stats["contrib_general"]
         self._targets = T.from_numpy(targets.astype(np.int64)).to(dev)
         self._cell_base = T.from_numpy(t.cell_base).to(dev)
         lv = t.level
