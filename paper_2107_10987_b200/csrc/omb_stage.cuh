@@ -409,6 +409,45 @@ struct Stage {
 #pragma unroll
     for (int k = 0; k < 5; k++) ad[k] = (dx ? ring[k] : ring[2]) + c0 + (k - 2) * dd;
     double rr[5] = {0, 0, 0, 0, 0}, pm1 = 0, pp1 = 0;
+#ifdef OMB_MONO_PAIRS
+    // two fields at a time -- (rho, p), (vx, vy), (vz, tau) -- straight-line unless both
+    // stencils are flat, so the two chains interleave
+#pragma unroll
+    for (int pi = 0; pi < 3; pi++) {
+      const int va = pi == 0 ? 0 : (pi == 1 ? 1 : 3), vb = pi == 0 ? 4 : (pi == 1 ? 2 : 5);
+      if (!full && pi > 0) {
+        lo[va] = hi[va] = lo[vb] = hi[vb] = 0.0;
+        continue;
+      }
+      double sa[5], sb[5];
+#pragma unroll
+      for (int k = 0; k < 5; k++) {
+        sa[k] = S[ad[k] + va * PL];
+        sb[k] = S[ad[k] + vb * PL];
+      }
+      bool fa = sa[0] == sa[2] && sa[1] == sa[2] && sa[3] == sa[2] && sa[4] == sa[2];
+      bool fb = sb[0] == sb[2] && sb[1] == sb[2] && sb[3] == sb[2] && sb[4] == sb[2];
+      if (fa && fb) {
+        lo[va] = hi[va] = sa[2];
+        lo[vb] = hi[vb] = sb[2];
+      } else {  // a flat stencil through the full path gives lo = hi = a as well (clamp, extremum)
+        double la = iface(sa[0], sa[1], sa[2], sa[3]), ha = iface(sa[1], sa[2], sa[3], sa[4]);
+        double lb = iface(sb[0], sb[1], sb[2], sb[3]), hb = iface(sb[1], sb[2], sb[3], sb[4]);
+        mono_sel(sa[2], la, ha);
+        mono_sel(sb[2], lb, hb);
+        lo[va] = la;
+        hi[va] = ha;
+        lo[vb] = lb;
+        hi[vb] = hb;
+      }
+      if (pi == 0) {
+#pragma unroll
+        for (int k = 0; k < 5; k++) rr[k] = sa[k];
+        pm1 = sb[1];
+        pp1 = sb[3];
+      }
+    }
+#else
 #pragma unroll
     for (int v = 0; v < NF; v++) {
       if (!full && v != 0 && v != 4) {
@@ -436,6 +475,7 @@ struct Stage {
         for (int k = 0; k < 5; k++) rr[k] = s[k];
       if (v == 4) { pm1 = s[1]; pp1 = s[3]; }
     }
+#endif
     if (A.contact) contact_steepen(rr, pm1, pp1, A.gamma, lo[0], hi[0]);
     if (lo[0] <= 0.0 || lo[4] <= 0.0) {
       fb += mult(X, ad[2] - ring[2]);
