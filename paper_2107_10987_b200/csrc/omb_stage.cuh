@@ -433,8 +433,13 @@ struct Stage {
       } else {  // a flat stencil through the full path gives lo = hi = a as well (clamp, extremum)
         double la = iface(sa[0], sa[1], sa[2], sa[3]), ha = iface(sa[1], sa[2], sa[3], sa[4]);
         double lb = iface(sb[0], sb[1], sb[2], sb[3]), hb = iface(sb[1], sb[2], sb[3], sb[4]);
+#ifdef OMB_MONO_PAIRS_BRANCHY
+        mono(sa[2], la, ha);
+        mono(sb[2], lb, hb);
+#else
         mono_sel(sa[2], la, ha);
         mono_sel(sb[2], lb, hb);
+#endif
         lo[va] = la;
         hi[va] = ha;
         lo[vb] = lb;
