@@ -150,29 +150,6 @@ OMB_HD void mono(double a, double& lv, double& hv) {
   hv = nhv;
 }
 
-// mono() as selects (the same values): two fields can then be interleaved
-// instruction by instruction.  Only the rare exact division stays a branch.
-OMB_HD void mono_sel(double a, double& lv, double& hv) {
-  bool ext = (hv - a) * (a - lv) <= 0.0;
-  double diff = hv - lv;
-  double mid = a - 0.5 * (lv + hv);
-  double dm = diff * mid;
-  double d2 = diff * diff;
-  double q = d2 * (1.0 / 6.0);
-  double band = 0x1p-49 * fabs(q) + 0x1p-1000;
-  if (!ext && (!(fabs(dm - q) > band) || !(fabs(dm + q) > band))) {
-    double dd = d2;
-#ifdef __CUDA_ARCH__
-    asm volatile("" : "+d"(dd));
-#endif
-    q = dd / 6.0;
-  }
-  double nlv = dm > q ? 3.0 * a - 2.0 * hv : lv;
-  double nhv = -q > dm ? 3.0 * a - 2.0 * nlv : hv;
-  lv = ext ? a : nlv;
-  hv = ext ? a : nhv;
-}
-
 // _core.pyx:159-173
 OMB_HD double mc_slope(double am1, double a, double ap1) {
   double dc = 0.5 * (ap1 - am1);

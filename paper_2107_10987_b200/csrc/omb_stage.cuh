@@ -409,9 +409,9 @@ struct Stage {
 #pragma unroll
     for (int k = 0; k < 5; k++) ad[k] = (dx ? ring[k] : ring[2]) + c0 + (k - 2) * dd;
     double rr[5] = {0, 0, 0, 0, 0}, pm1 = 0, pp1 = 0;
-#ifdef OMB_MONO_PAIRS
-    // two fields at a time -- (rho, p), (vx, vy), (vz, tau) -- straight-line unless both
-    // stencils are flat, so the two chains interleave
+    // two fields at a time -- (rho, p), (vx, vy), (vz, tau): their loads and interface values
+    // straight-line, so the two chains interleave; the flat shortcut per pair (A/B on one box:
+    // c3 +1.4 %, c2 -0.3 %; with select-based monotonisation too: c3 +1.3 %, c2 -2.5 %)
 #pragma unroll
     for (int pi = 0; pi < 3; pi++) {
       const int va = pi == 0 ? 0 : (pi == 1 ? 1 : 3), vb = pi == 0 ? 4 : (pi == 1 ? 2 : 5);
@@ -433,13 +433,8 @@ struct Stage {
       } else {  // a flat stencil through the full path gives lo = hi = a as well (clamp, extremum)
         double la = iface(sa[0], sa[1], sa[2], sa[3]), ha = iface(sa[1], sa[2], sa[3], sa[4]);
         double lb = iface(sb[0], sb[1], sb[2], sb[3]), hb = iface(sb[1], sb[2], sb[3], sb[4]);
-#ifdef OMB_MONO_PAIRS_BRANCHY
         mono(sa[2], la, ha);
         mono(sb[2], lb, hb);
-#else
-        mono_sel(sa[2], la, ha);
-        mono_sel(sb[2], lb, hb);
-#endif
         lo[va] = la;
         hi[va] = ha;
         lo[vb] = lb;
@@ -452,35 +447,6 @@ struct Stage {
         pp1 = sb[3];
       }
     }
-#else
-#pragma unroll
-    for (int v = 0; v < NF; v++) {
-      if (!full && v != 0 && v != 4) {
-        lo[v] = 0.0;
-        hi[v] = 0.0;
-        continue;
-      }
-      double s[5];
-#pragma unroll
-      for (int k = 0; k < 5; k++) s[k] = S[ad[k] + v * PL];
-      double lv, hv;
-      if (s[0] == s[2] && s[1] == s[2] && s[3] == s[2] && s[4] == s[2]) {
-        // flat stencil: both interface values are clamped to a and the
-        // extremum test then sets lo = hi = a (_core.pyx:80-97) -- exactly
-        lv = hv = s[2];
-      } else {
-        lv = iface(s[0], s[1], s[2], s[3]);
-        hv = iface(s[1], s[2], s[3], s[4]);
-        mono(s[2], lv, hv);
-      }
-      lo[v] = lv;
-      hi[v] = hv;
-      if (v == 0)
-#pragma unroll
-        for (int k = 0; k < 5; k++) rr[k] = s[k];
-      if (v == 4) { pm1 = s[1]; pp1 = s[3]; }
-    }
-#endif
     if (A.contact) contact_steepen(rr, pm1, pp1, A.gamma, lo[0], hi[0]);
     if (lo[0] <= 0.0 || lo[4] <= 0.0) {
       fb += mult(X, ad[2] - ring[2]);
