@@ -656,11 +656,17 @@ struct Stage {
   OMB_HD void faces_yz(int tid, int nthr, int first = 0) {
     bool fin = interior(X - 1), start = interior(X);
     bool q = A.quad;
-    int t0 = tid - first;
+#ifdef OMB_FACES_SPLIT
+    // only the threads from `first` on (the others convert the next plane): some do two items
+    if (tid < first) return;
+    int t0 = tid - first, step = nthr - first;
+#else
+    int t0 = tid - first, step = nthr;
     if (t0 < 0) t0 += nthr;
+#endif
     // one item = the y face and the z face of slot (v, s): 432 items, one
     // round on 512 threads, two independent chains per thread
-    for (int it = t0; it < NF * NYF; it += nthr)
+    for (int it = t0; it < NF * NYF; it += step)
 #pragma unroll
     for (int zf = 0; zf < 2; zf++) {
       int v = it / NYF, s = it % NYF;  // NYF == NZF
