@@ -623,6 +623,43 @@ struct Stage {
     for (int it = tid; it < ntot; it += nthr) {
       int ip, py, pz, qy, qz, l, ax0, nax, stride;
       double* dst;
+#ifdef OMB_P4_ORDER
+      // bank-free order: 8 x 8 blocks as half-warps of (8 z of row y, row y + 4) -- the lo/hi slot
+      // pitch 10 puts them 8 doubles apart mod 16 -- then the rows / columns left over
+      if (it < 64 || (it >= 128 && it < 136)) {  // y-face centre (y in [2,10], z in [3,10])
+        py = it < 64 ? 2 + (it >> 4) + 4 * ((it >> 3) & 1) : 10;
+        pz = 3 + (it & 7);
+        int sy = (py - 2) * 8 + (pz - 3);
+        ip = 0; l = 1; qy = py + 1; qz = pz;
+        ax0 = 1; nax = 1; dst = S + Smem::IPCY + sy; stride = NYF;
+      } else if (it < 144) {  // z-face centre (y in [3,10], z in [2,10])
+        int r = it - 64;
+        if (it < 128) { py = 3 + (r >> 4) + 4 * ((r >> 3) & 1); pz = 2 + (r & 7); }
+        else { py = 3 + (it - 136); pz = 10; }
+        int s2 = (py - 3) * 9 + (pz - 2);
+        ip = 1; l = 2; qy = py; qz = pz + 1;
+        ax0 = 2; nax = 1; dst = S + Smem::IPCZ + s2; stride = NZF;
+      } else {  // edge points: each (axis k, line li) group's 8 x 8 block, then the 4 x 17 left
+        int j = it - 144, grp, a, b;
+        if (j < 256) {
+          grp = j >> 6;
+          int r = j & 63;
+          a = 2 + (r >> 4) + 4 * ((r >> 3) & 1);
+          b = 2 + (r & 7);
+        } else {
+          grp = (j - 256) / 17;
+          int r = (j - 256) % 17;
+          a = r < 9 ? 10 : 2 + (r - 9);
+          b = r < 9 ? 2 + r : 10;
+        }
+        int k = grp >> 1, li = grp & 1, c = (a - 2) * 9 + (b - 2);
+        l = li == 0 ? 7 : 8;
+        ip = li + 2;
+        py = a; pz = li == 0 ? b : b + 1;
+        qy = py + 1; qz = pz + ldz(l);
+        ax0 = 1 + k; nax = 1; dst = S + Smem::IPR + ((li * 2 + k) * NF) * NCOR + c; stride = NCOR;
+      }
+#else
       if (it < NYF) {  // y-face centre: line 1, axis y
         ip = 0; l = 1; py = 2 + it / 8; pz = 3 + it % 8; qy = py + 1; qz = pz;
         ax0 = 1; nax = 1; dst = S + Smem::IPCY + it; stride = NYF;
@@ -639,6 +676,7 @@ struct Stage {
         qy = py + 1; qz = pz + ldz(l);
         ax0 = 1 + k; nax = 1; dst = S + Smem::IPR + ((li * 2 + k) * NF) * NCOR + c; stride = NCOR;
       }
+#endif
       KtState sP, sQ;
       lhi_state(ip, 1, py, pz, sP);
       lhi_state(ip, 0, qy, qz, sQ);
