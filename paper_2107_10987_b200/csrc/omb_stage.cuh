@@ -694,14 +694,10 @@ struct Stage {
   OMB_HD void faces_yz(int tid, int nthr, int first = 0) {
     bool fin = interior(X - 1), start = interior(X);
     bool q = A.quad;
-#ifdef OMB_FACES_SPLIT
-    // only the threads from `first` on (the others convert the next plane): some do two items
-    if (tid < first) return;
-    int t0 = tid - first, step = nthr - first;
-#else
+    // (threads below `first` take the last items: tried instead, only threads from `first` on
+    // with two items on some -- 3 % slower, profiles/r02/ab8_faces_split.txt)
     int t0 = tid - first, step = nthr;
     if (t0 < 0) t0 += nthr;
-#endif
     // one item = the y face and the z face of slot (v, s): 432 items, one
     // round on 512 threads, two independent chains per thread
     for (int it = t0; it < NF * NYF; it += step)
