@@ -542,9 +542,28 @@ struct Stage {
     double* FXc = S + Smem::FX + (X % 3) * NF * NFACEX;
     int ntot = A.quad ? NF * NYF : NF * NFACEX;
     for (int it = tid; it < ntot; it += nthr) {
+#ifdef OMB_P2_ORDER
+      // per field: the 64 x-faces / y / z boundary edges of 8 x 8 blocks as paired-row half-warps
+      // (bank-free through the pitch-10 point-flux slots), the 8 leftover edges of each after
+      int v, r, yb, zb, yc, zc, f = NFACEX;
+      if (it < NF * NFACEX) {
+        v = it >> 6;
+        r = it & 63;
+        int yy = (r >> 4) + 4 * ((r >> 3) & 1), zz = r & 7;
+        f = (yy) * 8 + zz;  // x-face (3 + yy, 3 + zz)
+        yb = 2 + yy; zb = 3 + zz; yc = 3 + yy; zc = 2 + zz;
+      } else {
+        v = (it - NF * NFACEX) >> 3;
+        r = (it - NF * NFACEX) & 7;
+        yb = 10; zb = 3 + r; yc = 3 + r; zc = 10;
+      }
+      if (f < NFACEX) {
+        int y = 3 + f / 8, z = 3 + f % 8;
+#else
       int v = A.quad ? it / NYF : it / NFACEX, f = A.quad ? it % NYF : it % NFACEX;
       if (f < NFACEX) {
         int y = 3 + f / 8, z = 3 + f % 8;
+#endif
         double C = rawA(0, 0, v, y, z);
         FXc[v * NFACEX + f] = C;
         if (!A.quad) {
@@ -558,11 +577,16 @@ struct Stage {
         }
       }
       if (A.quad) {  // f < NYF == NZF
+#ifdef OMB_P2_ORDER
+        S[Smem::BYE + v * NYF + yslot(yb, zb)] = edge_acc(rawA(3, 1, v, yb, zb), rawA(4, 1, v, yb + 1, zb));
+        S[Smem::BZE + v * NZF + zslot(yc, zc)] = edge_acc(rawA(5, 2, v, yc, zc), rawA(6, 2, v, yc, zc + 1));
+#else
         int y = 2 + f / 8, z = 3 + f % 8;
         S[Smem::BYE + v * NYF + f] = edge_acc(rawA(3, 1, v, y, z), rawA(4, 1, v, y + 1, z));
         y = 3 + f / 9;
         z = 2 + f % 9;
         S[Smem::BZE + v * NZF + f] = edge_acc(rawA(5, 2, v, y, z), rawA(6, 2, v, y, z + 1));
+#endif
       }
     }
   }
@@ -573,9 +597,27 @@ struct Stage {
   OMB_HD void combine_B(int tid, int nthr) {
     double* FXc = S + Smem::FX + (X % 3) * NF * NFACEX;
     for (int it = tid; it < NF * NCOR; it += nthr) {
+#ifdef OMB_P2_ORDER
+      // per field: the x-faces and an 8 x 8 block of corners as paired-row half-warps, then the
+      // 17 corners left (a = 10 or b = 10)
+      int v, c, f = NFACEX;
+      if (it < NF * NFACEX) {
+        v = it >> 6;
+        int r = it & 63, yy = (r >> 4) + 4 * ((r >> 3) & 1), zz = r & 7;
+        f = yy * 8 + zz;
+        c = yy * 9 + zz;  // corner (2 + yy, 2 + zz)
+      } else {
+        v = (it - NF * NFACEX) / 17;
+        int r = (it - NF * NFACEX) % 17;
+        c = r < 9 ? 8 * 9 + r : (r - 9) * 9 + 8;
+      }
+      if (f < NFACEX) {
+        int y = 3 + f / 8, z = 3 + f % 8;
+#else
       int v = it / NCOR, c = it % NCOR;
       if (c < NFACEX) {
         int f = c, y = 3 + f / 8, z = 3 + f % 8;
+#endif
         double C = FXc[v * NFACEX + f];
         double edev = S[Smem::EDEV + v * NFACEX + f];
         double vdev = (pdev_vert(vertex(0, v, y - 1, z - 1), C) + pdev_vert(vertex(0, v, y - 1, z), C)) +
