@@ -542,7 +542,6 @@ struct Stage {
     double* FXc = S + Smem::FX + (X % 3) * NF * NFACEX;
     int ntot = A.quad ? NF * NYF : NF * NFACEX;
     for (int it = tid; it < ntot; it += nthr) {
-#ifdef OMB_P2_ORDER
       // per field: the 64 x-faces / y / z boundary edges of 8 x 8 blocks as paired-row half-warps
       // (bank-free through the pitch-10 point-flux slots), the 8 leftover edges of each after
       int v, r, yb, zb, yc, zc, f = NFACEX;
@@ -559,11 +558,6 @@ struct Stage {
       }
       if (f < NFACEX) {
         int y = 3 + f / 8, z = 3 + f % 8;
-#else
-      int v = A.quad ? it / NYF : it / NFACEX, f = A.quad ? it % NYF : it % NFACEX;
-      if (f < NFACEX) {
-        int y = 3 + f / 8, z = 3 + f % 8;
-#endif
         double C = rawA(0, 0, v, y, z);
         FXc[v * NFACEX + f] = C;
         if (!A.quad) {
@@ -577,16 +571,8 @@ struct Stage {
         }
       }
       if (A.quad) {  // f < NYF == NZF
-#ifdef OMB_P2_ORDER
         S[Smem::BYE + v * NYF + yslot(yb, zb)] = edge_acc(rawA(3, 1, v, yb, zb), rawA(4, 1, v, yb + 1, zb));
         S[Smem::BZE + v * NZF + zslot(yc, zc)] = edge_acc(rawA(5, 2, v, yc, zc), rawA(6, 2, v, yc, zc + 1));
-#else
-        int y = 2 + f / 8, z = 3 + f % 8;
-        S[Smem::BYE + v * NYF + f] = edge_acc(rawA(3, 1, v, y, z), rawA(4, 1, v, y + 1, z));
-        y = 3 + f / 9;
-        z = 2 + f % 9;
-        S[Smem::BZE + v * NZF + f] = edge_acc(rawA(5, 2, v, y, z), rawA(6, 2, v, y, z + 1));
-#endif
       }
     }
   }
@@ -597,7 +583,6 @@ struct Stage {
   OMB_HD void combine_B(int tid, int nthr) {
     double* FXc = S + Smem::FX + (X % 3) * NF * NFACEX;
     for (int it = tid; it < NF * NCOR; it += nthr) {
-#ifdef OMB_P2_ORDER
       // per field: the x-faces and an 8 x 8 block of corners as paired-row half-warps, then the
       // 17 corners left (a = 10 or b = 10)
       int v, c, f = NFACEX;
@@ -613,11 +598,6 @@ struct Stage {
       }
       if (f < NFACEX) {
         int y = 3 + f / 8, z = 3 + f % 8;
-#else
-      int v = it / NCOR, c = it % NCOR;
-      if (c < NFACEX) {
-        int f = c, y = 3 + f / 8, z = 3 + f % 8;
-#endif
         double C = FXc[v * NFACEX + f];
         double edev = S[Smem::EDEV + v * NFACEX + f];
         double vdev = (pdev_vert(vertex(0, v, y - 1, z - 1), C) + pdev_vert(vertex(0, v, y - 1, z), C)) +
@@ -665,7 +645,6 @@ struct Stage {
     for (int it = tid; it < ntot; it += nthr) {
       int ip, py, pz, qy, qz, l, ax0, nax, stride;
       double* dst;
-#ifdef OMB_P4_ORDER
       // bank-free order: 8 x 8 blocks as half-warps of (8 z of row y, row y + 4) -- the lo/hi slot
       // pitch 10 puts them 8 doubles apart mod 16 -- then the rows / columns left over
       if (it < 64 || (it >= 128 && it < 136)) {  // y-face centre (y in [2,10], z in [3,10])
@@ -701,24 +680,6 @@ struct Stage {
         qy = py + 1; qz = pz + ldz(l);
         ax0 = 1 + k; nax = 1; dst = S + Smem::IPR + ((li * 2 + k) * NF) * NCOR + c; stride = NCOR;
       }
-#else
-      if (it < NYF) {  // y-face centre: line 1, axis y
-        ip = 0; l = 1; py = 2 + it / 8; pz = 3 + it % 8; qy = py + 1; qz = pz;
-        ax0 = 1; nax = 1; dst = S + Smem::IPCY + it; stride = NYF;
-      } else if (it < NYF + NZF) {  // z-face centre: line 2, axis z
-        int s2 = it - NYF;
-        ip = 1; l = 2; py = 3 + s2 / 9; pz = 2 + s2 % 9; qy = py; qz = pz + 1;
-        ax0 = 2; nax = 1; dst = S + Smem::IPCZ + s2; stride = NZF;
-      } else {  // edge point (a+1/2, b+1/2) of lines 7 / 8, axis y (k = 0) or z (k = 1)
-        int j = it - NYF - NZF, k = j / (2 * NCOR), jj = j % (2 * NCOR);
-        int li = jj / NCOR, c = jj % NCOR, a = 2 + c / 9, b = 2 + c % 9;
-        l = li == 0 ? 7 : 8;
-        ip = li + 2;
-        py = a; pz = li == 0 ? b : b + 1;
-        qy = py + 1; qz = pz + ldz(l);
-        ax0 = 1 + k; nax = 1; dst = S + Smem::IPR + ((li * 2 + k) * NF) * NCOR + c; stride = NCOR;
-      }
-#endif
       KtState sP, sQ;
       lhi_state(ip, 1, py, pz, sP);
       lhi_state(ip, 0, qy, qz, sQ);
