@@ -549,7 +549,7 @@ struct Stage {
         v = it >> 6;
         r = it & 63;
         int yy = (r >> 4) + 4 * ((r >> 3) & 1), zz = r & 7;
-        f = (yy) * 8 + zz;  // x-face (3 + yy, 3 + zz)
+        f = yy * 8 + zz;  // x-face (3 + yy, 3 + zz)
         yb = 2 + yy; zb = 3 + zz; yc = 3 + yy; zc = 2 + zz;
       } else {
         v = (it - NF * NFACEX) >> 3;
@@ -570,7 +570,7 @@ struct Stage {
           S[Smem::EDEV + v * NFACEX + f] = (pdev_edge(e0, C) + pdev_edge(e1, C)) + (pdev_edge(e2, C) + pdev_edge(e3, C));
         }
       }
-      if (A.quad) {  // f < NYF == NZF
+      if (A.quad) {  // y-edge point (yb, zb) of y faces, z-edge point (yc, zc) of z faces
         S[Smem::BYE + v * NYF + yslot(yb, zb)] = edge_acc(rawA(3, 1, v, yb, zb), rawA(4, 1, v, yb + 1, zb));
         S[Smem::BZE + v * NZF + zslot(yc, zc)] = edge_acc(rawA(5, 2, v, yc, zc), rawA(6, 2, v, yc, zc + 1));
       }
