@@ -369,11 +369,6 @@ class LeafBatch:
         if ptrs is not None and U.flags.c_contiguous:
             lib.omb_host_pack(ptrs.ctypes.data, self.L, 8, self.fstride, U.ctypes.data)
             return U
-        if self.blocks is not None:  # 16^3 / 32^3 leaves: all blocks of a leaf at once
-            from .blocks import pack
-
-            pack(self.blocks, U)
-            return U
         for i, lf in enumerate(self.leaves):
             U[:, i] = lf.subgrid.interior
         return U
@@ -383,11 +378,6 @@ class LeafBatch:
         ptrs = self._leaf_ptrs(self.ncompute) if lib is not None else None
         if ptrs is not None and U.flags.c_contiguous and self.ncompute == self.L:
             lib.omb_host_unpack(U.ctypes.data, self.L, 8, self.fstride, ptrs.ctypes.data)
-            return
-        if self.blocks is not None:
-            from .blocks import unpack
-
-            unpack(self.blocks, U)
             return
         for i, lf in enumerate(self.leaves[:self.ncompute]):
             lf.subgrid.interior[:] = U[:, i]

@@ -54,8 +54,8 @@ class BlockSubGrid:
         self.interior = parent.interior[:, s[0], s[1], s[2]]
 
     @property
-    def u(self):  # no padded array of its own: the fast host transfer paths fall back to views
-        return None
+    def u(self):  # no padded array of its own: host transfers go through the interior views
+        return None                       # (numpy; a leaf-at-once fancy-index gather was slower)
 
 
 class Block:
@@ -92,12 +92,9 @@ class BlockTree:
         self.lower = tree.lower
         bs = [(x, y, z) for x in range(self.nb) for y in range(self.nb) for z in range(self.nb)]
         self._blocks = []
-        self.parent_leaves = tree.sorted_leaves()
-        for lf in self.parent_leaves:
+        for lf in tree.sorted_leaves():
             blk = sorted((Block(lf, b, self.extra) for b in bs), key=lambda k: k.path)
             self._blocks += blk
-        # block index -> (bx, by, bz) inside a leaf, in the batch order (the same for every leaf)
-        self.order = np.array([bk.b for bk in self._blocks[:self.nb ** 3]], dtype=np.int64).T
         self._at = {(bk.level, *map(int, bk.ipos)): bk for bk in self._blocks}
 
     def leaves(self):
@@ -121,19 +118,3 @@ class BlockTree:
             return None
         return pos
 
-
-def pack(bt, U):
-    """The leaves' interiors into the batch layout U [6][L][8][8][8], a leaf's nb^3 blocks at once."""
-    nb, B = bt.nb, bt.nb ** 3
-    bx, by, bz = bt.order
-    for j, lf in enumerate(bt.parent_leaves):
-        a = lf.subgrid.interior.reshape(6, nb, 8, nb, 8, nb, 8)
-        U[:, j * B:(j + 1) * B] = a[:, bx, :, by, :, bz, :].transpose(1, 0, 2, 3, 4)
-
-
-def unpack(bt, U):
-    nb, B = bt.nb, bt.nb ** 3
-    bx, by, bz = bt.order
-    for j, lf in enumerate(bt.parent_leaves):
-        a = lf.subgrid.interior.reshape(6, nb, 8, nb, 8, nb, 8)
-        a[:, bx, :, by, :, bz, :] = U[:, j * B:(j + 1) * B].transpose(1, 0, 2, 3, 4)
