@@ -250,6 +250,14 @@ OMB_HD void gather_cell(const double* U, long long fstride, const LeafInfo& LI, 
 
 // values a thread carries across the barrier after P1 (<= 2 items per
 // thread: P1 has <= 500 items and the kernel runs >= 256 threads)
+// rounds of the reconstruction phases: the CUDA kernel runs 512 threads, so each thread takes at
+// most one item of P1A (500), P1B (400) and P3 (400) -- the second round exists only for the host
+// emulation's smaller thread counts
+#if defined(__CUDA_ARCH__) && defined(OMB_ONE_ROUND)
+constexpr int ROUNDS_P1 = 1;
+#else
+constexpr int ROUNDS_P1 = 2;
+#endif
 struct Hold {
   double h0[NF], h1[NF];
   int s0, s1;
@@ -476,7 +484,7 @@ struct Stage {
     int nitems = g == 0 ? (A.new_mode ? OMB_ITEMS_P1A_NEW_N : OMB_ITEMS_P1A_OLD_N) : OMB_ITEMS_P1B_NEW_N;
     h.s0 = h.s1 = -1;
 #pragma unroll 1
-    for (int k = 0; k < 2; k++) {
+    for (int k = 0; k < ROUNDS_P1; k++) {
       int it = tid + k * nthr;
       if (it >= nitems) break;
       unsigned e = item_entry(toff, it);
@@ -616,7 +624,8 @@ struct Stage {
   OMB_HD void inplane_lines(int tid, int nthr) {
     int toff = A.new_mode ? OMB_ITEMS_P3_NEW_OFF : OMB_ITEMS_P3_OLD_OFF;
     int nitems = A.new_mode ? OMB_ITEMS_P3_NEW_N : OMB_ITEMS_P3_OLD_N;
-    for (int it = tid; it < nitems; it += nthr) {
+#pragma unroll 1
+    for (int it = tid; it < nitems && it < tid + ROUNDS_P1 * nthr; it += nthr) {
       unsigned e = item_entry(toff, it);
       int pos = e & 127, ip = (e >> 7) & 15, l = ip_line(ip);
       int y = 2 + pos / 10, z = 2 + pos % 10;

@@ -44,7 +44,7 @@ static int g_order = 0;
 extern "C" void emu_set_order(int mode) { g_order = mode; }
 
 extern "C" int emu_stage(const OmbStageDesc* d, int nthr) {
-  if (nthr < 2 * NFACEX) return -1;  // the phase layout needs >= 128 threads
+  if (nthr < 256) return -1;  // the phase layout: >= 128 threads; two rounds of <= 500 items: >= 250
   StageArgs A;
   A.ucur = d->ucur; A.u0 = d->u0; A.unext = d->unext; A.grav = d->grav; A.fstride = d->fstride;
   A.info = (const LeafInfo*)d->info; A.run_off = d->run_off; A.run_leaf = d->run_leaf; A.dt = d->dt;
