@@ -252,8 +252,9 @@ OMB_HD void gather_cell(const double* U, long long fstride, const LeafInfo& LI, 
 // thread: P1 has <= 500 items and the kernel runs >= 256 threads)
 // rounds of the reconstruction phases: the CUDA kernel runs 512 threads, so each thread takes at
 // most one item of P1A (500), P1B (400) and P3 (400) -- the second round exists only for the host
-// emulation's smaller thread counts
-#if defined(__CUDA_ARCH__) && defined(OMB_ONE_ROUND)
+// emulation's smaller thread counts.  (Compiling the second round into the kernel cost 12 B of
+// spills and 4-5 %: profiles/r02/ab11_one_round.txt.)
+#if defined(__CUDA_ARCH__)
 constexpr int ROUNDS_P1 = 1;
 #else
 constexpr int ROUNDS_P1 = 2;
