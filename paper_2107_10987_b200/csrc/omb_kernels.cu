@@ -287,6 +287,7 @@ __global__ void __launch_bounds__(NT, 1) k_stage(StageArgs A) {
   st.fb = 0;
   st.bind_run_info();
   st.stage_run_info(tid, nthr);
+  st.load_items(tid);
   __syncthreads();
   Hold h;
   const int R = st.R;

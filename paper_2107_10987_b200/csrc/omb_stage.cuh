@@ -275,6 +275,22 @@ struct Stage {
   // thread-carried reductions
   double amax;
   long long fb;
+#ifdef OMB_PRELOAD_ITEMS
+  // this thread's item of P1A / P1B / P3 (the same every plane), loaded once per CTA
+  unsigned item_p1a, item_p1b, item_p3;
+#endif
+
+  OMB_HD void load_items(int tid) {
+#ifdef OMB_PRELOAD_ITEMS
+    int na = A.new_mode ? OMB_ITEMS_P1A_NEW_N : OMB_ITEMS_P1A_OLD_N;
+    int oa = A.new_mode ? OMB_ITEMS_P1A_NEW_OFF : OMB_ITEMS_P1A_OLD_OFF;
+    int n3 = A.new_mode ? OMB_ITEMS_P3_NEW_N : OMB_ITEMS_P3_OLD_N;
+    int o3 = A.new_mode ? OMB_ITEMS_P3_NEW_OFF : OMB_ITEMS_P3_OLD_OFF;
+    item_p1a = tid < na ? item_entry(oa, tid) : 0u;
+    item_p1b = tid < OMB_ITEMS_P1B_NEW_N ? item_entry(OMB_ITEMS_P1B_NEW_OFF, tid) : 0u;
+    item_p3 = tid < n3 ? item_entry(o3, tid) : 0u;
+#endif
+  }
 
   OMB_HD double& sm(int off) { return S[off]; }
   OMB_HD double* prp(int x, int v) { return S + Smem::PR + ((x % 5) * NF + v) * PL; }
@@ -488,7 +504,11 @@ struct Stage {
     for (int k = 0; k < ROUNDS_P1; k++) {
       int it = tid + k * nthr;
       if (it >= nitems) break;
+#ifdef OMB_PRELOAD_ITEMS
+      unsigned e = k == 0 ? (g == 0 ? item_p1a : item_p1b) : item_entry(toff, it);
+#else
       unsigned e = item_entry(toff, it);
+#endif
       int pos = e & 127, dl = dl0 + ((e >> 7) & 15);
       int l = dl_line(dl);
       int y = 2 + pos / 10, z = 2 + pos % 10;
@@ -627,7 +647,11 @@ struct Stage {
     int nitems = A.new_mode ? OMB_ITEMS_P3_NEW_N : OMB_ITEMS_P3_OLD_N;
 #pragma unroll 1
     for (int it = tid; it < nitems && it < tid + ROUNDS_P1 * nthr; it += nthr) {
+#ifdef OMB_PRELOAD_ITEMS
+      unsigned e = it == tid ? item_p3 : item_entry(toff, it);
+#else
       unsigned e = item_entry(toff, it);
+#endif
       int pos = e & 127, ip = (e >> 7) & 15, l = ip_line(ip);
       int y = 2 + pos / 10, z = 2 + pos % 10;
       double lo[NF], hi[NF];

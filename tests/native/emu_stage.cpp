@@ -70,7 +70,7 @@ extern "C" int emu_stage(const OmbStageDesc* d, int nthr) {
     }
     int R = st[0].R;
 #define ALL(stmt) for (int k_ = 0; k_ < nthr; k_++) { int t = order[k_]; g_tid = t; Stage& s = st[t]; (void)s; stmt; }
-    ALL(s.bind_run_info(); s.stage_run_info(t, nthr));
+    ALL(s.bind_run_info(); s.stage_run_info(t, nthr); s.load_items(t));
     // the phase sequence of k_stage (omb_kernels.cu), one ALL() per barrier interval,
     // with its cp.async commits and waits at the same points
     ALL(for (int X = 0; X < 4; X++) s.prefetch_plane(X, t, nthr, Smem::RAW + X * NF * PL);
