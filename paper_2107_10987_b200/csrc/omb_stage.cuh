@@ -434,6 +434,48 @@ struct Stage {
 #pragma unroll
     for (int k = 0; k < 5; k++) ad[k] = (dx ? ring[k] : ring[2]) + c0 + (k - 2) * dd;
     double rr[5] = {0, 0, 0, 0, 0}, pm1 = 0, pp1 = 0;
+#ifdef OMB_MONO_TRIPLES
+    // three fields at a time -- (rho, p, vx), (vy, vz, tau) -- one flat shortcut per triple
+#pragma unroll
+    for (int ti = 0; ti < 2; ti++) {
+      const int v0 = ti == 0 ? 0 : 2, v1 = ti == 0 ? 4 : 3, v2 = ti == 0 ? 1 : 5;
+      if (!full && ti > 0) {
+        lo[v0] = hi[v0] = lo[v1] = hi[v1] = lo[v2] = hi[v2] = 0.0;
+        continue;
+      }
+      double sa[5], sb[5], sc[5];
+#pragma unroll
+      for (int k = 0; k < 5; k++) {
+        sa[k] = S[ad[k] + v0 * PL];
+        sb[k] = S[ad[k] + v1 * PL];
+        sc[k] = S[ad[k] + v2 * PL];
+      }
+      bool fa = sa[0] == sa[2] && sa[1] == sa[2] && sa[3] == sa[2] && sa[4] == sa[2];
+      bool fb = sb[0] == sb[2] && sb[1] == sb[2] && sb[3] == sb[2] && sb[4] == sb[2];
+      bool fc = sc[0] == sc[2] && sc[1] == sc[2] && sc[3] == sc[2] && sc[4] == sc[2];
+      if (fa && fb && fc) {
+        lo[v0] = hi[v0] = sa[2];
+        lo[v1] = hi[v1] = sb[2];
+        lo[v2] = hi[v2] = sc[2];
+      } else {
+        double la = iface(sa[0], sa[1], sa[2], sa[3]), ha = iface(sa[1], sa[2], sa[3], sa[4]);
+        double lb = iface(sb[0], sb[1], sb[2], sb[3]), hb = iface(sb[1], sb[2], sb[3], sb[4]);
+        double lc = iface(sc[0], sc[1], sc[2], sc[3]), hc = iface(sc[1], sc[2], sc[3], sc[4]);
+        mono(sa[2], la, ha);
+        mono(sb[2], lb, hb);
+        mono(sc[2], lc, hc);
+        lo[v0] = la; hi[v0] = ha;
+        lo[v1] = lb; hi[v1] = hb;
+        lo[v2] = lc; hi[v2] = hc;
+      }
+      if (ti == 0) {
+#pragma unroll
+        for (int k = 0; k < 5; k++) rr[k] = sa[k];
+        pm1 = sb[1];
+        pp1 = sb[3];
+      }
+    }
+#else
     // two fields at a time -- (rho, p), (vx, vy), (vz, tau): their loads and interface values
     // straight-line, so the two chains interleave; the flat shortcut per pair (A/B on one box:
     // c3 +1.4 %, c2 -0.3 %; with select-based monotonisation too: c3 +1.3 %, c2 -2.5 %)
@@ -472,6 +514,7 @@ struct Stage {
         pp1 = sb[3];
       }
     }
+#endif
     if (A.contact) contact_steepen(rr, pm1, pp1, A.gamma, lo[0], hi[0]);
     if (lo[0] <= 0.0 || lo[4] <= 0.0) {
       fb += mult(X, ad[2] - ring[2]);
