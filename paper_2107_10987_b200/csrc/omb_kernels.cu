@@ -272,7 +272,7 @@ __device__ unsigned long long g_phase_cycles[16];
 template <int NT, int SC>
 __global__ void __launch_bounds__(NT, 1) k_stage(StageArgs A) {
   static_assert(NT >= 2 * NFACEX, "P6 runs on the last 64 threads of the last P1 group");
-  static_assert(ROUNDS_P1 == 2 || NT >= OMB_ITEMS_P1A_NEW_N, "one round of reconstruction items needs >= 500 threads");
+  static_assert(ITEM_ROUNDS == 2 || NT >= OMB_ITEMS_P1A_NEW_N, "one round of reconstruction items needs >= 500 threads");
   extern __shared__ double S[];
   const int tid = threadIdx.x, nthr = blockDim.x;
   Stage st;

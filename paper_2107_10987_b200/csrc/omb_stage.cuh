@@ -182,6 +182,15 @@ constexpr int FXO = 0, FYO = NF * 9 * 64, FZO = 2 * NF * 9 * 64;
 
 static_assert(sizeof(LeafInfo) == 20 * 8, "LeafInfo is 160 bytes (Smem::LINFO)");
 
+// item rounds of every phase: the CUDA kernel runs 512 threads and no phase has more than 500
+// items, so each thread takes at most one -- the second round exists only for the host emulation's
+// smaller thread counts (256, 384).  (Compiling the second round into the kernel cost 12 B of
+// spills and 4-5 %: profiles/r02/ab11_one_round.txt.)
+#if defined(__CUDA_ARCH__)
+constexpr int ITEM_ROUNDS = 1;
+#else
+constexpr int ITEM_ROUNDS = 2;
+#endif
 struct StageArgs {
   const double* ucur;   // [6][L][512] stage input (halo source)
   const double* u0;     // [6][L][512] RK3 u0 snapshot
@@ -250,15 +259,6 @@ OMB_HD void gather_cell(const double* U, long long fstride, const LeafInfo& LI, 
 
 // values a thread carries across the barrier after P1 (<= 2 items per
 // thread: P1 has <= 500 items and the kernel runs >= 256 threads)
-// rounds of the reconstruction phases: the CUDA kernel runs 512 threads, so each thread takes at
-// most one item of P1A (500), P1B (400) and P3 (400) -- the second round exists only for the host
-// emulation's smaller thread counts.  (Compiling the second round into the kernel cost 12 B of
-// spills and 4-5 %: profiles/r02/ab11_one_round.txt.)
-#if defined(__CUDA_ARCH__)
-constexpr int ROUNDS_P1 = 1;
-#else
-constexpr int ROUNDS_P1 = 2;
-#endif
 struct Hold {
   double h0[NF], h1[NF];
   int s0, s1;
@@ -434,48 +434,6 @@ struct Stage {
 #pragma unroll
     for (int k = 0; k < 5; k++) ad[k] = (dx ? ring[k] : ring[2]) + c0 + (k - 2) * dd;
     double rr[5] = {0, 0, 0, 0, 0}, pm1 = 0, pp1 = 0;
-#ifdef OMB_MONO_TRIPLES
-    // three fields at a time -- (rho, p, vx), (vy, vz, tau) -- one flat shortcut per triple
-#pragma unroll
-    for (int ti = 0; ti < 2; ti++) {
-      const int v0 = ti == 0 ? 0 : 2, v1 = ti == 0 ? 4 : 3, v2 = ti == 0 ? 1 : 5;
-      if (!full && ti > 0) {
-        lo[v0] = hi[v0] = lo[v1] = hi[v1] = lo[v2] = hi[v2] = 0.0;
-        continue;
-      }
-      double sa[5], sb[5], sc[5];
-#pragma unroll
-      for (int k = 0; k < 5; k++) {
-        sa[k] = S[ad[k] + v0 * PL];
-        sb[k] = S[ad[k] + v1 * PL];
-        sc[k] = S[ad[k] + v2 * PL];
-      }
-      bool fa = sa[0] == sa[2] && sa[1] == sa[2] && sa[3] == sa[2] && sa[4] == sa[2];
-      bool fb = sb[0] == sb[2] && sb[1] == sb[2] && sb[3] == sb[2] && sb[4] == sb[2];
-      bool fc = sc[0] == sc[2] && sc[1] == sc[2] && sc[3] == sc[2] && sc[4] == sc[2];
-      if (fa && fb && fc) {
-        lo[v0] = hi[v0] = sa[2];
-        lo[v1] = hi[v1] = sb[2];
-        lo[v2] = hi[v2] = sc[2];
-      } else {
-        double la = iface(sa[0], sa[1], sa[2], sa[3]), ha = iface(sa[1], sa[2], sa[3], sa[4]);
-        double lb = iface(sb[0], sb[1], sb[2], sb[3]), hb = iface(sb[1], sb[2], sb[3], sb[4]);
-        double lc = iface(sc[0], sc[1], sc[2], sc[3]), hc = iface(sc[1], sc[2], sc[3], sc[4]);
-        mono(sa[2], la, ha);
-        mono(sb[2], lb, hb);
-        mono(sc[2], lc, hc);
-        lo[v0] = la; hi[v0] = ha;
-        lo[v1] = lb; hi[v1] = hb;
-        lo[v2] = lc; hi[v2] = hc;
-      }
-      if (ti == 0) {
-#pragma unroll
-        for (int k = 0; k < 5; k++) rr[k] = sa[k];
-        pm1 = sb[1];
-        pp1 = sb[3];
-      }
-    }
-#else
     // two fields at a time -- (rho, p), (vx, vy), (vz, tau): their loads and interface values
     // straight-line, so the two chains interleave; the flat shortcut per pair (A/B on one box:
     // c3 +1.4 %, c2 -0.3 %; with select-based monotonisation too: c3 +1.3 %, c2 -2.5 %)
@@ -514,7 +472,6 @@ struct Stage {
         pp1 = sb[3];
       }
     }
-#endif
     if (A.contact) contact_steepen(rr, pm1, pp1, A.gamma, lo[0], hi[0]);
     if (lo[0] <= 0.0 || lo[4] <= 0.0) {
       fb += mult(X, ad[2] - ring[2]);
@@ -544,7 +501,7 @@ struct Stage {
     int nitems = g == 0 ? (A.new_mode ? OMB_ITEMS_P1A_NEW_N : OMB_ITEMS_P1A_OLD_N) : OMB_ITEMS_P1B_NEW_N;
     h.s0 = h.s1 = -1;
 #pragma unroll 1
-    for (int k = 0; k < ROUNDS_P1; k++) {
+    for (int k = 0; k < ITEM_ROUNDS; k++) {
       int it = tid + k * nthr;
       if (it >= nitems) break;
 #ifdef OMB_PRELOAD_ITEMS
@@ -613,7 +570,7 @@ struct Stage {
   OMB_HD void combine_A(int tid, int nthr) {
     double* FXc = S + Smem::FX + (X % 3) * NF * NFACEX;
     int ntot = A.quad ? NF * NYF : NF * NFACEX;
-    for (int it = tid; it < ntot; it += nthr) {
+    for (int it = tid; it < ntot && it < tid + ITEM_ROUNDS * nthr; it += nthr) {
       // per field: the 64 x-faces / y / z boundary edges of 8 x 8 blocks as paired-row half-warps
       // (bank-free through the pitch-10 point-flux slots), the 8 leftover edges of each after
       int v, r, yb, zb, yc, zc, f = NFACEX;
@@ -654,7 +611,7 @@ struct Stage {
   // (corners < 64) the final x face -- 486 items, one round.
   OMB_HD void combine_B(int tid, int nthr) {
     double* FXc = S + Smem::FX + (X % 3) * NF * NFACEX;
-    for (int it = tid; it < NF * NCOR; it += nthr) {
+    for (int it = tid; it < NF * NCOR && it < tid + ITEM_ROUNDS * nthr; it += nthr) {
       // per field: the x-faces and an 8 x 8 block of corners as paired-row half-warps, then the
       // 17 corners left (a = 10 or b = 10)
       int v, c, f = NFACEX;
@@ -689,7 +646,7 @@ struct Stage {
     int toff = A.new_mode ? OMB_ITEMS_P3_NEW_OFF : OMB_ITEMS_P3_OLD_OFF;
     int nitems = A.new_mode ? OMB_ITEMS_P3_NEW_N : OMB_ITEMS_P3_OLD_N;
 #pragma unroll 1
-    for (int it = tid; it < nitems && it < tid + ROUNDS_P1 * nthr; it += nthr) {
+    for (int it = tid; it < nitems && it < tid + ITEM_ROUNDS * nthr; it += nthr) {
 #ifdef OMB_PRELOAD_ITEMS
       unsigned e = it == tid ? item_p3 : item_entry(toff, it);
 #else
@@ -719,7 +676,7 @@ struct Stage {
   // states): 468 single-axis items, one round on 512 threads.
   OMB_HD void inplane_fluxes(int tid, int nthr) {
     int ntot = NYF + NZF + (A.quad ? 4 * NCOR : 0);
-    for (int it = tid; it < ntot; it += nthr) {
+    for (int it = tid; it < ntot && it < tid + ITEM_ROUNDS * nthr; it += nthr) {
       int ip, py, pz, qy, qz, l, ax0, nax, stride;
       double* dst;
       // bank-free order: 8 x 8 blocks as half-warps of (8 z of row y, row y + 4) -- the lo/hi slot
