@@ -275,13 +275,11 @@ struct Stage {
   // thread-carried reductions
   double amax;
   long long fb;
-#ifdef OMB_PRELOAD_ITEMS
-  // this thread's item of P1A / P1B / P3 (the same every plane), loaded once per CTA
+  // this thread's item of P1A / P1B / P3 (the same every plane), loaded once per CTA: the
+  // per-phase table loads sat at the head of each phase's chain (c3 +2.1 %, ab12_preload.txt)
   unsigned item_p1a, item_p1b, item_p3;
-#endif
 
   OMB_HD void load_items(int tid) {
-#ifdef OMB_PRELOAD_ITEMS
     int na = A.new_mode ? OMB_ITEMS_P1A_NEW_N : OMB_ITEMS_P1A_OLD_N;
     int oa = A.new_mode ? OMB_ITEMS_P1A_NEW_OFF : OMB_ITEMS_P1A_OLD_OFF;
     int n3 = A.new_mode ? OMB_ITEMS_P3_NEW_N : OMB_ITEMS_P3_OLD_N;
@@ -289,7 +287,6 @@ struct Stage {
     item_p1a = tid < na ? item_entry(oa, tid) : 0u;
     item_p1b = tid < OMB_ITEMS_P1B_NEW_N ? item_entry(OMB_ITEMS_P1B_NEW_OFF, tid) : 0u;
     item_p3 = tid < n3 ? item_entry(o3, tid) : 0u;
-#endif
   }
 
   OMB_HD double& sm(int off) { return S[off]; }
@@ -504,11 +501,7 @@ struct Stage {
     for (int k = 0; k < ITEM_ROUNDS; k++) {
       int it = tid + k * nthr;
       if (it >= nitems) break;
-#ifdef OMB_PRELOAD_ITEMS
       unsigned e = k == 0 ? (g == 0 ? item_p1a : item_p1b) : item_entry(toff, it);
-#else
-      unsigned e = item_entry(toff, it);
-#endif
       int pos = e & 127, dl = dl0 + ((e >> 7) & 15);
       int l = dl_line(dl);
       int y = 2 + pos / 10, z = 2 + pos % 10;
@@ -570,7 +563,7 @@ struct Stage {
   OMB_HD void combine_A(int tid, int nthr) {
     double* FXc = S + Smem::FX + (X % 3) * NF * NFACEX;
     int ntot = A.quad ? NF * NYF : NF * NFACEX;
-    for (int it = tid; it < ntot && it < tid + ITEM_ROUNDS * nthr; it += nthr) {
+    for (int it = tid; it < ntot; it += nthr) {
       // per field: the 64 x-faces / y / z boundary edges of 8 x 8 blocks as paired-row half-warps
       // (bank-free through the pitch-10 point-flux slots), the 8 leftover edges of each after
       int v, r, yb, zb, yc, zc, f = NFACEX;
@@ -611,7 +604,7 @@ struct Stage {
   // (corners < 64) the final x face -- 486 items, one round.
   OMB_HD void combine_B(int tid, int nthr) {
     double* FXc = S + Smem::FX + (X % 3) * NF * NFACEX;
-    for (int it = tid; it < NF * NCOR && it < tid + ITEM_ROUNDS * nthr; it += nthr) {
+    for (int it = tid; it < NF * NCOR; it += nthr) {
       // per field: the x-faces and an 8 x 8 block of corners as paired-row half-warps, then the
       // 17 corners left (a = 10 or b = 10)
       int v, c, f = NFACEX;
@@ -647,11 +640,7 @@ struct Stage {
     int nitems = A.new_mode ? OMB_ITEMS_P3_NEW_N : OMB_ITEMS_P3_OLD_N;
 #pragma unroll 1
     for (int it = tid; it < nitems && it < tid + ITEM_ROUNDS * nthr; it += nthr) {
-#ifdef OMB_PRELOAD_ITEMS
       unsigned e = it == tid ? item_p3 : item_entry(toff, it);
-#else
-      unsigned e = item_entry(toff, it);
-#endif
       int pos = e & 127, ip = (e >> 7) & 15, l = ip_line(ip);
       int y = 2 + pos / 10, z = 2 + pos % 10;
       double lo[NF], hi[NF];
@@ -676,7 +665,7 @@ struct Stage {
   // states): 468 single-axis items, one round on 512 threads.
   OMB_HD void inplane_fluxes(int tid, int nthr) {
     int ntot = NYF + NZF + (A.quad ? 4 * NCOR : 0);
-    for (int it = tid; it < ntot && it < tid + ITEM_ROUNDS * nthr; it += nthr) {
+    for (int it = tid; it < ntot; it += nthr) {
       int ip, py, pz, qy, qz, l, ax0, nax, stride;
       double* dst;
       // bank-free order: 8 x 8 blocks as half-warps of (8 z of row y, row y + 4) -- the lo/hi slot
