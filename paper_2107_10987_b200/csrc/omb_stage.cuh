@@ -505,19 +505,6 @@ struct Stage {
       int pos = e & 127, dl = dl0 + ((e >> 7) & 15);
       int l = dl_line(dl);
       int y = 2 + pos / 10, z = 2 + pos % 10;
-#ifdef OMB_PSTATE_FIRST
-      // the previous plane's state needs no reconstruction: its chain (a division and a square
-      // root) starts before this plane's, beside the stencil loads
-      bool kt0 = X >= 3 && (A.quad || l == 0) && ((e >> 12) & 1);
-      KtState sP0;
-      if (kt0) {
-        int pp0 = pos - ldy(l) * 10 - ldz(l);
-        double hp0[NF];
-#pragma unroll
-        for (int v = 0; v < NF; v++) hp0[v] = S[Smem::HI + (dl * NF + v) * NP + pp0];
-        kt_state(hp0, A.gamma, A.gm1, A.inv_gm1, sP0);
-      }
-#endif
       double lo[NF], hi[NF];
       mono6(l, X, y, z, lo, hi, (e >> 11) & 1);
       if (k == 0) {
@@ -537,11 +524,7 @@ struct Stage {
 #pragma unroll
       for (int v = 0; v < NF; v++) hp[v] = S[Smem::HI + (dl * NF + v) * NP + pp];
       KtState sP, sQ;
-#ifdef OMB_PSTATE_FIRST
-      sP = sP0;
-#else
       kt_state(hp, A.gamma, A.gm1, A.inv_gm1, sP);
-#endif
       kt_state(lo, A.gamma, A.gm1, A.inv_gm1, sQ);
       // axes served by this line: x always; y for lines 3,4; z for 5,6; all for 9..12
       int ax_second = (l == 3 || l == 4) ? 1 : 2;
