@@ -39,6 +39,21 @@ OMB_HD int ldx(int l) { return (int)((LDX_BITS >> (2 * l)) & 3u) - 1; }
 OMB_HD int ldy(int l) { return (int)((LDY_BITS >> (2 * l)) & 3u) - 1; }
 OMB_HD int ldz(int l) { return (int)((LDZ_BITS >> (2 * l)) & 3u) - 1; }
 
+#ifdef OMB_NOINLINE_RARE
+// the rarely taken exact operations as out-of-line calls: one copy of their code instead of one per
+// inlined call site (division: CUDA's fast path + its slow-path call; pow: ~150 instructions)
+#ifdef __CUDA_ARCH__
+__device__ __noinline__ double rare_div(double a, double b) { return a / b; }
+__device__ __noinline__ double rare_pow(double x, double y) { return pow_glibc(x, y); }
+#else
+inline double rare_div(double a, double b) { return a / b; }
+inline double rare_pow(double x, double y) { return pow_glibc(x, y); }
+#endif
+#else
+OMB_HD double rare_div(double a, double b) { return a / b; }
+OMB_HD double rare_pow(double x, double y) { return pow_glibc(x, y); }
+#endif
+
 // IEEE a/b that never takes CUDA's division slow path for a zero numerator
 // (CUDA routes 0/b through a called subroutine; zero momenta and zero
 // deviations are everywhere in the Sedov ambient).  For a == 0 the quotient
@@ -92,7 +107,7 @@ OMB_HD double div_by(double a, double b, double y) {
 #ifdef __CUDA_ARCH__
     asm volatile("" : "+d"(aa));  // keep the IEEE division inside this rare branch
 #endif
-    q2 = aa / b;
+    q2 = rare_div(aa, b);
   }
   return q2;
 }
@@ -141,7 +156,7 @@ OMB_HD void mono(double a, double& lv, double& hv) {
     // copy the compiler speculates the IEEE division for every field
     asm volatile("" : "+d"(dd));
 #endif
-    q = dd / 6.0;
+    q = rare_div(dd, 6.0);
   }
   double nlv = lv, nhv = hv;
   if (dm > q) nlv = 3.0 * a - 2.0 * hv;
@@ -277,7 +292,7 @@ OMB_HD void prim_cell(const double* u, double gamma, double gm1, double eta, dou
   double vx = u[1] * inv, vy = u[2] * inv, vz = u[3] * inv;
   double kin = 0.5 * ((u[1] * vx + u[2] * vy) + u[3] * vz);
   double e1 = u[4] - kin;
-  double eint = (e1 >= eta * u[4]) ? e1 : pow_glibc(u[5], gamma);
+  double eint = (e1 >= eta * u[4]) ? e1 : rare_pow(u[5], gamma);
   w[0] = rho;
   w[1] = vx;
   w[2] = vy;
