@@ -214,6 +214,8 @@ class B200FmmSolver:
             return
         import torch
 
+        self._order_cache = {}
+
         _check_balance(tree)
         t = EntityTable(tree)
         self.table = t
@@ -328,14 +330,33 @@ class B200FmmSolver:
         nt = int(sub.numel()) if sub is not None else int(self._targets.numel())
         for part, off, contrib, cc in ((0, self._off, self._contrib, ptr(self._cellcell)),
                                        (1, self._off1, self._contrib1, None)):
+            order = self._target_order(part, off, sub)
             _lib.check(lib.omb_fmm_m2l_part(part, ptr(off), ptr(contrib), ptr(self._D), cc, ptr(self._M),
-                                            ptr(self._L), nt, ptr(self._targets),
-                                            ptr(sub) if sub is not None else None, ptr(self._M0c),
+                                            ptr(self._L), nt, ptr(self._targets), ptr(order), ptr(self._M0c),
                                             self.table.nentities, sh), "omb_fmm_m2l_part")
         for _, par in self._down:
             _lib.check(lib.omb_fmm_downward(ptr(par), int(par.numel()), ptr(self._children), ptr(self._center),
                                             ptr(self._L), sh), "omb_fmm_downward")
         return self._L
+
+    def _target_order(self, part, off, sub):
+        """The M2L threads take their targets longest contribution list first (cached per pass):
+        a warp's 32 targets then have lists of about one length, instead of waiting for the longest
+        of a mixed set.  Each target's own additions keep their order (bitwise the same).
+        OMB_FMM_ORDER=0 keeps the entity order."""
+        import os
+
+        import torch
+
+        if os.environ.get("OMB_FMM_ORDER", "1") == "0":
+            return sub
+        cache = self.__dict__.setdefault("_order_cache", {})
+        key = (part, id(sub))
+        if key not in cache:
+            n = torch.diff(off)
+            idx = sub if sub is not None else torch.arange(n.numel(), device=n.device)
+            cache[key] = idx[torch.argsort(n[idx], descending=True, stable=True)].contiguous()
+        return cache[key]
 
     def fields_device(self, rho_dev, dx3_dev, out4, stream=None):
         """phi, gx, gy, gz per cell into out4 ([4][L][512] device tensor)."""
@@ -377,6 +398,7 @@ class B200FmmSolver:
         cells) and the octree's internal nodes -- everything the downward pass
         to its cells reads; the masses come from all ranks (all_gather).
         Bitwise the single-GPU result for this rank's cells."""
+        self._order_cache = {}
         import torch
 
         if self.theta == 0.0:
