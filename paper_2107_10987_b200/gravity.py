@@ -215,7 +215,6 @@ class B200FmmSolver:
         import torch
 
         self._order_cache = {}
-
         _check_balance(tree)
         t = EntityTable(tree)
         self.table = t
@@ -398,9 +397,9 @@ class B200FmmSolver:
         cells) and the octree's internal nodes -- everything the downward pass
         to its cells reads; the masses come from all ranks (all_gather).
         Bitwise the single-GPU result for this rank's cells."""
-        self._order_cache = {}
         import torch
 
+        self._order_cache = {}
         if self.theta == 0.0:
             raise NotImplementedError("theta = 0 with a partition")
         t = self.table
