@@ -39,16 +39,9 @@ OMB_HD int ldx(int l) { return (int)((LDX_BITS >> (2 * l)) & 3u) - 1; }
 OMB_HD int ldy(int l) { return (int)((LDY_BITS >> (2 * l)) & 3u) - 1; }
 OMB_HD int ldz(int l) { return (int)((LDZ_BITS >> (2 * l)) & 3u) - 1; }
 
-#ifdef OMB_NOINLINE_RARE
-// the rarely taken exact operations as out-of-line calls: one copy of their code instead of one per
-// inlined call site (division: CUDA's fast path + its slow-path call; pow: ~150 instructions)
-#ifdef __CUDA_ARCH__
-__device__ __noinline__ double rare_div(double a, double b) { return a / b; }
-__device__ __noinline__ double rare_pow(double x, double y) { return pow_glibc(x, y); }
-#else
+// the rarely taken exact operations (named so the call sites read as the rare branches they are)
 inline double rare_div(double a, double b) { return a / b; }
 inline double rare_pow(double x, double y) { return pow_glibc(x, y); }
-#endif
 #else
 OMB_HD double rare_div(double a, double b) { return a / b; }
 OMB_HD double rare_pow(double x, double y) { return pow_glibc(x, y); }
