@@ -39,13 +39,10 @@ OMB_HD int ldx(int l) { return (int)((LDX_BITS >> (2 * l)) & 3u) - 1; }
 OMB_HD int ldy(int l) { return (int)((LDY_BITS >> (2 * l)) & 3u) - 1; }
 OMB_HD int ldz(int l) { return (int)((LDZ_BITS >> (2 * l)) & 3u) - 1; }
 
-// the rarely taken exact operations (named so the call sites read as the rare branches they are)
-inline double rare_div(double a, double b) { return a / b; }
-inline double rare_pow(double x, double y) { return pow_glibc(x, y); }
-#else
+// the rarely taken exact operations (named so the call sites read as the rare branches they are;
+// as out-of-line calls they measured neutral, profiles/r02/ab16_noinline_rare.txt)
 OMB_HD double rare_div(double a, double b) { return a / b; }
 OMB_HD double rare_pow(double x, double y) { return pow_glibc(x, y); }
-#endif
 
 // IEEE a/b that never takes CUDA's division slow path for a zero numerator
 // (CUDA routes 0/b through a called subroutine; zero momenta and zero
