@@ -117,11 +117,8 @@ __global__ void k_fmm_upward(const long long* parents, int np, const long long* 
 // all of M and D), PART 1 = L4..L19 (needs M0..M3 and D4..D19).  Fewer live
 // accumulators per pass: 128 registers, twice the warps of the fused pass
 // against the latency of the source-moment loads.
-#ifndef OMB_M2L_MINB
-#define OMB_M2L_MINB 4
-#endif
 template <int PART>
-__global__ void __launch_bounds__(128, OMB_M2L_MINB) k_fmm_m2l(const long long* off, const unsigned long long* contrib,
+__global__ void __launch_bounds__(128, 4) k_fmm_m2l(const long long* off, const unsigned long long* contrib,
                                                     const double* D /*[G][2][20]*/, const unsigned char* cellcell,
                                                     const double* M, double* L, long long ntarget,
                                                     const long long* targets, const long long* subset,
@@ -139,17 +136,9 @@ __global__ void __launch_bounds__(128, OMB_M2L_MINB) k_fmm_m2l(const long long* 
   // word is loaded while this one is processed
   const long long q1 = off[ti + 1];
   unsigned long long wn = off[ti] < q1 ? __ldg(contrib + off[ti]) : 0ull;
-#ifdef OMB_M2L_PF2
-  unsigned long long wn2 = off[ti] + 1 < q1 ? __ldg(contrib + off[ti] + 1) : 0ull;
-#endif
   for (long long q = off[ti]; q < q1; q++) {
     unsigned long long w = wn;
-#ifdef OMB_M2L_PF2
-    wn = wn2;
-    if (q + 2 < q1) wn2 = __ldg(contrib + q + 2);
-#else
     if (q + 1 < q1) wn = __ldg(contrib + q + 1);
-#endif
     long long src = (long long)(w & 0xFFFFFFFFFFull);
     long long g = (long long)((w >> 40) & 0x7FFFFFull);
     int flip = (int)(w >> 63);
