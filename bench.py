@@ -274,6 +274,15 @@ def fp64_peak(lib, torch):
     return flops / sec / 1e12
 
 
+def _transfer_label(st):
+    if st._mapped is None:
+        return "threads (host packing + DMA)"
+    if st._gather_frac is None:
+        return "mapped (GPU reads/writes the pinned host leaves)"
+    return (f"hybrid (upload: GPU reads {st._gather_frac[0]:.0%} of the leaves from the pinned host slab, "
+            "host threads pack the rest + DMA; download: DMA + host threads)")
+
+
 def gpu_arm(args, rank, world):
     import gc
 
@@ -460,8 +469,7 @@ def gpu_arm(args, rank, world):
         e2e = {"value": cells * args.e2e_steps / wall, "unit": UNIT,
                "h2d_bytes_per_step": up, "d2h_bytes_per_step": down + 2 * 8 + 4 + 6 * 8,
                "steps": args.e2e_steps, "api": "B200HydroStepper.cfl_dt + rk3_step (host_sync=True)",
-               "transfer": "mapped (GPU reads/writes the pinned host leaves)" if st2._mapped is not None
-               else "threads (host packing + DMA)"}
+               "transfer": _transfer_label(st2)}
         del st2, t2, p2
         gc.collect()
         torch.cuda.empty_cache()

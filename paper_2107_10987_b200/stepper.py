@@ -169,14 +169,25 @@ class B200HydroStepper:
         # memory that the GPU reads / writes directly (omb_host_gather/scatter) -- no host
         # thread touches the data, which pays when several ranks share the host's memory
         # bandwidth (4 ranks: 2x faster than the threads path).  "threads": the arrays stay
-        # in place and host threads pack them around DMA copies (1 rank: 8 % faster).
-        # OMB_HOST_XFER=mapped|threads overrides the choice.
+        # in place and host threads pack them around DMA copies.  "hybrid" (1 rank): the
+        # arrays move into the mapped slab (aligned rows: host unpacking is faster there
+        # too), the GPU gathers the last OMB_GATHER_FRAC of the leaves on a side stream
+        # while host threads pack the rest; downloads go through the host threads.
+        # OMB_HOST_XFER=mapped|threads|hybrid overrides the choice.
         self._mapped = None
+        self._gather_frac = None
         xfer = os.environ.get("OMB_HOST_XFER", "auto")
         if xfer == "auto":
-            xfer = "mapped" if int(os.environ.get("LOCAL_WORLD_SIZE", "1")) > 1 else "threads"
+            xfer = "mapped" if int(os.environ.get("LOCAL_WORLD_SIZE", "1")) > 1 else "hybrid"
         if host_sync and xfer == "mapped":
-            self._rehome()
+            self._rehome(b.ncompute)
+        elif host_sync and xfer == "hybrid":
+            frac = min(1.0, max(0.0, float(os.environ.get("OMB_GATHER_FRAC", "0.1"))))
+            k = b.ncompute - int(round(b.ncompute * frac))  # leaves [0, k): host threads; [k, nc): GPU
+            self._rehome(b.ncompute - k)  # (the gather's stash: written, read by no scatter)
+            if self._mapped is not None:
+                self._gather_frac = (frac, k)
+                self._xfer_stream = torch.cuda.Stream(dev)
         # the last stage is launched in parts of OMB_TAIL_WAVES waves of runs (runs sorted by
         # leaf), and each part's leaves are copied back while the next part computes: by the
         # copy engine + host threads (omb_host_download_after), or, mapped, by a scatter kernel
@@ -294,11 +305,12 @@ class B200HydroStepper:
 
     SPAN_STASH = 48 * 56  # ghost z + line-edge doubles per leaf of the zero-copy spans (omb_host_gather)
 
-    def _rehome(self):
+    def _rehome(self, stash_leaves):
         """Move the owned leaves' padded arrays (SubGrid.u) into one pinned host slab,
         mapped into the device address space, and point each SubGrid at its slot
         (values copied; the leaf's arrays stay ordinary C-contiguous float64 numpy
-        arrays).  Skipped for subgrid types without the reference's ``_u`` slot."""
+        arrays).  Skipped for subgrid types without the reference's ``_u`` slot.
+        ``stash_leaves``: how many leaves the zero-copy kernels move per call."""
         b = self.batch
         nc = b.ncompute
         sgs = [lf.subgrid for lf in b.leaves[:nc]]
@@ -314,7 +326,8 @@ class B200HydroStepper:
         base = slab.data_ptr()
         ptrs = torch.arange(nc, dtype=torch.int64) * (6 * 14 ** 3 * 8) + base
         self._mapped = {"slab": slab, "views": views, "sgs": sgs, "ptrs": ptrs.to(self.dev),
-                        "stash": torch.empty(nc * self.SPAN_STASH, dtype=torch.float64, device=self.dev)}
+                        "stash": torch.empty(max(1, stash_leaves) * self.SPAN_STASH, dtype=torch.float64,
+                                             device=self.dev)}
 
     def _mapped_check(self):
         """Leaves whose array was replaced since the re-homing (a user assigned a new
@@ -329,15 +342,33 @@ class B200HydroStepper:
     @_on_device
     def upload(self):
         """Copy the host leaves' interiors into the device state.  Mapped slab: one
-        kernel reads them over PCIe.  Otherwise pipelined: host threads pack chunk c
-        while chunk c-1 is on the copy engine.  Only owned leaves: halo leaves come
-        from their owners every stage."""
+        kernel reads them over PCIe.  Threads: pipelined, host threads pack chunk c
+        while chunk c-1 is on the copy engine.  Hybrid: both at once on disjoint
+        leaf ranges.  Only owned leaves: halo leaves come from their owners every stage."""
         b = self.batch
         if self._mapped is not None:
             self._mapped_check()
             m = self._mapped
-            _lib.check(self.lib.omb_host_gather(ptr(m["ptrs"]), b.ncompute, b.fstride, ptr(self._buf[self._state]),
-                                                ptr(m["stash"]), stream_handle(None)), "omb_host_gather")
+            if self._gather_frac is None:
+                _lib.check(self.lib.omb_host_gather(ptr(m["ptrs"]), b.ncompute, b.fstride,
+                                                    ptr(self._buf[self._state]), ptr(m["stash"]), stream_handle(None)),
+                           "omb_host_gather")
+                return
+            k = self._gather_frac[1]
+            if k < b.ncompute:  # hybrid: the GPU reads leaves [k, nc) while host threads pack [0, k)
+                side, main = self._xfer_stream, torch.cuda.current_stream(self.dev)
+                side.wait_stream(main)
+                _lib.check(self.lib.omb_host_gather(ptr(m["ptrs"]) + 8 * k, b.ncompute - k, b.fstride,
+                                                    ptr(self._buf[self._state]) + 8 * 512 * k, ptr(m["stash"]),
+                                                    ctypes.c_void_p(side.cuda_stream)), "omb_host_gather")
+                self._upload_threads(k)
+                main.wait_stream(side)
+                return
+        self._upload_threads(b.ncompute)
+
+    def _upload_threads(self, count):
+        b = self.batch
+        if count == 0:
             return
         if self._pinned is None:
             self._pinned = torch.zeros(6 * b.fstride, dtype=torch.float64).pin_memory()
@@ -346,10 +377,10 @@ class B200HydroStepper:
         self._up_ev = torch.cuda.Event()
         ptrs = b._leaf_ptrs(b.ncompute)
         if ptrs is not None:
-            _lib.check(self.lib.omb_host_upload(ptrs.ctypes.data, b.ncompute, 8, b.fstride, ptr(self._pinned),
+            _lib.check(self.lib.omb_host_upload(ptrs.ctypes.data, count, 8, b.fstride, ptr(self._pinned),
                                                 ptr(self._buf[self._state]), self.TRANSFER_CHUNKS,
                                                 stream_handle(None)), "omb_host_upload")
-        else:
+        else:  # (not hybrid: its leaves are slab views)
             host = self._pinned.numpy().reshape(6, b.L + b.nvirtual, 8, 8, 8)
             b.pack(out=host)
             self._buf[self._state].copy_(self._pinned, non_blocking=True)
@@ -363,6 +394,7 @@ class B200HydroStepper:
         b = self.batch
         if self._mapped is not None:
             self._mapped_check()
+        if self._mapped is not None and self._gather_frac is None:
             m = self._mapped
             _lib.check(self.lib.omb_host_scatter(ptr(self._buf[self._state]), ptr(m["stash"]), b.ncompute,
                                                  b.fstride, ptr(m["ptrs"]), stream_handle(None)), "omb_host_scatter")
@@ -382,7 +414,7 @@ class B200HydroStepper:
     def _download_tail(self):
         b = self.batch
         t = self._tail
-        if self._mapped is not None:
+        if self._mapped is not None and self._gather_frac is None:
             # each part's final leaves are written to the mapped host slab as soon as the
             # part is done (its event), on the side stream, while later parts compute
             m = self._mapped

@@ -273,14 +273,16 @@ def _ghosts(t):
     return np.stack(out)
 
 
-@pytest.mark.parametrize("xfer", ["mapped", "mapped-tail", "threads"])
+@pytest.mark.parametrize("xfer", ["mapped", "mapped-tail", "threads", "hybrid"])
 def test_host_transfer_paths(monkeypatch, xfer):
-    """Both host<->device transfer paths give the golden step, leave the host
+    """Every host<->device transfer path gives the golden step, leaves the host
     ghost cells exactly as they were (the mapped path writes whole 64 B lines,
-    restoring the neighbouring ghost doubles from its stash), and pick up leaf
+    restoring the neighbouring ghost doubles from its stash), and picks up leaf
     arrays a user replaced.  mapped-tail: the last stage in one-run launch parts,
-    each part's leaves written to the host while the next computes."""
+    each part's leaves written to the host while the next computes.  hybrid: the
+    GPU gathers part of the leaves while host threads pack the others."""
     monkeypatch.setenv("OMB_HOST_XFER", xfer.split("-")[0])
+    monkeypatch.setenv("OMB_GATHER_FRAC", "0.4")
     if xfer == "mapped-tail":
         monkeypatch.setenv("OMB_TAIL_RUNS", "1")
     t, g = case_tree("smooth_reflecting")
@@ -292,7 +294,8 @@ def test_host_transfer_paths(monkeypatch, xfer):
         u[:, 3:11, 3:11, 3:11] = keep
     ghosts = _ghosts(t)
     st = _stepper(t)
-    assert (st._mapped is not None) == xfer.startswith("mapped")
+    assert (st._mapped is not None) == (xfer != "threads")
+    assert (st._gather_frac is not None) == (xfer == "hybrid")
     assert (st._tail is not None) == (xfer == "mapped-tail")
     st.rk3_step(st.cfl_dt(0.4))
     _check_state(t, g)
@@ -306,12 +309,13 @@ def test_host_transfer_paths(monkeypatch, xfer):
     assert bitwise_mismatch(_ghosts(t), ghosts) == 0
 
 
-@pytest.mark.parametrize("xfer", ["threads", "mapped"])
+@pytest.mark.parametrize("xfer", ["threads", "mapped", "hybrid"])
 @pytest.mark.parametrize("part_runs", [1, 3, 7])
 def test_overlapped_download(monkeypatch, part_runs, xfer):
     """The last stage launched in parts with each part's leaves copied back while
     the next computes gives the golden step (and the CFL-abort rollback still holds)."""
     monkeypatch.setenv("OMB_HOST_XFER", xfer)
+    monkeypatch.setenv("OMB_GATHER_FRAC", "0.3")
     monkeypatch.setenv("OMB_TAIL_RUNS", str(part_runs))
     t, g = case_tree("sedov_c1")
     st = _stepper(t)
