@@ -22,6 +22,8 @@ import numpy as np
 from ._abi import AMR_TASK_INTS, BC_CODES, LEAF_INFO_DTYPE
 from .geometry import NFIELDS
 
+_SU = operator.attrgetter("subgrid._u")
+
 OFFS = [(i, j, k) for i in (-1, 0, 1) for j in (-1, 0, 1) for k in (-1, 0, 1)]
 
 
@@ -345,12 +347,16 @@ class LeafBatch:
         (SubGrid.u), or None if one is not a C-contiguous float64 (6, 14, 14, 14)
         array.  Cached: rebuilt only when a leaf's array object changed (the
         cache holds the arrays, so their memory cannot be reused meanwhile)."""
+        cache = getattr(self, "_ptr_cache", {}).get(count)
+        if cache is not None:  # fast identity check (C-level loops; 32768 leaves ~1 ms)
+            try:
+                if all(map(operator.is_, map(_SU, cache[2]), cache[0])):
+                    return cache[1]
+            except AttributeError:  # subgrids without the reference's _u slot
+                pass
         arrs = [lf.subgrid.u for lf in self.leaves[:count]]
         if any(u is None for u in arrs):  # 16^3 / 32^3 blocks: interior views only
             return None
-        cache = getattr(self, "_ptr_cache", {}).get(count)
-        if cache is not None and all(map(operator.is_, arrs, cache[0])):
-            return cache[1]
         ptrs = np.empty(count, dtype=np.uintp)
         for i, u in enumerate(arrs):
             if not (u.flags.c_contiguous and u.dtype == np.float64 and u.shape == (NFIELDS, 14, 14, 14)):
@@ -358,7 +364,7 @@ class LeafBatch:
             ptrs[i] = u.__array_interface__["data"][0]
         if not hasattr(self, "_ptr_cache"):
             self._ptr_cache = {}
-        self._ptr_cache[count] = (arrs, ptrs)
+        self._ptr_cache[count] = (arrs, ptrs, self.leaves[:count])
         return ptrs
 
     def pack(self, out=None, lib=None):

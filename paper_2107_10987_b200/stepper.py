@@ -23,6 +23,7 @@ reference leaves it when it raises.
 """
 
 import ctypes
+import operator
 import os
 import sys
 
@@ -34,6 +35,9 @@ from .batch import LeafBatch
 from .device import ptr, require_cuda, stream_handle, torch
 from .errors import NumericsError
 from .hydro import SSP_RK3_STAGES, FloorConfig, StepStats
+
+
+_SU = operator.attrgetter("subgrid._u")
 
 
 class _DeviceArray:
@@ -188,6 +192,7 @@ class B200HydroStepper:
             if self._mapped is not None:
                 self._gather_frac = (frac, k)
                 self._xfer_stream = torch.cuda.Stream(dev)
+                self._scatter_tail = os.environ.get("OMB_SCATTER_TAIL", "1") == "1"
         # the last stage is launched in parts of OMB_TAIL_WAVES waves of runs (runs sorted by
         # leaf), and each part's leaves are copied back while the next part computes: by the
         # copy engine + host threads (omb_host_download_after), or, mapped, by a scatter kernel
@@ -325,7 +330,8 @@ class B200HydroStepper:
             views.append(sg._u)
         base = slab.data_ptr()
         ptrs = torch.arange(nc, dtype=torch.int64) * (6 * 14 ** 3 * 8) + base
-        self._mapped = {"slab": slab, "views": views, "sgs": sgs, "ptrs": ptrs.to(self.dev),
+        self._mapped = {"slab": slab, "views": views, "leaves": b.leaves[:nc], "ptrs": ptrs.to(self.dev),
+                        "hptrs": ptrs.numpy().astype(np.uintp),  # (fixed: _mapped_check keeps the views)
                         "stash": torch.empty(max(1, stash_leaves) * self.SPAN_STASH, dtype=torch.float64,
                                              device=self.dev)}
 
@@ -333,7 +339,10 @@ class B200HydroStepper:
         """Leaves whose array was replaced since the re-homing (a user assigned a new
         SubGrid.u) are copied into their slab slot again."""
         m = self._mapped
-        for k, (sg, v) in enumerate(zip(m["sgs"], m["views"])):
+        if all(map(operator.is_, map(_SU, m["leaves"]), m["views"])):  # (C-level loops: 32768 leaves ~2 ms)
+            return
+        for lf, v in zip(m["leaves"], m["views"]):
+            sg = lf.subgrid
             if sg._u is not v:
                 if sg._u is not None:
                     v[...] = sg._u
@@ -366,6 +375,13 @@ class B200HydroStepper:
                 return
         self._upload_threads(b.ncompute)
 
+    def _host_ptrs(self):
+        """The owned leaves' host array addresses: the slab's (after _mapped_check) or
+        the batch's cached table (None: not all standard arrays)."""
+        if self._mapped is not None:
+            return self._mapped["hptrs"]
+        return self.batch._leaf_ptrs(self.batch.ncompute)
+
     def _upload_threads(self, count):
         b = self.batch
         if count == 0:
@@ -375,7 +391,7 @@ class B200HydroStepper:
         if getattr(self, "_up_ev", None) is not None:
             self._up_ev.synchronize()  # the previous upload's copies still read the pinned buffer
         self._up_ev = torch.cuda.Event()
-        ptrs = b._leaf_ptrs(b.ncompute)
+        ptrs = self._host_ptrs()
         if ptrs is not None:
             _lib.check(self.lib.omb_host_upload(ptrs.ctypes.data, count, 8, b.fstride, ptr(self._pinned),
                                                 ptr(self._buf[self._state]), self.TRANSFER_CHUNKS,
@@ -402,7 +418,7 @@ class B200HydroStepper:
             return
         if self._pinned is None:
             self._pinned = torch.zeros(6 * b.fstride, dtype=torch.float64).pin_memory()
-        ptrs = b._leaf_ptrs(b.ncompute)
+        ptrs = self._host_ptrs()
         if ptrs is not None:
             _lib.check(self.lib.omb_host_download(ptr(self._buf[self._state]), ptr(self._pinned), b.ncompute, 8,
                                                   b.fstride, ptrs.ctypes.data, self.TRANSFER_CHUNKS,
@@ -433,17 +449,40 @@ class B200HydroStepper:
             side.synchronize()
             torch.cuda.current_stream(self.dev).synchronize()
             return
-        ptrs = b._leaf_ptrs(b.ncompute)
+        if self._mapped is not None:
+            self._mapped_check()
+        ptrs = self._host_ptrs()
         if ptrs is None:
             self.download()
             return
         if self._pinned is None:
             self._pinned = torch.zeros(6 * b.fstride, dtype=torch.float64).pin_memory()
-        ev = (ctypes.c_void_p * len(t["events"]))(*[e.cuda_event for e in t["events"]])
-        _lib.check(self.lib.omb_host_download_after(ptr(self._buf[self._state]), ptr(self._pinned), 8, b.fstride,
-                                                    ptrs.ctypes.data, len(t["events"]), t["bounds"].ctypes.data,
-                                                    ev, ctypes.c_void_p(t["stream"].cuda_stream)),
-                   "omb_host_download_after")
+        bnd, nparts = t["bounds"], len(t["events"])
+        side = None
+        if self._gather_frac is not None and self._scatter_tail:
+            # hybrid: the leaves the upload gathered ([k, nc), the last parts) are written back
+            # by the GPU on a side stream (their stash holds this step's host ghost doubles)
+            m, k, st = self._mapped, self._gather_frac[1], self.SPAN_STASH
+            side = self._xfer_stream
+            cur = ptr(self._buf[self._state])
+            for c in range(nparts):
+                lo, hi = max(int(bnd[c]), k), int(bnd[c + 1])
+                if hi <= lo:
+                    continue
+                side.wait_event(t["events"][c])
+                _lib.check(self.lib.omb_host_scatter(cur + 8 * 512 * lo, ptr(m["stash"]) + 8 * st * (lo - k), hi - lo,
+                                                     b.fstride, ptr(m["ptrs"]) + 8 * lo,
+                                                     ctypes.c_void_p(side.cuda_stream)), "omb_host_scatter")
+            nparts = int(np.searchsorted(bnd, k, side="left"))  # parts starting below k
+            bnd = np.minimum(bnd[:nparts + 1], k).astype(np.int32)
+        if nparts > 0:
+            ev = (ctypes.c_void_p * nparts)(*[e.cuda_event for e in t["events"][:nparts]])
+            _lib.check(self.lib.omb_host_download_after(ptr(self._buf[self._state]), ptr(self._pinned), 8, b.fstride,
+                                                        ptrs.ctypes.data, nparts, bnd.ctypes.data,
+                                                        ev, ctypes.c_void_p(t["stream"].cuda_stream)),
+                       "omb_host_download_after")
+        if side is not None:
+            side.synchronize()
 
     def state_tensor(self):
         return self._buf[self._state]

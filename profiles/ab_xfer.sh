@@ -1,8 +1,7 @@
-set -x
-for rep in 1 2; do
-for v in threads hybrid:0.05 hybrid:0.1 hybrid:0.15 hybrid:0.2; do
-  x=${v%%:*}; f=${v#*:}; [ "$f" = "$v" ] && f=0
-  OMB_HOST_XFER=$x OMB_GATHER_FRAC=$f python bench.py --steps 5 --warmup 3 --efficiency-steps 0 --no-cpu-baseline > gpurun_out/abx_${x}_${f}_$rep.json 2>/dev/null
+# host-transfer A/B at c3 (1 GPU): threads vs hybrid (upload fraction f gathered by the GPU, tail scatter on)
+for rep in 1 2 3 4; do
+for v in threads:0:1 hybrid:0.2:1 hybrid:0.1:1; do
+  IFS=: read x f sc <<< "$v"
+  OMB_HOST_XFER=$x OMB_GATHER_FRAC=$f OMB_SCATTER_TAIL=$sc python bench.py --steps 2 --warmup 3 --efficiency-steps 0 \
+    --e2e-steps 24 --no-cpu-baseline > gpurun_out/abx4_${x}_${f}_${sc}_$rep.json 2>/dev/null
 done; done
-for c in c2; do for v in threads hybrid:0.1; do x=${v%%:*}; f=${v#*:}; [ "$f" = "$v" ] && f=0
-  OMB_HOST_XFER=$x OMB_GATHER_FRAC=$f python bench.py --config c2 --steps 5 --warmup 3 --efficiency-steps 0 --no-cpu-baseline > gpurun_out/abx_${c}_${x}_${f}.json 2>/dev/null; done; done
