@@ -23,7 +23,7 @@
 extern "C" {
 #endif
 
-#define OMB_ABI_VERSION 6
+#define OMB_ABI_VERSION 7
 
 /* per-leaf topology / geometry record (device array, one per leaf) */
 typedef struct {
@@ -159,9 +159,12 @@ int omb_scalar_input(const double *u, long long fstride, int n_all, const double
  * (reference.py:39, hydro/eos.py:50-61) */
 int omb_selftest_pow(const double *x, const double *y, long long n, double *out, void *stream);
 /* host (CPU) packing between per-leaf padded arrays (6, n+6, n+6, n+6) -- SubGrid.u, tree.py:47-61 --
- * and the [6][L][n^3] device layout; multithreaded, used around H2D/D2H copies */
-int omb_host_pack(const double *const *leaf_u, int L, int n, long long fstride, double *out);
-int omb_host_unpack(const double *in, int L, int n, long long fstride, double *const *leaf_u);
+ * and the [6][L][n^3] device layout; multithreaded, used around H2D/D2H copies.  m = the padded edge
+ * of the host arrays: n + 6 for whole leaves; for the 8^3 blocks of 16^3 / 32^3 leaves (n = 8) the
+ * leaf's edge (22 / 38), leaf_u[i] pointing at the block's corner inside its leaf's array (ABI 7 added
+ * m to the five host-transfer calls) */
+int omb_host_pack(const double *const *leaf_u, int L, int n, int m, long long fstride, double *out);
+int omb_host_unpack(const double *in, int L, int n, int m, long long fstride, double *const *leaf_u);
 /* the same fused with the host<->device copy of a [6][fstride] device state (the e2e path of
  * HydroStepper's host state of record, step.py:94-102): leaves cut into nchunks chunks, host threads
  * pack chunk c into the pinned buffer while chunk c-1 is copied (upload), or unpack chunk c while
@@ -169,15 +172,16 @@ int omb_host_unpack(const double *in, int L, int n, long long fstride, double *c
  * download returns with the host arrays written. */
 /* host threads used by omb_host_pack/unpack/upload/download (0 = all cores, capped at 16) */
 int omb_set_host_threads(int n);
-int omb_host_upload(const double *const *leaf_u, int L, int n, long long fstride, double *pinned, double *dev,
-                    int nchunks, void *stream);
-int omb_host_download(const double *dev, double *pinned, int L, int n, long long fstride, double *const *leaf_u,
-                      int nchunks, void *stream);
+int omb_host_upload(const double *const *leaf_u, int L, int n, int m, long long fstride, double *pinned,
+                    double *dev, int nchunks, void *stream);
+int omb_host_download(const double *dev, double *pinned, int L, int n, int m, long long fstride,
+                      double *const *leaf_u, int nchunks, void *stream);
 /* the download overlapped with the launch parts of the stage producing it: chunk c = leaves
  * [bounds[c], bounds[c+1]) is copied on copy_stream after the cudaEvent_t ready[c] fires, then unpacked
  * by the host threads; returns with the host arrays written */
-int omb_host_download_after(const double *dev, double *pinned, int n, long long fstride, double *const *leaf_u,
-                            int nchunks, const int *bounds, void *const *ready, void *copy_stream);
+int omb_host_download_after(const double *dev, double *pinned, int n, int m, long long fstride,
+                            double *const *leaf_u, int nchunks, const int *bounds, void *const *ready,
+                            void *copy_stream);
 /* zero-copy host transfers (n = 8): leaf_u is a DEVICE array of L pointers to padded (6, 14, 14, 14)
  * arrays in mapped pinned host memory (the stepper re-homes SubGrid.u into one pinned slab).  The GPU
  * reads / writes them over PCIe in whole 64 B lines: per (field, x), rows y = 3..10 with all z, widened

@@ -12,7 +12,7 @@ from .errors import NativeError
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 SO_PATH = os.environ.get("OMB_LIB_PATH") or os.path.join(_HERE, "libomb200.so")  # override: A/B experiments
-ABI_VERSION = 6
+ABI_VERSION = 7
 _lib = None
 
 EXPORTS = ("omb_abi_version", "omb_last_error", "omb_stage_smem_bytes", "omb_primitives", "omb_reconstruct",
@@ -50,11 +50,11 @@ def load():
     L.omb_face_flux.argtypes = [vp, i, i, vp, vp]
     L.omb_physical_flux.argtypes = [vp, i, i, vp, vp]
     L.omb_scalar_input.argtypes = [vp, ll, i, vp, i, d, d, d, vp, vp]
-    L.omb_host_pack.argtypes = [vp, i, i, ll, vp]
-    L.omb_host_unpack.argtypes = [vp, i, i, ll, vp]
-    L.omb_host_upload.argtypes = [vp, i, i, ll, vp, vp, i, vp]
-    L.omb_host_download.argtypes = [vp, vp, i, i, ll, vp, i, vp]
-    L.omb_host_download_after.argtypes = [vp, vp, i, ll, vp, i, vp, vp, vp]
+    L.omb_host_pack.argtypes = [vp, i, i, i, ll, vp]
+    L.omb_host_unpack.argtypes = [vp, i, i, i, ll, vp]
+    L.omb_host_upload.argtypes = [vp, i, i, i, ll, vp, vp, i, vp]
+    L.omb_host_download.argtypes = [vp, vp, i, i, i, ll, vp, i, vp]
+    L.omb_host_download_after.argtypes = [vp, vp, i, i, ll, vp, i, vp, vp, vp]
     L.omb_host_gather.argtypes = [vp, i, ll, vp, vp, vp]
     L.omb_host_scatter.argtypes = [vp, vp, i, ll, vp, vp]
     L.omb_set_host_threads.argtypes = [i]

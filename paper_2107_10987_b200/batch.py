@@ -106,6 +106,8 @@ class LeafBatch:
                 raise UnsupportedTree(str(e)) from None
         self.tree = tree
         self.n = tree.n
+        # padded edge of the host arrays the host transfers read / write (blocks: their leaf's)
+        self.host_m = 8 * self.blocks.nb + 6 if self.blocks is not None else 14
         if tree.boundary not in BC_CODES:
             raise ValueError(f"unknown boundary {tree.boundary!r}")
         self.bc = BC_CODES[tree.boundary]
@@ -347,6 +349,8 @@ class LeafBatch:
         (SubGrid.u), or None if one is not a C-contiguous float64 (6, 14, 14, 14)
         array.  Cached: rebuilt only when a leaf's array object changed (the
         cache holds the arrays, so their memory cannot be reused meanwhile)."""
+        if self.blocks is not None:
+            return self._block_ptrs(count)
         cache = getattr(self, "_ptr_cache", {}).get(count)
         if cache is not None:  # fast identity check (C-level loops; 32768 leaves ~1 ms)
             try:
@@ -367,13 +371,47 @@ class LeafBatch:
         self._ptr_cache[count] = (arrs, ptrs, self.leaves[:count])
         return ptrs
 
+    def _block_ptrs(self, count):
+        """The same for 8^3 blocks of 16^3 / 32^3 leaves: each block's corner inside
+        its leaf's padded (6, m, m, m) array (m = host_m), so the host transfers copy
+        the block's interior straight out of / into the leaf's array.  Cached;
+        revalidated by the identity of the leaves' arrays."""
+        cache = getattr(self, "_ptr_cache", {}).get(count)
+        if cache is not None:
+            try:
+                if all(map(operator.is_, map(_SU, cache[2]), cache[0])):
+                    return cache[1]
+            except AttributeError:
+                pass
+        m = self.host_m
+        blocks = self.leaves[:count]
+        parents, where = [], {}
+        for bk in blocks:
+            if id(bk.leaf) not in where:
+                where[id(bk.leaf)] = len(parents)
+                parents.append(bk.leaf)
+        arrs = [lf.subgrid.u for lf in parents]
+        base = np.empty(len(parents), dtype=np.uintp)
+        for k, u in enumerate(arrs):
+            if u is None or not (u.flags.c_contiguous and u.dtype == np.float64 and u.shape == (NFIELDS, m, m, m)):
+                return None
+            base[k] = u.__array_interface__["data"][0]
+        ptrs = np.empty(count, dtype=np.uintp)
+        for i, bk in enumerate(blocks):
+            bx, by, bz = bk.b
+            ptrs[i] = int(base[where[id(bk.leaf)]]) + 8 * ((8 * bx * m + 8 * by) * m + 8 * bz)
+        if not hasattr(self, "_ptr_cache"):
+            self._ptr_cache = {}
+        self._ptr_cache[count] = (arrs, ptrs, parents)
+        return ptrs
+
     def pack(self, out=None, lib=None):
         """Interiors of all batch leaves into ``out`` ([6][L+nvirtual][8][8][8]);
         virtual (AMR ghost) leaves are left as they are."""
         U = out if out is not None else np.zeros((NFIELDS, self.L + self.nvirtual, 8, 8, 8))
         ptrs = self._leaf_ptrs(self.L) if lib is not None else None
         if ptrs is not None and U.flags.c_contiguous:
-            lib.omb_host_pack(ptrs.ctypes.data, self.L, 8, self.fstride, U.ctypes.data)
+            lib.omb_host_pack(ptrs.ctypes.data, self.L, 8, self.host_m, self.fstride, U.ctypes.data)
             return U
         for i, lf in enumerate(self.leaves):
             U[:, i] = lf.subgrid.interior
@@ -383,7 +421,7 @@ class LeafBatch:
         """Write the computed leaves back (halo leaves belong to other ranks)."""
         ptrs = self._leaf_ptrs(self.ncompute) if lib is not None else None
         if ptrs is not None and U.flags.c_contiguous and self.ncompute == self.L:
-            lib.omb_host_unpack(U.ctypes.data, self.L, 8, self.fstride, ptrs.ctypes.data)
+            lib.omb_host_unpack(U.ctypes.data, self.L, 8, self.host_m, self.fstride, ptrs.ctypes.data)
             return
         for i, lf in enumerate(self.leaves[:self.ncompute]):
             lf.subgrid.interior[:] = U[:, i]

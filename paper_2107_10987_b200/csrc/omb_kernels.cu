@@ -1083,20 +1083,22 @@ static int host_workers(int L) {
   return (int)nt;
 }
 }  // extern "C"
-template <int NN>
+// one unit = an n^3 interior inside a padded host array of edge m: a whole leaf
+// (m = n + 6, u = the leaf's array) or an 8^3 block of a 16^3 / 32^3 leaf (u = the
+// leaf's array advanced to the block's corner, m = the leaf's padded edge)
+template <int NN, int MM>
 static void copy_leaf_n(const double* u, double* packed, int i, long long fstride, bool to_packed) {
-  constexpr int m = NN + 6;
   constexpr long long n3 = (long long)NN * NN * NN;
   // packing: whole 64-byte rows of the (pinned) staging buffer are written
   // with streaming stores -- no read-for-ownership of the destination lines
   const bool stream = to_packed && NN % 2 == 0 && ((uintptr_t)packed & 15) == 0 && (fstride % 2) == 0;
   for (int v = 0; v < 6; v++) {
     double* P = packed + (long long)v * fstride + (long long)i * n3;
-    double* Q = const_cast<double*>(u) + (long long)v * m * m * m + (3 * m + 3) * m + 3;
+    double* Q = const_cast<double*>(u) + (long long)v * MM * MM * MM + (3 * MM + 3) * MM + 3;
     for (int x = 0; x < NN; x++)
       for (int y = 0; y < NN; y++) {
         double* p = P + (x * NN + y) * NN;
-        double* q = Q + (x * m + y) * m;
+        double* q = Q + (x * MM + y) * MM;
         if (stream) {
 #pragma unroll
           for (int k = 0; k < NN; k += 2) _mm_stream_pd(p + k, _mm_loadu_pd(q + k));
@@ -1110,9 +1112,10 @@ static void copy_leaf_n(const double* u, double* packed, int i, long long fstrid
   if (stream) _mm_sfence();
 }
 extern "C" {
-static void copy_leaf(const double* u, double* packed, int i, int n, long long fstride, bool to_packed) {
-  if (n == 8) return copy_leaf_n<8>(u, packed, i, fstride, to_packed);
-  int m = n + 6;
+static void copy_leaf(const double* u, double* packed, int i, int n, int m, long long fstride, bool to_packed) {
+  if (n == 8 && m == 14) return copy_leaf_n<8, 14>(u, packed, i, fstride, to_packed);
+  if (n == 8 && m == 22) return copy_leaf_n<8, 22>(u, packed, i, fstride, to_packed);
+  if (n == 8 && m == 38) return copy_leaf_n<8, 38>(u, packed, i, fstride, to_packed);
   long long n3 = (long long)n * n * n;
   for (int v = 0; v < 6; v++)
     for (int x = 0; x < n; x++)
@@ -1124,11 +1127,12 @@ static void copy_leaf(const double* u, double* packed, int i, int n, long long f
       }
 }
 
-static void host_copy(const double* const* leaf_u, int L, int n, long long fstride, double* packed, bool to_packed) {
+static void host_copy(const double* const* leaf_u, int L, int n, int m, long long fstride, double* packed,
+                      bool to_packed) {
   const int nt = host_workers(L);
   host_pool().run([&](int t) {
     for (int i = (int)((long long)L * t / nt); i < (int)((long long)L * (t + 1) / nt); i++)
-      copy_leaf(leaf_u[i], packed, i, n, fstride, to_packed);
+      copy_leaf(leaf_u[i], packed, i, n, m, fstride, to_packed);
   }, nt);
 }
 
@@ -1138,13 +1142,17 @@ int omb_set_host_threads(int n) {
   return 0;
 }
 
-int omb_host_pack(const double* const* leaf_u, int L, int n, long long fstride, double* out) {
-  host_copy(leaf_u, L, n, fstride, out, true);
+static bool bad_pitch(int n, int m) { return n <= 0 || m < n + 6; }
+
+int omb_host_pack(const double* const* leaf_u, int L, int n, int m, long long fstride, double* out) {
+  if (bad_pitch(n, m)) return set_err("omb_host_pack: padded edge m < n + 6");
+  host_copy(leaf_u, L, n, m, fstride, out, true);
   return 0;
 }
 
-int omb_host_unpack(const double* in, int L, int n, long long fstride, double* const* leaf_u) {
-  host_copy((const double* const*)leaf_u, L, n, fstride, const_cast<double*>(in), false);
+int omb_host_unpack(const double* in, int L, int n, int m, long long fstride, double* const* leaf_u) {
+  if (bad_pitch(n, m)) return set_err("omb_host_unpack: padded edge m < n + 6");
+  host_copy((const double* const*)leaf_u, L, n, m, fstride, const_cast<double*>(in), false);
   return 0;
 }
 
@@ -1153,9 +1161,10 @@ int omb_host_unpack(const double* in, int L, int n, long long fstride, double* c
 // chunk c into the pinned staging buffer while the copy engine moves chunk
 // c-1 (upload), or unpack chunk c while chunk c+1 is still in flight
 // (download).  One 2D copy per chunk covers the 6 field planes.
-int omb_host_upload(const double* const* leaf_u, int L, int n, long long fstride, double* pinned, double* dev,
-                    int nchunks, void* stream) {
+int omb_host_upload(const double* const* leaf_u, int L, int n, int m, long long fstride, double* pinned,
+                    double* dev, int nchunks, void* stream) {
   if (int rc = lib_init()) return rc;
+  if (bad_pitch(n, m)) return set_err("omb_host_upload: padded edge m < n + 6");
   if (L <= 0) return 0;
   if (nchunks < 1) nchunks = 1;
   if (nchunks > L) nchunks = L;
@@ -1169,7 +1178,7 @@ int omb_host_upload(const double* const* leaf_u, int L, int n, long long fstride
     for (int c = 0; c < nchunks; c++) {
       int lo = lo_of(c), hi = lo_of(c + 1);
       int a = lo + (int)((long long)(hi - lo) * t / nt), b = lo + (int)((long long)(hi - lo) * (t + 1) / nt);
-      for (int i = a; i < b; i++) copy_leaf(leaf_u[i], pinned, i, n, fstride, true);
+      for (int i = a; i < b; i++) copy_leaf(leaf_u[i], pinned, i, n, m, fstride, true);
       // the thread finishing chunk c last hands it to the copy engine
       if (done[c].fetch_add(1, std::memory_order_acq_rel) == nt - 1) {
         cudaError_t e = cudaMemcpy2DAsync(dev + lo * n3, fstride * 8, pinned + lo * n3, fstride * 8,
@@ -1183,9 +1192,10 @@ int omb_host_upload(const double* const* leaf_u, int L, int n, long long fstride
   return 0;
 }
 
-int omb_host_download(const double* dev, double* pinned, int L, int n, long long fstride, double* const* leaf_u,
-                      int nchunks, void* stream) {
+int omb_host_download(const double* dev, double* pinned, int L, int n, int m, long long fstride,
+                      double* const* leaf_u, int nchunks, void* stream) {
   if (int rc = lib_init()) return rc;
+  if (bad_pitch(n, m)) return set_err("omb_host_download: padded edge m < n + 6");
   if (L <= 0) return 0;
   if (nchunks < 1) nchunks = 1;
   if (nchunks > L) nchunks = L;
@@ -1206,7 +1216,7 @@ int omb_host_download(const double* dev, double* pinned, int L, int n, long long
       if (cudaEventSynchronize(ev[c]) != cudaSuccess) { bad.store(1); return; }
       int lo = lo_of(c), hi = lo_of(c + 1);
       int a = lo + (int)((long long)(hi - lo) * t / nt), b = lo + (int)((long long)(hi - lo) * (t + 1) / nt);
-      for (int i = a; i < b; i++) copy_leaf(leaf_u[i], pinned, i, n, fstride, false);
+      for (int i = a; i < b; i++) copy_leaf(leaf_u[i], pinned, i, n, m, fstride, false);
     }
   };
   host_pool().run(work, nt);
@@ -1306,9 +1316,11 @@ int omb_host_scatter(const double* dev, const double* stash, int L, long long fs
    [bounds[c], bounds[c+1])) is copied on copy_stream once `ready[c]` (an event
    the caller recorded after the launch part that finishes those leaves) has
    fired, and unpacked by the host threads as soon as its copy is done. */
-int omb_host_download_after(const double* dev, double* pinned, int n, long long fstride, double* const* leaf_u,
-                            int nchunks, const int* bounds, void* const* ready, void* copy_stream) {
+int omb_host_download_after(const double* dev, double* pinned, int n, int m, long long fstride,
+                            double* const* leaf_u, int nchunks, const int* bounds, void* const* ready,
+                            void* copy_stream) {
   if (int rc = lib_init()) return rc;
+  if (bad_pitch(n, m)) return set_err("omb_host_download_after: padded edge m < n + 6");
   if (nchunks <= 0) return 0;
   const int L = bounds[nchunks];
   if (L <= 0) return 0;
@@ -1330,7 +1342,7 @@ int omb_host_download_after(const double* dev, double* pinned, int n, long long 
       if (cudaEventSynchronize(ev[c]) != cudaSuccess) { bad.store(1); return; }
       int lo = bounds[c], hi = bounds[c + 1];
       int a = lo + (int)((long long)(hi - lo) * t / nt), b = lo + (int)((long long)(hi - lo) * (t + 1) / nt);
-      for (int i = a; i < b; i++) copy_leaf(leaf_u[i], pinned, i, n, fstride, false);
+      for (int i = a; i < b; i++) copy_leaf(leaf_u[i], pinned, i, n, m, fstride, false);
     }
   };
   host_pool().run(work, nt);

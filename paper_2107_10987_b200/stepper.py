@@ -393,7 +393,7 @@ class B200HydroStepper:
         self._up_ev = torch.cuda.Event()
         ptrs = self._host_ptrs()
         if ptrs is not None:
-            _lib.check(self.lib.omb_host_upload(ptrs.ctypes.data, count, 8, b.fstride, ptr(self._pinned),
+            _lib.check(self.lib.omb_host_upload(ptrs.ctypes.data, count, 8, b.host_m, b.fstride, ptr(self._pinned),
                                                 ptr(self._buf[self._state]), self.TRANSFER_CHUNKS,
                                                 stream_handle(None)), "omb_host_upload")
         else:  # (not hybrid: its leaves are slab views)
@@ -421,7 +421,7 @@ class B200HydroStepper:
         ptrs = self._host_ptrs()
         if ptrs is not None:
             _lib.check(self.lib.omb_host_download(ptr(self._buf[self._state]), ptr(self._pinned), b.ncompute, 8,
-                                                  b.fstride, ptrs.ctypes.data, self.TRANSFER_CHUNKS,
+                                                  b.host_m, b.fstride, ptrs.ctypes.data, self.TRANSFER_CHUNKS,
                                                   stream_handle(None)), "omb_host_download")
             return
         self._pinned.copy_(self._buf[self._state])
@@ -477,8 +477,8 @@ class B200HydroStepper:
             bnd = np.minimum(bnd[:nparts + 1], k).astype(np.int32)
         if nparts > 0:
             ev = (ctypes.c_void_p * nparts)(*[e.cuda_event for e in t["events"][:nparts]])
-            _lib.check(self.lib.omb_host_download_after(ptr(self._buf[self._state]), ptr(self._pinned), 8, b.fstride,
-                                                        ptrs.ctypes.data, nparts, bnd.ctypes.data,
+            _lib.check(self.lib.omb_host_download_after(ptr(self._buf[self._state]), ptr(self._pinned), 8, b.host_m,
+                                                        b.fstride, ptrs.ctypes.data, nparts, bnd.ctypes.data,
                                                         ev, ctypes.c_void_p(t["stream"].cuda_stream)),
                        "omb_host_download_after")
         if side is not None:

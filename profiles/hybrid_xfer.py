@@ -47,7 +47,7 @@ def main(level=5):
             lib.omb_host_gather(ptr(m["ptrs"]) + 8 * k, nc - k, b.fstride, ptr(dev) + 8 * 512 * k,
                                 ptr(m["stash"]) + 8 * SS * k, ctypes.c_void_p(side.cuda_stream))
         if k > 0:
-            lib.omb_host_upload(hptrs.ctypes.data, k, 8, b.fstride, ptr(pinned), ptr(dev), 8, stream_handle(None))
+            lib.omb_host_upload(hptrs.ctypes.data, k, 8, 14, b.fstride, ptr(pinned), ptr(dev), 8, stream_handle(None))
         main_s.wait_stream(side)
 
     def down(f):
@@ -57,7 +57,7 @@ def main(level=5):
             lib.omb_host_scatter(ptr(dev) + 8 * 512 * k, ptr(m["stash"]) + 8 * SS * k, nc - k, b.fstride,
                                  ptr(m["ptrs"]) + 8 * k, ctypes.c_void_p(side.cuda_stream))
         if k > 0:
-            lib.omb_host_download(ptr(dev), ptr(pinned), k, 8, b.fstride, hptrs.ctypes.data, 8, stream_handle(None))
+            lib.omb_host_download(ptr(dev), ptr(pinned), k, 8, 14, b.fstride, hptrs.ctypes.data, 8, stream_handle(None))
         side.synchronize()
 
     def tm(fn, n=5):

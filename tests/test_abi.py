@@ -6,6 +6,7 @@ import os
 import re
 
 import numpy as np
+import pytest
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
@@ -59,22 +60,32 @@ def test_struct_layouts_match_header(tmp_path):
     assert got == checks
 
 
-def test_host_pack_roundtrip():
+@pytest.mark.parametrize("n,level", [(8, 2), (16, 1), (32, 1)])
+def test_host_pack_roundtrip(n, level):
+    """The native host packing (omb_host_pack / unpack: the copies of the e2e path) equals
+    the per-leaf numpy copies -- for 16^3 / 32^3 leaves block by block, straight out of the
+    leaf's padded array -- and the unpack leaves every ghost cell untouched."""
     import octomini_host as mesh
     from paper_2107_10987_b200 import _lib
     from paper_2107_10987_b200.batch import LeafBatch
 
-    t = mesh.build_uniform_tree(2, 8, boundary="periodic")
+    t = mesh.build_uniform_tree(level, n, boundary="periodic")
     rng = np.random.default_rng(0)
     for lf in t.leaves():
-        lf.subgrid.interior[:] = rng.normal(size=(6, 8, 8, 8))
+        lf.subgrid.u[...] = rng.normal(size=lf.subgrid.u.shape)
+    ghosts = [lf.subgrid.u.copy() for lf in t.sorted_leaves()]
     b = LeafBatch(t)
+    assert b.host_m == n + 6
     L = _lib.load()
     ref = b.pack()
     fast = b.pack(lib=L)
     assert np.array_equal(ref, fast)
     b.unpack(fast * 3.0, lib=L)
     assert np.array_equal(b.pack(), ref * 3.0)
+    for lf, g in zip(t.sorted_leaves(), ghosts):
+        g[:, 3:n + 3, 3:n + 3, 3:n + 3] *= 3.0
+        assert np.array_equal(lf.subgrid.u, g)
+    assert L.omb_host_pack(b._leaf_ptrs(b.L).ctypes.data, b.L, 8, 8, b.fstride, fast.ctypes.data) < 0  # m < n + 6
 
 
 def test_no_cpu_fallback_without_gpu():
