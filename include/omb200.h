@@ -217,8 +217,10 @@ int omb_gather_leaves(const double *u, long long fstride, const OmbLeafInfo *inf
  *   too small.  center [nent][3], width [nent], children [nent][8] (-1 for cells), is_cell [nent].
  * Device passes (stream-ordered): masses rho*dx^3 into the cell entities' M0 (M = [nent][20]);
  *   upward per level (parents [np] of that level); M2L per target entity with its contributions
- *   in the reference's order (off [ntarget+1] into contrib: source | group << 40 | flip << 63,
- *   D [G][2][20] kernel derivatives and their parity flip, cellcell [G]); downward per level;
+ *   in the reference's order (off [ntarget+1] into contrib: source | group << 40 | cell-cell << 62 | flip << 63,
+ *   D [G][2][20] kernel derivatives and their parity flip; cellcell non-NULL when the lists hold
+ *   cell-cell contributions -- the kernels read the kind from bit 62 of each word, which
+ *   omb_fmm_build sets); downward per level;
  *   fields phi / gx / gy / gz [nleaf][512] of the cell entities (cell_base [nleaf]). */
 long long omb_fmm_traverse(const double *center, const double *width, const long long *children,
                            const unsigned char *is_cell, long long nent, long long root, double theta,

@@ -109,7 +109,7 @@ __global__ void k_fmm_upward(const long long* parents, int np, const long long* 
 // ---------------------------------------------------------------------------
 // M2L: L[x] += contributions in the reference's order (_core.pyx:534-608)
 // ---------------------------------------------------------------------------
-// contribution word: source entity (bits 0..39) | group (40..62) | flip (63)
+// contribution word: source entity (bits 0..39) | group (40..61) | cell-cell (62) | flip (63)
 //
 // Two passes over each target's contributions, each owning a subset of the
 // 20 local components (every component still accumulates its contributions
@@ -132,36 +132,34 @@ __global__ void __launch_bounds__(128, 4) k_fmm_m2l(const long long* off, const 
   double l[KN];
 #pragma unroll
   for (int k = 0; k < KN; k++) l[k] = L[x * NC + K0 + k];
-  // software pipeline over the (dependent-load) chain: the next contribution's
-  // word is loaded while this one is processed
-  const long long q1 = off[ti + 1];
-  unsigned long long wn = off[ti] < q1 ? __ldg(contrib + off[ti]) : 0ull;
-  for (long long q = off[ti]; q < q1; q++) {
-    unsigned long long w = wn;
-    if (q + 1 < q1) wn = __ldg(contrib + q + 1);
+  // one contribution, added in the list's order
+  auto add = [&](unsigned long long w) {
     long long src = (long long)(w & 0xFFFFFFFFFFull);
-    long long g = (long long)((w >> 40) & 0x7FFFFFull);
+    long long g = (long long)((w >> 40) & 0x3FFFFFull);
     int flip = (int)(w >> 63);
     const double* Dg = D + (g * 2 + flip) * NC;
     const double* Ms = M + src * NC;
-    if (cellcell && cellcell[g]) {  // (null: a list without cell-cell contributions)
-      // L[eb,0] += ma*D0; L[eb,c] += ma*D_c; L[ea,0] += mb*D0; L[ea,c] += mb*(-D_c)
-      // (the flipped D holds -D_c: x*(-d) is the reference's mb*(-D1))
-      if (PART == 0) {
-        // the monopole from the compact mass array when given (8 B per entity: L2-resident,
-        // where the 160 B moment records are not)
-        double m = M0c ? __ldg(M0c + src) : __ldg(Ms);
-        l[0] += m * __ldg(Dg);
-#pragma unroll
-        for (int c = 0; c < 3; c++) l[1 + c] += m * __ldg(Dg + 1 + c);
-      }
-      continue;
-    }
-    double M0 = __ldg(Ms);
+    bool cc = cellcell && ((w >> 62) & 1);  // (null: a list without cell-cell contributions)
     if (PART == 0) {
-      double acc = __ldg(Dg) * M0;
+      // the loads both kinds of contribution need go out at once, before the kind is known: the
+      // monopole (from the compact mass array when given -- 8 B per entity, L2-resident where the
+      // 160 B moment records are not; the same value) and D0..D3, as two 16-byte loads (D rows
+      // are 160 B): a warp's lanes read up to 32 different rows, so each load instruction costs
+      // up to one L1 wavefront per lane -- half as many instructions this way (c5g FMM 27.4 ->
+      // 26.4 ms per stage, profiles/r02/abf5_m2l_vec.txt)
+      double M0 = M0c ? __ldg(M0c + src) : __ldg(Ms);
+      double2 da = __ldg(reinterpret_cast<const double2*>(Dg)), db = __ldg(reinterpret_cast<const double2*>(Dg + 2));
+      double d[4] = {da.x, da.y, db.x, db.y};
+      if (cc) {
+        // L[eb,0] += ma*D0; L[eb,c] += ma*D_c; L[ea,0] += mb*D0; L[ea,c] += mb*(-D_c)
+        // (the flipped D holds -D_c: x*(-d) is the reference's mb*(-D1))
 #pragma unroll
-      for (int a = 0; a < 3; a++) acc = acc - __ldg(Dg + 1 + a) * __ldg(Ms + 1 + a);
+        for (int c = 0; c < 4; c++) l[c] += M0 * d[c];
+        return;
+      }
+      double acc = d[0] * M0;
+#pragma unroll
+      for (int a = 0; a < 3; a++) acc = acc - d[1 + a] * __ldg(Ms + 1 + a);
 #pragma unroll
       for (int i = 0; i < 6; i++) acc = acc + ((0.5 * c_mult2[i]) * __ldg(Dg + 4 + i)) * __ldg(Ms + 4 + i);
 #pragma unroll
@@ -169,7 +167,7 @@ __global__ void __launch_bounds__(128, 4) k_fmm_m2l(const long long* off, const 
       l[0] += acc;
 #pragma unroll
       for (int a = 0; a < 3; a++) {
-        acc = __ldg(Dg + 1 + a) * M0;
+        acc = d[1 + a] * M0;
 #pragma unroll
         for (int b = 0; b < 3; b++) acc = acc - __ldg(Dg + 4 + idx2(a, b)) * __ldg(Ms + 1 + b);
 #pragma unroll
@@ -178,6 +176,8 @@ __global__ void __launch_bounds__(128, 4) k_fmm_m2l(const long long* off, const 
         l[1 + a] += acc;
       }
     } else {
+      if (cc) return;  // (PART 1 lists hold none)
+      double M0 = __ldg(Ms);
 #pragma unroll
       for (int i = 0; i < 6; i++) {
         double acc = __ldg(Dg + 4 + i) * M0;
@@ -188,7 +188,23 @@ __global__ void __launch_bounds__(128, 4) k_fmm_m2l(const long long* off, const 
 #pragma unroll
       for (int i = 0; i < 10; i++) l[6 + i] += __ldg(Dg + 10 + i) * M0;
     }
+  };
+  long long q = off[ti];
+  const long long q1 = off[ti + 1];
+  // the words two at a time (16-byte loads at even positions), the next pair in flight while
+  // this one is added: each lane reads its own list, so a warp's load costs up to one L1
+  // wavefront per lane -- half as many loads (c5g FMM 27.6 -> 25.4 ms per stage with the
+  // 16-byte D loads, profiles/r02/abf6_m2l_pairs.txt)
+  if (q & 1) add(__ldg(contrib + q++));
+  const ulonglong2* cp = reinterpret_cast<const ulonglong2*>(contrib);
+  ulonglong2 wn = q + 1 < q1 ? __ldg(cp + (q >> 1)) : make_ulonglong2(0ull, 0ull);
+  for (; q + 1 < q1; q += 2) {
+    ulonglong2 w = wn;
+    if (q + 3 < q1) wn = __ldg(cp + (q >> 1) + 1);
+    add(w.x);
+    add(w.y);
   }
+  if (q < q1) add(__ldg(contrib + q));
 #pragma unroll
   for (int k = 0; k < KN; k++) L[x * NC + K0 + k] = l[k];
 }
@@ -414,8 +430,9 @@ long long omb_fmm_traverse(const double* center, const double* width, const long
 // pair, (b <- a, D) before (a <- b, flipped D) (_core.pyx:583-608).
 // Outputs: ngroups, group_first [G] (discovery index of the group's first
 // pair, for R), group_flags [G] (2*a_cell + b_cell), off [nent+1] (CSR over
-// ALL entities), contrib [2*np] (source | group << 40 | flip << 63).
-// Returns G, or -1 if G exceeds gcap.
+// ALL entities), contrib [2*np] (source | group << 40 | cell-cell << 62 | flip << 63;
+// cell-cell = both entities of the group's pairs are cells: group_flags == 3).
+// Returns G, or -1 if G exceeds gcap or 2^22.
 long long omb_fmm_build(const long long* pa, const long long* pb, const long long* pk, long long np, long long nent,
                         long long* group_first, unsigned char* group_flags, long long gcap, long long* off,
                         unsigned long long* contrib) {
@@ -427,7 +444,7 @@ long long omb_fmm_build(const long long* pa, const long long* pb, const long lon
   for (auto& kv : first) keys.push_back(kv.first);
   std::sort(keys.begin(), keys.end());
   long long G = (long long)keys.size();
-  if (G > gcap) return -1;
+  if (G > gcap || G > (1LL << 22)) return -1;
   std::unordered_map<long long, long long> gid;
   gid.reserve(2 * G);
   for (long long g = 0; g < G; g++) {
@@ -455,8 +472,9 @@ long long omb_fmm_build(const long long* pa, const long long* pb, const long lon
   for (long long r = 0; r < np; r++) {
     long long i = order[r];
     unsigned long long g = (unsigned long long)pg[i];
-    contrib[pos[pb[i]]++] = (unsigned long long)pa[i] | (g << 40);
-    contrib[pos[pa[i]]++] = (unsigned long long)pb[i] | (g << 40) | (1ull << 63);
+    unsigned long long cc = group_flags[pg[i]] == 3 ? 1ull << 62 : 0ull;
+    contrib[pos[pb[i]]++] = (unsigned long long)pa[i] | (g << 40) | cc;
+    contrib[pos[pa[i]]++] = (unsigned long long)pb[i] | (g << 40) | cc | (1ull << 63);
   }
   return G;
 }

@@ -254,7 +254,7 @@ class B200FmmSolver:
         del contrib
         # the L4..L19 pass needs no cell-cell contribution (90 % of them at theta 0.5): its
         # lists are the subsequence of the others, same order, CSR over the same targets
-        g = (self._contrib >> 40) & 0x7FFFFF
+        g = (self._contrib >> 40) & 0x3FFFFF  # (bits 40..61; bit 62 flags the cell-cell words)
         keep = self._cellcell[g] == 0
         del g
         cs = T.cumsum(keep, 0)
