@@ -38,13 +38,19 @@ namespace {
 
 constexpr int NC = 20;  // [M0, M1(3), M2(6), M3(10)]
 // symmetric tensor component tables (multipole.py:21-42)
-__constant__ int c_s2a[6] = {0, 0, 0, 1, 1, 2};
-__constant__ int c_s2b[6] = {0, 1, 2, 1, 2, 2};
-__constant__ int c_s3a[10] = {0, 0, 0, 0, 0, 0, 1, 1, 1, 2};
-__constant__ int c_s3b[10] = {0, 0, 0, 1, 1, 2, 1, 1, 2, 2};
-__constant__ int c_s3c[10] = {0, 1, 2, 1, 2, 2, 1, 2, 2, 2};
-__constant__ double c_mult2[6] = {1.0, 2.0, 2.0, 1.0, 2.0, 1.0};
-__constant__ double c_mult3[10] = {1.0, 3.0, 3.0, 3.0, 6.0, 3.0, 1.0, 3.0, 3.0, 1.0};
+// as arithmetic on the (unrolled, constant) index, so the compiler folds them and the
+// register arrays they index stay in registers (constant-bank tables sent those arrays to
+// local memory)
+//   S2: 00 01 02 11 12 22;  S3: 000 001 002 011 012 022 111 112 122 222
+__device__ __forceinline__ int c_s2a(int i) { return i < 3 ? 0 : (i < 5 ? 1 : 2); }
+__device__ __forceinline__ int c_s2b(int i) { return i < 3 ? i : (i < 5 ? i - 2 : 2); }
+__device__ __forceinline__ int c_s3a(int i) { return i < 6 ? 0 : (i < 9 ? 1 : 2); }
+__device__ __forceinline__ int c_s3b(int i) { return i < 3 ? 0 : (i < 5 ? 1 : (i == 5 ? 2 : (i < 8 ? 1 : 2))); }
+__device__ __forceinline__ int c_s3c(int i) {
+  return i < 3 ? i : (i == 3 ? 1 : (i < 6 ? 2 : (i == 6 ? 1 : 2)));
+}
+__device__ __forceinline__ double c_mult2(int i) { return (i == 1 || i == 2 || i == 4) ? 2.0 : 1.0; }
+__device__ __forceinline__ double c_mult3(int i) { return i == 4 ? 6.0 : ((i == 0 || i == 6 || i == 9) ? 1.0 : 3.0); }
 
 __device__ __forceinline__ int idx2(int a, int b) {  // (a,b) -> 0..5
   int lo = a < b ? a : b, hi = a < b ? b : a;
@@ -77,11 +83,11 @@ __device__ void translate_add(const double* f, const double t[3], double* out, b
   r[0] = M0;
   for (int a = 0; a < 3; a++) r[1 + a] = f[1 + a] + M0 * t[a];
   for (int i = 0; i < 6; i++) {
-    int a = c_s2a[i], b = c_s2b[i];
+    int a = c_s2a(i), b = c_s2b(i);
     r[4 + i] = ((f[4 + i] + f[1 + a] * t[b]) + f[1 + b] * t[a]) + (M0 * t[a]) * t[b];
   }
   for (int i = 0; i < 10; i++) {
-    int a = c_s3a[i], b = c_s3b[i], c = c_s3c[i];
+    int a = c_s3a(i), b = c_s3b(i), c = c_s3c(i);
     double m2ab = f[4 + idx2(a, b)], m2ac = f[4 + idx2(a, c)], m2bc = f[4 + idx2(b, c)];
     r[10 + i] = ((((((f[10 + i] + m2ab * t[c]) + m2ac * t[b]) + m2bc * t[a]) + (f[1 + a] * t[b]) * t[c]) +
                   (f[1 + b] * t[a]) * t[c]) +
@@ -157,36 +163,59 @@ __global__ void __launch_bounds__(128, 4) k_fmm_m2l(const long long* off, const 
         for (int c = 0; c < 4; c++) l[c] += M0 * d[c];
         return;
       }
+      // the moment and derivative rows by 16-byte loads (rows are 160 B), into register arrays
+      // whose indices all fold to constants
+      double m[20], dg[20];
+#pragma unroll
+      for (int i = 0; i < 10; i++) {
+        double2 mv = __ldg(reinterpret_cast<const double2*>(Ms) + i);
+        m[2 * i] = mv.x;
+        m[2 * i + 1] = mv.y;
+      }
+#pragma unroll
+      for (int i = 2; i < 10; i++) {
+        double2 dv = __ldg(reinterpret_cast<const double2*>(Dg) + i);
+        dg[2 * i] = dv.x;
+        dg[2 * i + 1] = dv.y;
+      }
       double acc = d[0] * M0;
 #pragma unroll
-      for (int a = 0; a < 3; a++) acc = acc - d[1 + a] * __ldg(Ms + 1 + a);
+      for (int a = 0; a < 3; a++) acc = acc - d[1 + a] * m[1 + a];
 #pragma unroll
-      for (int i = 0; i < 6; i++) acc = acc + ((0.5 * c_mult2[i]) * __ldg(Dg + 4 + i)) * __ldg(Ms + 4 + i);
+      for (int i = 0; i < 6; i++) acc = acc + ((0.5 * c_mult2(i)) * dg[4 + i]) * m[4 + i];
 #pragma unroll
-      for (int i = 0; i < 10; i++) acc = acc - ((c_mult3[i] / 6.0) * __ldg(Dg + 10 + i)) * __ldg(Ms + 10 + i);
+      for (int i = 0; i < 10; i++) acc = acc - ((c_mult3(i) / 6.0) * dg[10 + i]) * m[10 + i];
       l[0] += acc;
 #pragma unroll
       for (int a = 0; a < 3; a++) {
         acc = d[1 + a] * M0;
 #pragma unroll
-        for (int b = 0; b < 3; b++) acc = acc - __ldg(Dg + 4 + idx2(a, b)) * __ldg(Ms + 1 + b);
+        for (int b = 0; b < 3; b++) acc = acc - dg[4 + idx2(a, b)] * m[1 + b];
 #pragma unroll
         for (int i = 0; i < 6; i++)
-          acc = acc + ((0.5 * c_mult2[i]) * __ldg(Dg + 10 + idx3(a, c_s2a[i], c_s2b[i]))) * __ldg(Ms + 4 + i);
+          acc = acc + ((0.5 * c_mult2(i)) * dg[10 + idx3(a, c_s2a(i), c_s2b(i))]) * m[4 + i];
         l[1 + a] += acc;
       }
     } else {
       if (cc) return;  // (PART 1 lists hold none)
-      double M0 = __ldg(Ms);
+      double2 m01 = __ldg(reinterpret_cast<const double2*>(Ms)), m23 = __ldg(reinterpret_cast<const double2*>(Ms) + 1);
+      double m[4] = {m01.x, m01.y, m23.x, m23.y}, dg[20];
+#pragma unroll
+      for (int i = 2; i < 10; i++) {
+        double2 dv = __ldg(reinterpret_cast<const double2*>(Dg) + i);
+        dg[2 * i] = dv.x;
+        dg[2 * i + 1] = dv.y;
+      }
+      double M0 = m[0];
 #pragma unroll
       for (int i = 0; i < 6; i++) {
-        double acc = __ldg(Dg + 4 + i) * M0;
+        double acc = dg[4 + i] * M0;
 #pragma unroll
-        for (int b = 0; b < 3; b++) acc = acc - __ldg(Dg + 10 + idx3(c_s2a[i], c_s2b[i], b)) * __ldg(Ms + 1 + b);
+        for (int b = 0; b < 3; b++) acc = acc - dg[10 + idx3(c_s2a(i), c_s2b(i), b)] * m[1 + b];
         l[i] += acc;
       }
 #pragma unroll
-      for (int i = 0; i < 10; i++) l[6 + i] += __ldg(Dg + 10 + i) * M0;
+      for (int i = 0; i < 10; i++) l[6 + i] += dg[10 + i] * M0;
     }
   };
   long long q = off[ti];
@@ -216,25 +245,25 @@ __device__ void translate_local(const double* f, const double s[3], double* out)
   double acc0 = f[0];
   for (int a = 0; a < 3; a++) acc0 = acc0 + f[1 + a] * s[a];
   for (int i = 0; i < 6; i++) {
-    int a = c_s2a[i], b = c_s2b[i];
-    acc0 = acc0 + (((0.5 * c_mult2[i]) * f[4 + i]) * s[a]) * s[b];
+    int a = c_s2a(i), b = c_s2b(i);
+    acc0 = acc0 + (((0.5 * c_mult2(i)) * f[4 + i]) * s[a]) * s[b];
   }
   for (int i = 0; i < 10; i++) {
-    int a = c_s3a[i], b = c_s3b[i], c = c_s3c[i];
-    acc0 = acc0 + ((((c_mult3[i] / 6.0) * f[10 + i]) * s[a]) * s[b]) * s[c];
+    int a = c_s3a(i), b = c_s3b(i), c = c_s3c(i);
+    acc0 = acc0 + ((((c_mult3(i) / 6.0) * f[10 + i]) * s[a]) * s[b]) * s[c];
   }
   out[0] = acc0;
   for (int a = 0; a < 3; a++) {
     double acc = f[1 + a];
     for (int b = 0; b < 3; b++) acc = acc + f[4 + idx2(a, b)] * s[b];
     for (int i = 0; i < 6; i++) {
-      int b = c_s2a[i], c = c_s2b[i];
-      acc = acc + (((0.5 * c_mult2[i]) * f[10 + idx3(a, b, c)]) * s[b]) * s[c];
+      int b = c_s2a(i), c = c_s2b(i);
+      acc = acc + (((0.5 * c_mult2(i)) * f[10 + idx3(a, b, c)]) * s[b]) * s[c];
     }
     out[1 + a] = acc;
   }
   for (int i = 0; i < 6; i++) {
-    int a = c_s2a[i], b = c_s2b[i];
+    int a = c_s2a(i), b = c_s2b(i);
     double acc = f[4 + i];
     for (int c = 0; c < 3; c++) acc = acc + f[10 + idx3(a, b, c)] * s[c];
     out[4 + i] = acc;
