@@ -121,10 +121,13 @@ __global__ void k_fmm_upward(const long long* parents, int np, const long long* 
 // 20 local components (every component still accumulates its contributions
 // in the reference's order, so the split is exact): PART 0 = L0..L3 (needs
 // all of M and D), PART 1 = L4..L19 (needs M0..M3 and D4..D19).  Fewer live
-// accumulators per pass: 128 registers, twice the warps of the fused pass
-// against the latency of the source-moment loads.
+// accumulators per pass: fewer registers, more warps against the latency of
+// the source-moment loads.
+// 5 blocks of 128 per SM (<= 102 registers, no spills once the tensor tables fold): 20 warps
+// against the load latency instead of 16 (c5g FMM 15.6 -> 14.2 ms per stage; 6 blocks spill:
+// profiles/r02/abf9_abf10_m2l_occupancy.txt)
 template <int PART>
-__global__ void __launch_bounds__(128, 4) k_fmm_m2l(const long long* off, const unsigned long long* contrib,
+__global__ void __launch_bounds__(128, 5) k_fmm_m2l(const long long* off, const unsigned long long* contrib,
                                                     const double* D /*[G][2][20]*/, const unsigned char* cellcell,
                                                     const double* M, double* L, long long ntarget,
                                                     const long long* targets, const long long* subset,
