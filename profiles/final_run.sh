@@ -14,3 +14,5 @@ python bench.py --config c5g --steps 5 --warmup 3 --e2e-steps 2 > gpurun_out/${T
 python bench.py --subgrid 16 --steps 30 --e2e-steps 2 --no-cpu-baseline > gpurun_out/${TAG}_n16.json 2> gpurun_out/${TAG}_n16.err
 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29611 \
   bench.py --gpus 2 --config c4 > gpurun_out/${TAG}_c4_n2.json 2> gpurun_out/${TAG}_c4_n2.err
+python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29612 \
+  bench.py --gpus 2 --config c5g --steps 5 --warmup 3 --e2e-steps 2 > gpurun_out/${TAG}_c5g_n2.json 2> gpurun_out/${TAG}_c5g_n2.err
