@@ -945,7 +945,13 @@ OMB_HD double amr_cell(const double* U, long long fstride, const int* t, int v, 
     k[a] = c[a] >= N / 2 ? 1 : 0;
     f[a] = 2 * c[a] - k[a] * N;
   }
-  const double* F = Uv + (long long)t[5 + k[0] + 2 * k[1] + 4 * k[2]] * 512;
+  // the covering child: a select over the 8 (a runtime index into t would send the caller's
+  // register copy of the task to local memory)
+  const int ci = k[0] + 2 * k[1] + 4 * k[2];
+  int child = t[5];
+#pragma unroll
+  for (int j = 1; j < 8; j++) child = ci == j ? t[5 + j] : child;
+  const double* F = Uv + (long long)child * 512;
   auto at = [&](int x, int y, int z) { return F[(f[0] + x) * 64 + (f[1] + y) * 8 + (f[2] + z)]; };
   return 0.125 * (((at(0, 0, 0) + at(1, 0, 0)) + (at(0, 1, 0) + at(1, 1, 0))) +
                   ((at(0, 0, 1) + at(1, 0, 1)) + (at(0, 1, 1) + at(1, 1, 1))));
