@@ -19,7 +19,7 @@ EXPORTS = ("omb_abi_version", "omb_last_error", "omb_stage_smem_bytes", "omb_pri
            "omb_fluxes", "omb_stage", "omb_cfl", "omb_gather", "omb_gather_leaves", "omb_fp64_peak", "omb_pack_leaves", "omb_unpack_leaves", "omb_selftest_div", "omb_selftest_pow", "omb_kt_flux", "omb_physical_flux", "omb_face_flux", "omb_scalar_input", "omb_host_pack", "omb_host_unpack", "omb_host_upload", "omb_host_download", "omb_host_download_after", "omb_host_gather", "omb_host_scatter", "omb_set_host_threads", "omb_amr_ghosts",
            "omb_reflux_update", "omb_leaf_sums", "omb_disk_order",
            "omb_gather_rows", "omb_scatter_rows", "omb_enable_peer_access", "omb_ipc_alloc", "omb_ipc_open",
-           "omb_fmm_traverse", "omb_fmm_build", "omb_fmm_build_direct", "omb_fmm_direct", "omb_fmm_masses", "omb_fmm_upward", "omb_fmm_m2l", "omb_fmm_m2l_part", "omb_fmm_downward",
+           "omb_fmm_traverse", "omb_fmm_build", "omb_fmm_build_direct", "omb_fmm_direct", "omb_fmm_masses", "omb_fmm_upward", "omb_fmm_m2l", "omb_fmm_m2l_part", "omb_fmm_m2l0_pair", "omb_fmm_downward",
            "omb_fmm_fields", "omb_fmm_rhodot", "omb_fmm_last_error")
 
 
@@ -74,6 +74,7 @@ def load():
     L.omb_fmm_upward.argtypes = [vp, i, vp, vp, vp, vp]
     L.omb_fmm_m2l.argtypes = [vp, vp, vp, vp, vp, vp, ll, vp, vp, vp]
     L.omb_fmm_m2l_part.argtypes = [i, vp, vp, vp, vp, vp, vp, ll, vp, vp, vp, ll, vp]
+    L.omb_fmm_m2l0_pair.argtypes = [vp, vp, vp, vp, vp, vp, vp, vp, ll, vp, vp, vp, vp, ll, vp]
     L.omb_fmm_downward.argtypes = [vp, i, vp, vp, vp, vp]
     L.omb_fmm_fields.argtypes = [vp, vp, i, vp, vp, vp, vp, vp]
     L.omb_fmm_rhodot.argtypes = [vp, ll, vp, i, i, vp, i, vp, vp]

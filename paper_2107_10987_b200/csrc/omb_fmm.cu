@@ -241,6 +241,99 @@ __global__ void __launch_bounds__(128, 5) k_fmm_m2l(const long long* off, const 
   for (int k = 0; k < KN; k++) L[x * NC + K0 + k] = l[k];
 }
 
+// PART 0 for two solves over the same lists at once (the stage's density and rho_dot solves:
+// same tree, same interactions, different masses): each contribution word and D row is read once
+// for both.  Each solve's accumulators see its contributions in the list's order, as in k_fmm_m2l.
+// c5g FMM 14.2 -> 12.4 ms per stage; 4 blocks per SM (3: 12.9, 5: spills, 16.0 ms;
+// profiles/r02/abf12_abf13_m2l_pair.txt)
+__device__ __forceinline__ void m2l0_general(const double* d, const double* dg, const double* Ms, double M0,
+                                             double* l) {
+  double m[20];
+#pragma unroll
+  for (int i = 0; i < 10; i++) {
+    double2 mv = __ldg(reinterpret_cast<const double2*>(Ms) + i);
+    m[2 * i] = mv.x;
+    m[2 * i + 1] = mv.y;
+  }
+  double acc = d[0] * M0;
+#pragma unroll
+  for (int a = 0; a < 3; a++) acc = acc - d[1 + a] * m[1 + a];
+#pragma unroll
+  for (int i = 0; i < 6; i++) acc = acc + ((0.5 * c_mult2(i)) * dg[4 + i]) * m[4 + i];
+#pragma unroll
+  for (int i = 0; i < 10; i++) acc = acc - ((c_mult3(i) / 6.0) * dg[10 + i]) * m[10 + i];
+  l[0] += acc;
+#pragma unroll
+  for (int a = 0; a < 3; a++) {
+    acc = d[1 + a] * M0;
+#pragma unroll
+    for (int b = 0; b < 3; b++) acc = acc - dg[4 + idx2(a, b)] * m[1 + b];
+#pragma unroll
+    for (int i = 0; i < 6; i++) acc = acc + ((0.5 * c_mult2(i)) * dg[10 + idx3(a, c_s2a(i), c_s2b(i))]) * m[4 + i];
+    l[1 + a] += acc;
+  }
+}
+
+__global__ void __launch_bounds__(128, 4) k_fmm_m2l0_pair(const long long* off, const unsigned long long* contrib,
+                                                          const double* D, const unsigned char* cellcell,
+                                                          const double* Ma, const double* Mb, double* La, double* Lb,
+                                                          long long ntarget, const long long* targets,
+                                                          const long long* subset, const double* M0a,
+                                                          const double* M0b) {
+  long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (k >= ntarget) return;
+  long long ti = subset ? subset[k] : k;
+  if (off[ti] == off[ti + 1]) return;
+  long long x = targets[ti];
+  double la[4], lb[4];
+#pragma unroll
+  for (int c = 0; c < 4; c++) {
+    la[c] = La[x * NC + c];
+    lb[c] = Lb[x * NC + c];
+  }
+  auto add = [&](unsigned long long w) {
+    long long src = (long long)(w & 0xFFFFFFFFFFull);
+    long long g = (long long)((w >> 40) & 0x3FFFFFull);
+    const double* Dg = D + (g * 2 + (int)(w >> 63)) * NC;
+    double ma = __ldg(M0a + src), mb = __ldg(M0b + src);
+    double2 da = __ldg(reinterpret_cast<const double2*>(Dg)), db = __ldg(reinterpret_cast<const double2*>(Dg + 2));
+    double d[4] = {da.x, da.y, db.x, db.y};
+    if (cellcell && ((w >> 62) & 1)) {
+#pragma unroll
+      for (int c = 0; c < 4; c++) la[c] += ma * d[c];
+#pragma unroll
+      for (int c = 0; c < 4; c++) lb[c] += mb * d[c];
+      return;
+    }
+    double dg[20];
+#pragma unroll
+    for (int i = 2; i < 10; i++) {
+      double2 dv = __ldg(reinterpret_cast<const double2*>(Dg) + i);
+      dg[2 * i] = dv.x;
+      dg[2 * i + 1] = dv.y;
+    }
+    m2l0_general(d, dg, Ma + src * NC, ma, la);
+    m2l0_general(d, dg, Mb + src * NC, mb, lb);
+  };
+  long long q = off[ti];
+  const long long q1 = off[ti + 1];
+  if (q & 1) add(__ldg(contrib + q++));
+  const ulonglong2* cp = reinterpret_cast<const ulonglong2*>(contrib);
+  ulonglong2 wn = q + 1 < q1 ? __ldg(cp + (q >> 1)) : make_ulonglong2(0ull, 0ull);
+  for (; q + 1 < q1; q += 2) {
+    ulonglong2 w = wn;
+    if (q + 3 < q1) wn = __ldg(cp + (q >> 1) + 1);
+    add(w.x);
+    add(w.y);
+  }
+  if (q < q1) add(__ldg(contrib + q));
+#pragma unroll
+  for (int c = 0; c < 4; c++) {
+    La[x * NC + c] = la[c];
+    Lb[x * NC + c] = lb[c];
+  }
+}
+
 // ---------------------------------------------------------------------------
 // downward: L[child] += translate_local(L[p], center[child] - center[p])
 // ---------------------------------------------------------------------------
@@ -590,6 +683,23 @@ int omb_fmm_m2l_part(int part, const long long* off, const unsigned long long* c
     k_fmm_m2l<1><<<nb, 128, 0, (cudaStream_t)stream>>>(off, contrib, D, cellcell, M, L, ntarget, targets, subset);
   cudaError_t e = cudaGetLastError();
   return e == cudaSuccess ? 0 : ferr("omb_fmm_m2l_part", e);
+}
+
+int omb_fmm_m2l0_pair(const long long* off, const unsigned long long* contrib, const double* D,
+                      const unsigned char* cellcell, const double* Ma, const double* Mb, double* La, double* Lb,
+                      long long ntarget, const long long* targets, const long long* subset, double* m0a,
+                      double* m0b, long long nentities, void* stream) {
+  if (ntarget <= 0) return 0;
+  if (!m0a || !m0b || nentities <= 0) return ferr("omb_fmm_m2l0_pair", cudaErrorInvalidValue);
+  long long b = (nentities + 255) / 256;
+  unsigned gb = (unsigned)(b < 148 * 16 ? b : 148 * 16);
+  k_fmm_m0<<<gb, 256, 0, (cudaStream_t)stream>>>(Ma, nentities, m0a);
+  k_fmm_m0<<<gb, 256, 0, (cudaStream_t)stream>>>(Mb, nentities, m0b);
+  unsigned nb = (unsigned)((ntarget + 127) / 128);
+  k_fmm_m2l0_pair<<<nb, 128, 0, (cudaStream_t)stream>>>(off, contrib, D, cellcell, Ma, Mb, La, Lb, ntarget, targets,
+                                                        subset, m0a, m0b);
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? 0 : ferr("omb_fmm_m2l0_pair", e);
 }
 
 int omb_fmm_downward(const long long* parents, int np, const long long* children, const double* center, double* L,

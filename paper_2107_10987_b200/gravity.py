@@ -19,6 +19,8 @@ Every floating-point operation keeps the reference's order, so phi and g are
 bitwise those of the reference's compiled backend (tests/test_fmm.py).
 """
 
+import os
+
 import numpy as np
 
 from . import _lib
@@ -370,7 +372,8 @@ class B200FmmSolver:
         monopole copy and the two M2L passes, downward levels, fields) + the
         -div(momentum) source."""
         per = 2 if self.theta == 0.0 else 5 + len(self._up) + len(self._down)
-        return 2 * per + 1
+        paired = self.theta != 0.0 and os.environ.get("OMB_FMM_PAIR", "1") != "0"
+        return 2 * per + 1 - (1 if paired else 0)  # (paired: one pass-0 launch for both solves)
 
     def stage_fields(self, U, fstride, info, bc, nleaf, grav, stream=None):
         """The stepper's per-stage solve (solver.py:134-153 on device data):
@@ -386,10 +389,57 @@ class B200FmmSolver:
             self._scratch = torch.empty(2 * n, dtype=torch.float64, device=self.dev)
         phi, rhodot = self._scratch[:n], self._scratch[n:2 * n]
         G = grav.reshape(4, -1)
+        if self.theta != 0.0 and os.environ.get("OMB_FMM_PAIR", "1") != "0":
+            # both solves at once (one pass over the interaction lists for the two mass sets)
+            _lib.check(lib.omb_fmm_rhodot(ptr(U), fstride, ptr(info), bc, nleaf, None, 0, ptr(rhodot), sh),
+                       "omb_fmm_rhodot")
+            self._run_pair(U[:n], rhodot, self._dx3_dev, stream)
+            _lib.check(lib.omb_fmm_fields(ptr(self._L), ptr(self._cell_base), nleaf, ptr(phi), ptr(G[0]),
+                                          ptr(G[1]), ptr(G[2]), sh), "omb_fmm_fields")
+            _lib.check(lib.omb_fmm_fields(ptr(self._L2), ptr(self._cell_base), nleaf, ptr(G[3]), ptr(phi),
+                                          ptr(phi), ptr(phi), sh), "omb_fmm_fields")
+            return
         self._solve_into(U[:n], self._dx3_dev, phi, G[0], G[1], G[2], stream)
         _lib.check(lib.omb_fmm_rhodot(ptr(U), fstride, ptr(info), bc, nleaf, None, 0, ptr(rhodot), sh),
                    "omb_fmm_rhodot")
         self._solve_into(rhodot, self._dx3_dev, G[3], phi, phi, phi, stream)
+
+    def _run_pair(self, rho_a, rho_b, dx3_dev, stream=None):
+        """Two solves (masses rho_a, rho_b) sharing the pass over the interaction lists:
+        L of a in self._L, of b in self._L2.  Each solve bitwise as _run alone."""
+        import torch
+
+        lib, sh = self.lib, stream_handle(stream)
+        nleaf = len(self.table.leaf_paths)
+        if getattr(self, "_M2", None) is None:
+            self._M2 = torch.zeros_like(self._M)
+            self._L2 = torch.zeros_like(self._L)
+            self._M0c2 = torch.zeros_like(self._M0c)
+        for M, L in ((self._M, self._L), (self._M2, self._L2)):
+            M.zero_()
+            L.zero_()
+        for rho, M in ((rho_a, self._M), (rho_b, self._M2)):
+            _lib.check(lib.omb_fmm_masses(ptr(rho), ptr(self._cell_base), nleaf, ptr(dx3_dev), ptr(M), sh),
+                       "omb_fmm_masses")
+            for _, par in self._up:
+                _lib.check(lib.omb_fmm_upward(ptr(par), int(par.numel()), ptr(self._children), ptr(self._center),
+                                              ptr(M), sh), "omb_fmm_upward")
+        sub = getattr(self, "_subset", None)
+        nt = int(sub.numel()) if sub is not None else int(self._targets.numel())
+        order = self._target_order(0, self._off, sub)
+        _lib.check(lib.omb_fmm_m2l0_pair(ptr(self._off), ptr(self._contrib), ptr(self._D), ptr(self._cellcell),
+                                         ptr(self._M), ptr(self._M2), ptr(self._L), ptr(self._L2), nt,
+                                         ptr(self._targets), ptr(order), ptr(self._M0c), ptr(self._M0c2),
+                                         self.table.nentities, sh), "omb_fmm_m2l0_pair")
+        order = self._target_order(1, self._off1, sub)
+        for M, L in ((self._M, self._L), (self._M2, self._L2)):
+            _lib.check(lib.omb_fmm_m2l_part(1, ptr(self._off1), ptr(self._contrib1), ptr(self._D), None, ptr(M),
+                                            ptr(L), nt, ptr(self._targets), ptr(order), None, self.table.nentities,
+                                            sh), "omb_fmm_m2l_part")
+        for L in (self._L, self._L2):
+            for _, par in self._down:
+                _lib.check(lib.omb_fmm_downward(ptr(par), int(par.numel()), ptr(self._children), ptr(self._center),
+                                                ptr(L), sh), "omb_fmm_downward")
 
     # -- leaf-partitioned runs (one rank per GPU) -------------------------------
     def set_partition(self, part):
