@@ -498,6 +498,13 @@ class B200FmmSolver:
             self._rho_all[a:b].copy_(ga[r, 0, :b - a])
             self._rho_all[G * 512 + a:G * 512 + b].copy_(ga[r, 1, :b - a])
         Gv = grav.reshape(4, -1)
+        if os.environ.get("OMB_FMM_PAIR", "1") != "0":  # both solves in one pass over the lists
+            self._run_pair(self._rho_all[:G * 512], self._rho_all[G * 512:], self._dx3_dev, stream)
+            for L, outs in ((self._L, (self._scr, Gv[0], Gv[1], Gv[2])), (self._L2, (Gv[3], self._scr, self._scr,
+                                                                                   self._scr))):
+                _lib.check(lib.omb_fmm_fields(ptr(L), ptr(self._my_cell_base), nown, *[ptr(o) for o in outs], sh),
+                           "omb_fmm_fields")
+            return
         for k, (rho, outs) in enumerate(((self._rho_all[:G * 512], (self._scr, Gv[0], Gv[1], Gv[2])),
                                          (self._rho_all[G * 512:], (Gv[3], self._scr, self._scr, self._scr)))):
             self._run(rho, self._dx3_dev, stream)
