@@ -382,12 +382,12 @@ __global__ void k_fmm_downward(const long long* parents, int np, const long long
 // cell masses: M[cell_entity(leaf, c)] = rho(leaf, c) * dx3(leaf); other components 0
 __global__ void k_fmm_masses(const double* rho, long long fstride_unused, const long long* cell_base, int L,
                              const double* dx3, double* M) {
+  // one thread per (cell, component): a leaf's cell records are consecutive, so the stores coalesce
   long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-  if (i >= (long long)L * 512) return;
-  int leaf = (int)(i / 512), c = (int)(i % 512);
-  double* m = M + (cell_base[leaf] + c) * NC;
-  m[0] = rho[i] * dx3[leaf];
-  for (int k = 1; k < NC; k++) m[k] = 0.0;
+  if (i >= (long long)L * 512 * NC) return;
+  long long r = i / NC;
+  int k = (int)(i - r * NC), leaf = (int)(r / 512), c = (int)(r % 512);
+  M[(cell_base[leaf] + c) * NC + k] = k == 0 ? rho[r] * dx3[leaf] : 0.0;
 }
 
 __global__ void k_fmm_fields(const double* L, const long long* cell_base, int nleaf, double* phi, double* gx,
@@ -635,7 +635,7 @@ int omb_fmm_direct(const long long* off, const unsigned long long* contrib, cons
 
 int omb_fmm_masses(const double* rho, const long long* cell_base, int nleaf, const double* dx3, double* M,
                    void* stream) {
-  long long n = (long long)nleaf * 512;
+  long long n = (long long)nleaf * 512 * NC;
   if (n == 0) return 0;
   k_fmm_masses<<<(unsigned)((n + 255) / 256), 256, 0, (cudaStream_t)stream>>>(rho, 0, cell_base, nleaf, dx3, M);
   cudaError_t e = cudaGetLastError();
