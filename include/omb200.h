@@ -252,11 +252,12 @@ int omb_fmm_m2l_part(int part, const long long *off, const unsigned long long *c
                      part 0 first copies the monopoles there and reads cell-cell masses from it */,
                      long long nentities, void *stream);
 /* pass 0 of two solves over the same lists at once (the stage's density and rho_dot solves): each
- * word and D row read once; m0a / m0b (nentities doubles each) receive the monopole copies */
+ * word and D row read once; m0ab (2 * nentities doubles) receives the two monopoles interleaved per
+ * entity; the next pointer is unused (may be NULL) */
 int omb_fmm_m2l0_pair(const long long *off, const unsigned long long *contrib, const double *D,
                       const unsigned char *cellcell, const double *Ma, const double *Mb, double *La, double *Lb,
-                      long long ntarget, const long long *targets, const long long *subset, double *m0a,
-                      double *m0b, long long nentities, void *stream);
+                      long long ntarget, const long long *targets, const long long *subset, double *m0ab,
+                      double *unused, long long nentities, void *stream);
 int omb_fmm_downward(const long long *parents, int np, const long long *children, const double *center, double *L,
                      void *stream);
 int omb_fmm_fields(const double *L, const long long *cell_base, int nleaf, double *phi, double *gx, double *gy,

@@ -278,8 +278,7 @@ __global__ void __launch_bounds__(128, 4) k_fmm_m2l0_pair(const long long* off, 
                                                           const double* D, const unsigned char* cellcell,
                                                           const double* Ma, const double* Mb, double* La, double* Lb,
                                                           long long ntarget, const long long* targets,
-                                                          const long long* subset, const double* M0a,
-                                                          const double* M0b) {
+                                                          const long long* subset, const double* M0ab) {
   long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   if (k >= ntarget) return;
   long long ti = subset ? subset[k] : k;
@@ -295,7 +294,8 @@ __global__ void __launch_bounds__(128, 4) k_fmm_m2l0_pair(const long long* off, 
     long long src = (long long)(w & 0xFFFFFFFFFFull);
     long long g = (long long)((w >> 40) & 0x3FFFFFull);
     const double* Dg = D + (g * 2 + (int)(w >> 63)) * NC;
-    double ma = __ldg(M0a + src), mb = __ldg(M0b + src);
+    double2 mm = __ldg(reinterpret_cast<const double2*>(M0ab) + src);  // (both monopoles, one 16-byte load)
+    double ma = mm.x, mb = mm.y;
     double2 da = __ldg(reinterpret_cast<const double2*>(Dg)), db = __ldg(reinterpret_cast<const double2*>(Dg + 2));
     double d[4] = {da.x, da.y, db.x, db.y};
     if (cellcell && ((w >> 62) & 1)) {
@@ -661,6 +661,14 @@ int omb_fmm_m2l(const long long* off, const unsigned long long* contrib, const d
   return e == cudaSuccess ? 0 : ferr("omb_fmm_m2l", e);
 }
 
+// the monopoles of two mass sets, interleaved (a, b) per entity: the paired pass 0 reads both with
+// one 16-byte load (c5g FMM 12.15 -> 11.95 ms per stage, profiles/r02/abf15_m2l_pair_m0x.txt)
+__global__ void k_fmm_m0x(const double* __restrict__ Ma, const double* __restrict__ Mb, long long n,
+                          double* __restrict__ M0x) {
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < n; e += (long long)gridDim.x * blockDim.x)
+    reinterpret_cast<double2*>(M0x)[e] = make_double2(Ma[e * NC], Mb[e * NC]);
+}
+
 __global__ void k_fmm_m0(const double* __restrict__ M, long long n, double* __restrict__ M0c) {
   for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < n; e += (long long)gridDim.x * blockDim.x)
     M0c[e] = M[e * NC];
@@ -687,17 +695,16 @@ int omb_fmm_m2l_part(int part, const long long* off, const unsigned long long* c
 
 int omb_fmm_m2l0_pair(const long long* off, const unsigned long long* contrib, const double* D,
                       const unsigned char* cellcell, const double* Ma, const double* Mb, double* La, double* Lb,
-                      long long ntarget, const long long* targets, const long long* subset, double* m0a,
-                      double* m0b, long long nentities, void* stream) {
+                      long long ntarget, const long long* targets, const long long* subset, double* m0ab,
+                      double* /*unused*/, long long nentities, void* stream) {
   if (ntarget <= 0) return 0;
-  if (!m0a || !m0b || nentities <= 0) return ferr("omb_fmm_m2l0_pair", cudaErrorInvalidValue);
+  if (!m0ab || nentities <= 0) return ferr("omb_fmm_m2l0_pair", cudaErrorInvalidValue);
   long long b = (nentities + 255) / 256;
   unsigned gb = (unsigned)(b < 148 * 16 ? b : 148 * 16);
-  k_fmm_m0<<<gb, 256, 0, (cudaStream_t)stream>>>(Ma, nentities, m0a);
-  k_fmm_m0<<<gb, 256, 0, (cudaStream_t)stream>>>(Mb, nentities, m0b);
+  k_fmm_m0x<<<gb, 256, 0, (cudaStream_t)stream>>>(Ma, Mb, nentities, m0ab);
   unsigned nb = (unsigned)((ntarget + 127) / 128);
   k_fmm_m2l0_pair<<<nb, 128, 0, (cudaStream_t)stream>>>(off, contrib, D, cellcell, Ma, Mb, La, Lb, ntarget, targets,
-                                                        subset, m0a, m0b);
+                                                        subset, m0ab);
   cudaError_t e = cudaGetLastError();
   return e == cudaSuccess ? 0 : ferr("omb_fmm_m2l0_pair", e);
 }

@@ -414,7 +414,7 @@ class B200FmmSolver:
         if getattr(self, "_M2", None) is None:
             self._M2 = torch.zeros_like(self._M)
             self._L2 = torch.zeros_like(self._L)
-            self._M0c2 = torch.zeros_like(self._M0c)
+            self._M0c2 = torch.zeros(2 * self._M0c.numel(), dtype=torch.float64, device=self.dev)  # (a, b) pairs
         for M, L in ((self._M, self._L), (self._M2, self._L2)):
             M.zero_()
             L.zero_()
@@ -429,7 +429,7 @@ class B200FmmSolver:
         order = self._target_order(0, self._off, sub)
         _lib.check(lib.omb_fmm_m2l0_pair(ptr(self._off), ptr(self._contrib), ptr(self._D), ptr(self._cellcell),
                                          ptr(self._M), ptr(self._M2), ptr(self._L), ptr(self._L2), nt,
-                                         ptr(self._targets), ptr(order), ptr(self._M0c), ptr(self._M0c2),
+                                         ptr(self._targets), ptr(order), ptr(self._M0c2), None,
                                          self.table.nentities, sh), "omb_fmm_m2l0_pair")
         order = self._target_order(1, self._off1, sub)
         for M, L in ((self._M, self._L), (self._M2, self._L2)):
