@@ -8,7 +8,7 @@ every cell from its 3-wide stencil alone -- same-level ghost cells are copies
 of the neighbour's interior -- so each n^3 leaf is run as (n/8)^3 BLOCKS of
 8^3: ``BlockTree`` is a view of the caller's tree whose leaves are those
 blocks, each block's ``subgrid.interior`` a numpy view into its leaf's
-interior (writes land in the caller's arrays).  What depends on the leaf size
+current interior (writes land in the caller's arrays).  What depends on the leaf size
 is restored per block through its LeafInfo flags (``blocks.block_flags``):
 
 * the positivity-fallback count: the reference counts every position of
@@ -40,7 +40,7 @@ def block_flags(b, nb):
 
 
 class BlockSubGrid:
-    __slots__ = ("n", "level", "origin", "dx", "interior", "leaf_origin", "offset")
+    __slots__ = ("n", "level", "origin", "dx", "leaf_origin", "offset", "_parent", "_sl")
 
     def __init__(self, parent, b, level):
         self.n = 8
@@ -50,8 +50,12 @@ class BlockSubGrid:
         self.offset = 8 * np.asarray(b)
         # cell centres as the leaf forms them: origin + dx * (8 b + i)
         self.origin = parent.origin + parent.dx * self.offset.astype(np.float64)
-        s = [slice(8 * int(x), 8 * int(x) + 8) for x in b]
-        self.interior = parent.interior[:, s[0], s[1], s[2]]
+        self._parent = parent
+        self._sl = (slice(None),) + tuple(slice(8 * int(x), 8 * int(x) + 8) for x in b)
+
+    @property
+    def interior(self):  # a view into the leaf's CURRENT array (a user may replace SubGrid.u)
+        return self._parent.interior[self._sl]
 
     @property
     def u(self):  # no padded array of its own: host transfers go through the interior views

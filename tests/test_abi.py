@@ -98,3 +98,25 @@ def test_no_cpu_fallback_without_gpu():
 
     with pytest.raises(NativeError):
         kernels.primitives(np.ones((6, 14, 14, 14)), 1.4, 1e-3)
+
+
+def test_block_ptrs_follow_replaced_leaf_arrays():
+    """The cached block pointer table of 16^3 leaves is revalidated by the identity of the
+    leaves' arrays: a leaf array a user replaces is picked up by the next pack."""
+    import octomini_host as mesh
+    from paper_2107_10987_b200 import _lib
+    from paper_2107_10987_b200.batch import LeafBatch
+
+    t = mesh.build_uniform_tree(1, 16, boundary="periodic")
+    rng = np.random.default_rng(1)
+    for lf in t.leaves():
+        lf.subgrid.u[...] = rng.normal(size=lf.subgrid.u.shape)
+    b = LeafBatch(t)
+    L = _lib.load()
+    p0 = b._leaf_ptrs(b.L).copy()
+    lf = t.sorted_leaves()[3]
+    lf.subgrid._u = lf.subgrid.u * 2.0  # a new array object
+    p1 = b._leaf_ptrs(b.L)
+    moved = p0 != p1
+    assert moved.sum() == 8 and moved[24:32].all()  # exactly that leaf's 8 blocks
+    assert np.array_equal(b.pack(lib=L), b.pack())
