@@ -403,12 +403,13 @@ class B200HydroStepper:
         self._up_ev.record()
 
     @_on_device
-    def download(self):
+    def download(self, checked=False):
         """Copy the device state back into the host leaves (the owned ones).  Mapped
         slab: one kernel writes them over PCIe, then the stream is synchronised.
-        Otherwise pipelined: chunk c is unpacked while chunk c+1 is in flight."""
+        Otherwise pipelined: chunk c is unpacked while chunk c+1 is in flight.
+        checked: the slab views were revalidated since the last user code ran."""
         b = self.batch
-        if self._mapped is not None:
+        if self._mapped is not None and not checked:
             self._mapped_check()
         if self._mapped is not None and self._gather_frac is None:
             m = self._mapped
@@ -427,7 +428,7 @@ class B200HydroStepper:
         self._pinned.copy_(self._buf[self._state])
         b.unpack(self._pinned.numpy().reshape(6, b.L + b.nvirtual, 8, 8, 8))
 
-    def _download_tail(self):
+    def _download_tail(self, checked=False):
         b = self.batch
         t = self._tail
         if self._mapped is not None and self._gather_frac is None:
@@ -449,11 +450,11 @@ class B200HydroStepper:
             side.synchronize()
             torch.cuda.current_stream(self.dev).synchronize()
             return
-        if self._mapped is not None:
+        if self._mapped is not None and not checked:
             self._mapped_check()
         ptrs = self._host_ptrs()
         if ptrs is None:
-            self.download()
+            self.download(checked=True)
             return
         if self._pinned is None:
             self._pinned = torch.zeros(6 * b.fstride, dtype=torch.float64).pin_memory()
@@ -730,12 +731,14 @@ class B200HydroStepper:
     def rk3_step(self, dt):
         """One SSP-RK3 step (step.py:94-102) on the device."""
         if self.host_sync and not self._fresh:
-            self.upload()
+            self.upload()  # (revalidates the slab views)
+        elif self.host_sync and self._mapped is not None:
+            self._mapped_check()  # leaf arrays a user replaced since cfl_dt's upload
         self._fresh = False
         tail = self.host_sync and self._tail is not None
         start, outs = self.launch_step(dt, tail=tail)
         if tail:
-            self._download_tail()  # the result, copied back while its last stage runs
+            self._download_tail(checked=True)  # the result, copied back while its last stage runs
         self._reduce_stats()
         acc = self._acc.cpu().numpy()
         amax = acc[:3].view(np.float64)
@@ -759,5 +762,5 @@ class B200HydroStepper:
             u_prev = outs[s]
         self.stats = stats
         if self.host_sync and not tail:
-            self.download()
+            self.download(checked=True)
         return stats
